@@ -1,0 +1,374 @@
+"""TEST INFRASTRUCTURE ONLY -- float64 direct-sum oracle of the paper's discrete A and A*.
+
+Imported only by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline/reference legs.
+Shares no code with paper_2510_24687_b200 (the CUDA path); the only common module is
+``synth`` (input generators).
+
+What it computes.  Every FFT of the paper's
+Algorithm 1 is written as the DFT it stands for -- a dense matrix of
+roots of unity with exact integer index reduction, applied by BLAS -- so a reader can
+check each line against the paper:
+
+  D1  Alg.1 steps 1-2, F_2D convention P:L256-260:
+      F[p,q] = (h^2/2pi) sum_{iy,ix} f[iy,ix] exp(-2 pi i [p(ix-n/2) + q(iy-n/2)]/N)
+  D2  Alg.1 step 3 (bilinear):
+      P[j,l] = bilinear interpolation of F at (u,v) = (lambda_j/dxi)(cos phi_l, sin phi_l)
+  D3  Alg.1 step 4, E:eq3:   fhat_k(lambda_j) = (1/n_phi) sum_l P[j,l] e^{-i k phi_l}
+  D4  E:eq2 + quadrature:    H_k(lambda_j) = i^|k| w_j dlam lambda_j J_|k|(R lambda_j) fhat_k
+  D5  Alg.1 step 5, E:inverse_cos_tr:  G_k(t_m) = sum_j H_k(lambda_j) cos(c lambda_j t_m)
+  D6  Alg.1 step 6, E:FourSerForg:     g(t_m, phi_l) = sum_{k=-K}^{K-1} G_k(t_m) e^{i k phi_l}
+  D7  Alg.1 step 7: restriction to the detectors, real part.
+
+The adjoint is the exact conjugate-transposed chain (reading G4), scaled to the L2 inner
+products of eqn:innerProducts (reading G18):
+  A* g = omega * Re( D1^H D2^T D3^H D4^H D5^T D6^H D7^T g ),  omega = dt * 2 pi R / (n_ring h^2),
+which is the discrete counterpart of E:adjoint and follows Alg. 2's step
+order with step 5's interpolation replaced by the transpose of Alg. 1 step 3.
+
+Pins (tests/test_oracle_*.py): P1 numpy.fft + Gaussian closed form; P2 bilinear
+exactness; P3 pure harmonics; P4 Bessel via Jacobi-Anger (E:Anger) and the J0 zero;
+P5 scipy DCT-I; P6 Im A f == 0; P7 rotation/reflection equivariance; P8 delta at the
+origin; (1) continuous Gaussian solution by 1-D quadrature; (2) brute-force E:kwave at
+n=32; (3) adjoint identity and dense transpose.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+from scipy import special
+
+ANGLE_TOL = 1e-9
+
+
+# ----------------------------------------------------------------------------- D0
+@dataclass(frozen=True)
+class Constants:
+    """D0 constants (readings G1, G2, G6, G7, G8, G9, G11, G15)."""
+    n: int
+    n_det: int
+    n_t: int
+    R: float
+    c: float
+    T: float
+    h: float          # pixel pitch 2/n (G1)
+    T_new: float      # model time max(2cT, 6) rounded up to M*c*dt (G7)
+    L: float          # extended half-width, power of two >= T_new0 + 2 (G6)
+    N: int            # Cartesian FFT size 2L/h
+    dxi: float        # Cartesian frequency pitch pi/L
+    dt: float         # time step T/n_t (G2)
+    M: int            # DCT-I length T_new/(c dt)
+    dlam: float       # radial pitch pi/T_new (G7)
+    J: int            # last radial index floor(lambda_max/dlam), lambda_max = pi/h (G8)
+    wJ: float         # trapezoid weight of the last node (1/2 if J dlam == lambda_max)
+    n_ring: int       # canonical ring the detectors sit on (G3)
+    ring: tuple       # ring index r_d of each detector
+    K: int            # n_phi/2, harmonics k in [-K, K-1] (G11)
+    omega: float      # L2 adjoint scale dt * 2 pi R / (n_ring h^2) (G18, G20)
+
+    @property
+    def n_phi(self) -> int:
+        return self.n_ring
+
+    @property
+    def NL(self) -> int:
+        return self.J + 1
+
+
+def infer_ring(angles: np.ndarray, n_det: int) -> tuple[int, np.ndarray]:
+    """Smallest n_ring (multiple of 4, >= n_det) with every angle on 2 pi r / n_ring (G3)."""
+    a = np.asarray(angles, dtype=np.float64)
+    start = max(4, 4 * ((n_det + 3) // 4))
+    for n_ring in range(start, 65537, 4):
+        x = a * n_ring / (2.0 * np.pi)
+        r = np.rint(x)
+        if np.all(np.abs(x - r) * (2.0 * np.pi / n_ring) < ANGLE_TOL):
+            ring = np.mod(r.astype(np.int64), n_ring)
+            if len(np.unique(ring)) != len(ring):
+                raise ValueError("detectors are not distinct ring positions")
+            return n_ring, ring
+    raise ValueError("detector angles are not on a canonical uniform ring")
+
+
+def derive(n, n_det, n_t, R, c, T, angles, L_override: float | None = None) -> Constants:
+    """D0: every constant of the discretisation, in float64.
+
+    ``L_override`` exists only for the oracle-only refinement study of check (1)."""
+    if n < 8 or n % 2:
+        raise ValueError("n must be even and >= 8")
+    h = 2.0 / n
+    T_new0 = max(2.0 * c * T, 6.0)
+    L = float(2 ** math.ceil(math.log2(T_new0 + 2.0) - 1e-12))   # P:L531-533, G6
+    if L_override is not None:
+        L = float(L_override)
+    N = int(round(2 * L / h))
+    dxi = math.pi / L                                            # 2 pi / (N h)
+    dt = T / n_t                                                 # t_m = (m+1) dt, G2
+    M = int(math.ceil(T_new0 / (c * dt) - 1e-9))
+    T_new = M * c * dt
+    dlam = math.pi / T_new                                       # G7
+    lam_max = math.pi / h                                        # G8
+    J = int(math.floor(lam_max / dlam + 1e-9))
+    wJ = 0.5 if abs(J * dlam - lam_max) <= 1e-9 * lam_max else 1.0
+    n_ring, ring = infer_ring(np.asarray(angles), n_det)
+    K = n_ring // 2
+    omega = dt * 2.0 * math.pi * R / (n_ring * h * h)
+    return Constants(n, n_det, n_t, R, c, T, h, T_new, L, N, dxi, dt, M, dlam, J, wJ,
+                     n_ring, tuple(int(r) for r in ring), K, omega)
+
+
+def derive_geom(geom, **kw) -> Constants:
+    return derive(geom.n, geom.n_det, geom.n_t, geom.R, geom.c, geom.T, geom.angles_array(), **kw)
+
+
+# ----------------------------------------------------------------------------- helpers
+@lru_cache(maxsize=None)
+def _roots(Nr: int) -> np.ndarray:
+    """exp(-2 pi i r / Nr) for r = 0..Nr-1 in float64 (index-reduced twiddle table)."""
+    r = np.arange(Nr, dtype=np.float64)
+    return np.cos(2 * np.pi * r / Nr) - 1j * np.sin(2 * np.pi * r / Nr)
+
+
+def _dft_matrix(freqs: np.ndarray, pos: np.ndarray, Nr: int, sign: int = -1) -> np.ndarray:
+    """E[a, b] = exp(sign * 2 pi i freqs[a] * pos[b] / Nr), exponent reduced mod Nr in integers."""
+    idx = np.mod(np.outer(freqs.astype(np.int64), pos.astype(np.int64)), Nr)
+    E = _roots(Nr)[idx]
+    return E if sign < 0 else np.conj(E)
+
+
+def _freqs(N: int) -> np.ndarray:
+    return np.arange(-N // 2, N // 2, dtype=np.int64)
+
+
+def _unit_circle(n_phi: int) -> tuple[np.ndarray, np.ndarray]:
+    """(cos phi_l, sin phi_l), phi_l = 2 pi l / n_phi, quadrant-reduced so that multiples of
+    pi/2 are exactly 0 and +-1."""
+    l = np.arange(n_phi)
+    if n_phi % 4 == 0:
+        Q = n_phi // 4
+        qd, rem = l // Q, l % Q
+        base = 2 * np.pi * rem / n_phi
+        c0, s0 = np.cos(base), np.sin(base)
+        cs = np.choose(qd, [c0, -s0, -c0, s0])
+        sn = np.choose(qd, [s0, c0, -s0, -c0])
+        return cs, sn
+    return np.cos(2 * np.pi * l / n_phi), np.sin(2 * np.pi * l / n_phi)
+
+
+def _i_pow(k: np.ndarray) -> np.ndarray:
+    """i^|k| exactly."""
+    return np.array([1, 1j, -1, -1j])[np.abs(k) % 4]
+
+
+# ----------------------------------------------------------------------------- D1
+def cartesian_spectrum(f: np.ndarray, C: Constants) -> np.ndarray:
+    """D1, Alg. 1 steps 1-2 with the F_2D convention of P:L256-260.
+
+    Returns F[p + N/2, q + N/2] for p, q in [-N/2, N/2): p pairs with x (column index ix),
+    q with y (row index iy).  Zero-extension to the box [-L, L]^2 is implicit: the sum runs
+    over the image nodes only."""
+    n, N = C.n, C.N
+    pos = np.arange(n) - n // 2
+    E = _dft_matrix(_freqs(N), pos, N)              # E[p, i] = exp(-2 pi i p (i - n/2)/N)
+    scale = C.h * C.h / (2 * np.pi)
+    return scale * (E @ (np.asarray(f, np.float64).T @ E.T))   # F[p,q] = s sum E[p,ix] f[iy,ix] E[q,iy]
+
+
+def cartesian_spectrum_adjoint(Ft: np.ndarray, C: Constants) -> np.ndarray:
+    """D1^H: f~[iy, ix] = (h^2/2pi) sum_{p,q} Ft[p,q] exp(+2 pi i [p(ix-n/2) + q(iy-n/2)]/N)."""
+    n, N = C.n, C.N
+    pos = np.arange(n) - n // 2
+    E = _dft_matrix(_freqs(N), pos, N)
+    scale = C.h * C.h / (2 * np.pi)
+    G = E.conj().T @ Ft @ E.conj()                   # G[ix, iy]
+    return scale * G.T
+
+
+# ----------------------------------------------------------------------------- D2
+def polar_nodes(C: Constants):
+    """Polar nodes in Cartesian index units: (u, v) = (lambda_j / dxi)(cos phi_l, sin phi_l)."""
+    j = np.arange(C.J + 1, dtype=np.float64)
+    rho = (j * C.L) / C.T_new                         # lambda_j / dxi = j dlam / dxi
+    cs, sn = _unit_circle(C.n_phi)
+    return rho[:, None] * cs[None, :], rho[:, None] * sn[None, :]
+
+
+def polar_cells(C: Constants):
+    """Bilinear cells of the polar nodes (j, l), j in [0, J], l in [0, n_phi):
+    u = (lambda_j/dxi) cos phi_l, v = (lambda_j/dxi) sin phi_l, p0 = floor(u), alpha = u - p0,
+    q0 = floor(v), beta = v - q0 (reading G13)."""
+    u, v = polar_nodes(C)
+    p0 = np.floor(u)
+    q0 = np.floor(v)
+    return p0.astype(np.int64), q0.astype(np.int64), u - p0, v - q0
+
+
+def polar_resample(F: np.ndarray, C: Constants) -> np.ndarray:
+    """D2, Alg. 1 step 3: P[j, l] on the polar grid, F periodic mod N."""
+    N = C.N
+    p0, q0, a, b = polar_cells(C)
+    ip0 = np.mod(p0 + N // 2, N)
+    ip1 = np.mod(p0 + 1 + N // 2, N)
+    iq0 = np.mod(q0 + N // 2, N)
+    iq1 = np.mod(q0 + 1 + N // 2, N)
+    return ((1 - a) * (1 - b) * F[ip0, iq0] + a * (1 - b) * F[ip1, iq0]
+            + (1 - a) * b * F[ip0, iq1] + a * b * F[ip1, iq1])
+
+
+def polar_resample_transpose(Pt: np.ndarray, C: Constants) -> np.ndarray:
+    """D2^T: scatter-add of Pt[j, l] into the Cartesian grid with D2's weights."""
+    N = C.N
+    p0, q0, a, b = polar_cells(C)
+    ip0 = np.mod(p0 + N // 2, N)
+    ip1 = np.mod(p0 + 1 + N // 2, N)
+    iq0 = np.mod(q0 + N // 2, N)
+    iq1 = np.mod(q0 + 1 + N // 2, N)
+    Ft = np.zeros((N, N), dtype=np.complex128)
+    np.add.at(Ft, (ip0, iq0), (1 - a) * (1 - b) * Pt)
+    np.add.at(Ft, (ip1, iq0), a * (1 - b) * Pt)
+    np.add.at(Ft, (ip0, iq1), (1 - a) * b * Pt)
+    np.add.at(Ft, (ip1, iq1), a * b * Pt)
+    return Ft
+
+
+# ----------------------------------------------------------------------------- D3 / D6
+def _harmonics(C: Constants) -> np.ndarray:
+    return np.arange(-C.K, C.K, dtype=np.int64)
+
+
+def angular_coefficients(P: np.ndarray, C: Constants) -> np.ndarray:
+    """D3, E:eq3: fk[j, k+K] = (1/n_phi) sum_l P[j, l] exp(-2 pi i k l / n_phi)."""
+    W = _dft_matrix(np.arange(C.n_phi), _harmonics(C), C.n_phi)      # W[l, k]
+    return (P @ W) / C.n_phi
+
+
+def angular_coefficients_adjoint(fkt: np.ndarray, C: Constants) -> np.ndarray:
+    """D3^H: Pt[j, l] = (1/n_phi) sum_k fkt[j, k] exp(+2 pi i k l / n_phi)."""
+    W = _dft_matrix(np.arange(C.n_phi), _harmonics(C), C.n_phi)
+    return (fkt @ W.conj().T) / C.n_phi
+
+
+def synthesis(G: np.ndarray, C: Constants) -> np.ndarray:
+    """D6, E:FourSerForg: g[m, l] = sum_{k=-K}^{K-1} G[m, k] exp(+2 pi i k l / n_phi)."""
+    S = _dft_matrix(_harmonics(C), np.arange(C.n_phi), C.n_phi, sign=+1)   # S[k, l]
+    return G @ S
+
+
+def synthesis_adjoint(gfull: np.ndarray, C: Constants) -> np.ndarray:
+    """D6^H: Gt[m, k] = sum_l gfull[m, l] exp(-2 pi i k l / n_phi)."""
+    S = _dft_matrix(_harmonics(C), np.arange(C.n_phi), C.n_phi, sign=+1)
+    return gfull @ S.conj().T
+
+
+# ----------------------------------------------------------------------------- D4
+@lru_cache(maxsize=8)
+def _bessel(K: int, J: int, dlam: float, R: float) -> np.ndarray:
+    lam = np.arange(J + 1) * dlam
+    return special.jv(np.arange(K + 1)[:, None], R * lam[None, :])     # [|k|, j]
+
+
+def multiplier_table(C: Constants) -> np.ndarray:
+    """m[|k|, j] = w_j dlam lambda_j J_|k|(R lambda_j), |k| = 0..K (E:eq2 P:L463-466 with the
+    trapezoid rule in lambda, readings G9, G17); real float64."""
+    j = np.arange(C.J + 1)
+    lam = j * C.dlam
+    w = np.ones(C.J + 1)
+    w[0] = 0.5
+    w[C.J] = C.wJ if C.J > 0 else w[C.J]
+    return (w * C.dlam * lam)[None, :] * _bessel(C.K, C.J, C.dlam, C.R)
+
+
+def apply_multiplier(fk: np.ndarray, C: Constants, conj: bool = False) -> np.ndarray:
+    """D4: H[j, k] = i^|k| m[|k|, j] fk[j, k]  (conj=True: D4^H with (-i)^|k|, E:Four_coef_u)."""
+    k = _harmonics(C)
+    m = multiplier_table(C)[np.abs(k), :].T                              # [j, k]
+    ph = _i_pow(k)
+    if conj:
+        ph = np.conj(ph)
+    return fk * (m * ph[None, :])
+
+
+# ----------------------------------------------------------------------------- D5
+def _cos_matrix(C: Constants) -> np.ndarray:
+    """cosm[m, j] = cos(c lambda_j t_m) = cos(pi j (m+1) / M), argument reduced mod 2M."""
+    m1 = np.arange(1, C.n_t + 1, dtype=np.int64)
+    j = np.arange(C.J + 1, dtype=np.int64)
+    r = np.mod(np.outer(m1, j), 2 * C.M)
+    table = np.cos(np.pi * np.arange(2 * C.M) / C.M)
+    return table[r]
+
+
+def cosine_transform(H: np.ndarray, C: Constants) -> np.ndarray:
+    """D5, E:inverse_cos_tr: G[m, k] = sum_j cos(c lambda_j t_m) H[j, k]."""
+    return _cos_matrix(C) @ H
+
+
+def cosine_transform_adjoint(Gt: np.ndarray, C: Constants) -> np.ndarray:
+    """D5^T: Ht[j, k] = sum_m cos(c lambda_j t_m) Gt[m, k]."""
+    return _cos_matrix(C).T @ Gt
+
+
+# ----------------------------------------------------------------------------- D7
+def restrict(gfull: np.ndarray, C: Constants, check: bool = True) -> np.ndarray:
+    """D7, Alg. 1 step 7: g[m, d] = Re g(t_m, phi_{r_d}); Im must vanish (G19)."""
+    sub = gfull[:, np.asarray(C.ring)]
+    if check:
+        scale = max(np.abs(sub.real).max(), 1e-300)
+        im = np.abs(sub.imag).max()
+        if im > 1e-10 * scale:
+            raise AssertionError(f"imaginary residue {im:.3e} vs {scale:.3e} (G19)")
+    return sub.real
+
+
+def restrict_adjoint(g: np.ndarray, C: Constants) -> np.ndarray:
+    """D7^T: zero-extend detector data to the full ring (Alg. 2 step 1)."""
+    out = np.zeros((g.shape[0], C.n_phi), dtype=np.complex128)
+    out[:, np.asarray(C.ring)] = g
+    return out
+
+
+# ----------------------------------------------------------------------------- chains
+def forward_stages(f: np.ndarray, C: Constants) -> dict:
+    """Algorithm 1 on one image, keeping every intermediate (full layout)."""
+    st = {}
+    st["F"] = cartesian_spectrum(f, C)             # steps 1-2
+    st["P"] = polar_resample(st["F"], C)           # step 3
+    st["fk"] = angular_coefficients(st["P"], C)    # step 4
+    st["H"] = apply_multiplier(st["fk"], C)        # E:eq2 multiplier
+    st["G"] = cosine_transform(st["H"], C)         # step 5
+    st["gfull"] = synthesis(st["G"], C)            # step 6
+    st["g"] = restrict(st["gfull"], C)             # step 7
+    return st
+
+
+def adjoint_stages(g: np.ndarray, C: Constants) -> dict:
+    """Exact transpose of Algorithm 1, in Algorithm 2's step order."""
+    st = {}
+    st["gfull"] = restrict_adjoint(np.asarray(g, np.float64), C)     # step 1
+    st["G"] = synthesis_adjoint(st["gfull"], C)                       # step 2
+    st["Hc"] = cosine_transform_adjoint(st["G"], C)                   # step 3 (cos sums)
+    st["H"] = apply_multiplier(st["Hc"], C, conj=True)                # step 3 ((-i)^|k| J)
+    st["P"] = angular_coefficients_adjoint(st["H"], C)                # step 4
+    st["F"] = polar_resample_transpose(st["P"], C)                    # step 5 (transpose)
+    st["u"] = cartesian_spectrum_adjoint(st["F"], C)                  # step 6
+    st["f"] = C.omega * st["u"].real                                  # step 7, omega (G18)
+    return st
+
+
+def _batched(fn, x, C):
+    x = np.asarray(x)
+    if x.ndim == 2:
+        return fn(x, C)
+    return np.stack([fn(xi, C) for xi in x])
+
+
+def forward(f: np.ndarray, C: Constants) -> np.ndarray:
+    """A f for one image [n, n] or a batch [B, n, n]; returns [.., n_t, n_det] float64."""
+    return _batched(lambda x, c: forward_stages(x, c)["g"], f, C)
+
+
+def adjoint(g: np.ndarray, C: Constants) -> np.ndarray:
+    """A* g for [n_t, n_det] or [B, n_t, n_det]; returns [.., n, n] float64."""
+    return _batched(lambda x, c: adjoint_stages(x, c)["f"], g, C)
