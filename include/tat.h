@@ -1,0 +1,134 @@
+/*
+ * tat.h -- C ABI of libtat: the fast O(n^2 log n) 2-D circular-geometry wave operators
+ * of arxiv 2510.24687 ("PAT/TAT"), forward A and exact adjoint A*, on one B200 (sm_100a).
+ *
+ * Operation (§3.1 Algorithm 1; §3.2 Algorithm 2):
+ *   A  : initial pressure f on an n x n grid  ->  traces g(t_m, z_d) at detectors z_d on the
+ *        circle of radius R (E:green_conv, L210-216; discretised as DESIGN.md "D0-D7").
+ *   A* : the exact transpose of the discrete A under the L2 inner products of
+ *        eqn:innerProducts (L217-222):  A* = omega * A^T,
+ *        omega = dt * 2 pi R / (n_ring * h^2)  (readings G4, G18, G20).
+ *
+ * Conventions:
+ *   - f[b][iy][ix] (float32, row-major, contiguous) is the sample at
+ *       x = (ix - n/2) h, y = (iy - n/2) h, h = 2/n          (reading G1)
+ *   - g[b][m][d] (float32, row-major, contiguous) is the trace at t_m = (m+1) T / n_t
+ *       (reading G2) and detector d, in the caller's detector_angles order.
+ *   - detector_angles are radians, counter-clockwise from +x, and must lie on a canonical
+ *       uniform ring theta = 2 pi r / n_ring (reading G3); n_ring is inferred as the smallest
+ *       multiple of 4 >= n_det that fits every angle within 1e-9 rad.
+ *   - Every call processes exactly `batch` images (the batch the plan was created for).
+ *
+ * Ownership: the plan owns its device tables and its workspace (allocated at create time).
+ * The caller owns f, g and the stream.  tat_forward / tat_adjoint only ENQUEUE kernels on
+ * `stream`: no host synchronisation, no allocation, no memcpy; asynchronous faults surface
+ * at the caller's next synchronisation.  Calls on one plan must be stream-ordered (the
+ * workspace is shared); distinct plans are independent.
+ *
+ * Errors: arguments are validated on the host before any launch; a failed call writes
+ * nothing.  The thread-local message of the last failure is tat_last_error().
+ * NaN/Inf in f or g propagate (no scan pass).
+ */
+#ifndef TAT_H
+#define TAT_H
+
+#include <stddef.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tat_plan tat_plan;   /* opaque */
+
+typedef enum {
+  TAT_OK = 0,
+  TAT_ERR_INVALID_ARGUMENT = 1,     /* null pointer, n < 8 / odd / not a power of two, n_det < 1,
+                                       n_t < 1, batch < 1, R, c, T not finite > 0, non-finite angle */
+  TAT_ERR_UNSUPPORTED_GEOMETRY = 2, /* angles not on a canonical ring (n_ring % 4 == 0,
+                                       n_ring >= n_det, distinct ring positions), or a size the
+                                       sm_100a kernels do not implement (see tat_last_error()) */
+  TAT_ERR_OUT_OF_MEMORY = 3,
+  TAT_ERR_CUDA = 4                  /* CUDA API or launch failure */
+} tat_status;
+
+/* Build a plan (the Bessel values J_|k|(R lambda_j) are
+ * precomputed; here in float64 on the host by Miller's downward recurrence, then stored as
+ * float32 multiplier tables on the device together with the bilinear resampling tables).
+ *   plan            out: *plan receives the new plan (unchanged on failure)
+ *   n               image side (even power of two; kernels implement 32 <= n <= 1024)
+ *   n_det, n_t      detectors and time samples
+ *   R, c, T         ring radius, speed of sound, time horizon (t in (0, T])
+ *   batch           images per call
+ *   detector_angles host array of n_det float64 radians (copied; caller keeps ownership)
+ * Synchronous (uses the legacy default stream for uploads).  Errors as above. */
+tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t,
+                           double R, double c, double T, int batch,
+                           const double* detector_angles);
+
+/* g = A f  (Algorithm 1).  f: device [batch][n][n] float32; g: device [batch][n_t][n_det]
+ * float32.  Enqueued on `stream`.  TAT_ERR_INVALID_ARGUMENT on null plan/pointers. */
+tat_status tat_forward(const tat_plan* plan, const float* f, float* g, cudaStream_t stream);
+
+/* f = A* g  (Algorithm 2 as the exact transposed chain).  g: device [batch][n_t][n_det];
+ * f: device [batch][n][n].  Enqueued on `stream`. */
+tat_status tat_adjoint(const tat_plan* plan, const float* g, float* f, cudaStream_t stream);
+
+/* Host-buffer variants (end-to-end path): copy the host input into plan-owned device staging
+ * (cudaMemcpyAsync on `stream`), run the operator, copy the result back to the host buffer.
+ * Stream-ordered: the caller synchronises `stream` before reading the output.  Pinned host
+ * memory gives asynchronous copies; pageable memory is staged by the driver. */
+tat_status tat_forward_host(const tat_plan* plan, const float* f_host, float* g_host,
+                            cudaStream_t stream);
+tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_host,
+                            cudaStream_t stream);
+
+/* NULL-safe.  The caller must ensure no work using the plan is in flight. */
+void tat_plan_destroy(tat_plan* plan);
+
+/* Introspection: the plan's derived constants (D0) and table sizes. */
+typedef struct {
+  int n, n_det, n_t, batch;
+  int N;            /* Cartesian FFT size 2L/h */
+  int J;            /* last radial index; N_lambda = J + 1 */
+  int M;            /* DCT-I length; the lambda->t transform runs as a 2M-point FFT */
+  int n_ring;       /* canonical ring size = n_phi */
+  int K;            /* n_ring / 2; harmonics k in [-K, K-1] */
+  int n_nodes_half; /* polar nodes in the half-plane store (n_ring/2 * (J+1)) */
+  double L, T_new, dxi, dlam, omega, dt, h, wJ;
+  size_t workspace_bytes, table_bytes;
+  int launches_forward, launches_adjoint;
+} tat_plan_info_t;
+
+/* ring_index: optional host int array of n_det receiving the ring position r_d of each
+ * detector (or NULL). */
+tat_status tat_plan_info(const tat_plan* plan, tat_plan_info_t* out, int* ring_index);
+
+/* Host-only (no device access): validate the arguments exactly as tat_plan_create does and
+ * report the derived constants.  Returns TAT_ERR_UNSUPPORTED_GEOMETRY (with `out` filled)
+ * when the geometry is valid but outside what the sm_100a kernels implement. */
+tat_status tat_plan_derive(int n, int n_det, int n_t, double R, double c, double T, int batch,
+                           const double* detector_angles, tat_plan_info_t* out, int* ring_index);
+
+/* Host-only: the float32 multiplier table the plan uploads, row-major [K+1][J+1]:
+ *   m'[k][j] = (h^2/2pi) (1/n_ring) w_j dlam lambda_j J_k(R lambda_j)
+ * (E:eq2 P:L463-466 with the trapezoid rule in lambda and the 1/n_phi of E:eq3 and the
+ * h^2/2pi of the F_2D convention folded in).  out_len is in floats. */
+tat_status tat_plan_host_multiplier(int n, int n_det, int n_t, double R, double c, double T,
+                                    const double* detector_angles, float* out, size_t out_len);
+
+/* Optional per-stage device timing (CUDA events recorded between the kernels of each call on
+ * the call's stream).  tat_profile_begin arms recording for up to max_calls calls;
+ * tat_profile_end synchronises the events and writes the summed milliseconds per stage:
+ * stage_ms[0..4] = forward K1..K5, stage_ms[5..9] = adjoint K5T..K1T (10 floats), and the
+ * number of forward / adjoint calls recorded.  Not thread-safe with concurrent calls. */
+tat_status tat_profile_begin(tat_plan* plan, int max_calls);
+tat_status tat_profile_end(tat_plan* plan, float* stage_ms, int* n_forward, int* n_adjoint);
+
+const char* tat_status_string(tat_status s);
+const char* tat_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAT_H */

@@ -1,0 +1,282 @@
+// Host plan builder (float64): constants, Bessel multiplier, resampling tables.
+//
+// PAPER.md L571-574 / L698-701: "additional time saving is achieved by pre-computing and
+// storing the values of the Bessel functions J_|k|(lambda) for the values of k from 0 to half
+// the number of discretization points in theta, and for all values of lambda".  This file
+// builds those tables (and the bilinear cells of Alg. 1 step 3) once per
+// geometry.  It shares no code with oracle/ (which uses scipy for J and dense DFTs).
+#include "tat_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+namespace tat {
+
+static const double kPi = 3.14159265358979323846264338327950288;
+
+static bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
+
+static std::string fmt(const char* f, double a = 0, double b = 0) {
+  char buf[256];
+  snprintf(buf, sizeof buf, f, a, b);
+  return buf;
+}
+
+// D0: every constant in float64, mirroring the paper's grid rules.
+std::string derive_consts(int n, int n_det, int n_t, double R, double c, double T, int batch,
+                          const double* angles, Consts& C, std::vector<int>& ring_out,
+                          int& code) {
+  code = 1;
+  if (!angles) return "detector_angles is NULL";
+  if (n < 8 || (n & 1) || !is_pow2(n)) return fmt("n=%g must be an even power of two >= 8", n);
+  if (n_det < 1) return "n_det must be >= 1";
+  if (n_t < 1) return "n_t must be >= 1";
+  if (batch < 1) return "batch must be >= 1";
+  if (!(std::isfinite(R) && R > 0)) return "R must be finite and > 0";
+  if (!(std::isfinite(c) && c > 0)) return "c must be finite and > 0";
+  if (!(std::isfinite(T) && T > 0)) return "T must be finite and > 0";
+  for (int d = 0; d < n_det; ++d)
+    if (!std::isfinite(angles[d])) return fmt("detector angle %g is not finite", d);
+
+  C = Consts();
+  C.n = n; C.n_det = n_det; C.n_t = n_t; C.batch = batch; C.R = R; C.c = c; C.T = T;
+  C.h = 2.0 / n;
+  C.T_new0 = std::max(2.0 * c * T, 6.0);
+  C.Lbox = std::pow(2.0, std::ceil(std::log2(C.T_new0 + 2.0) - 1e-12));
+  C.N = (int)std::lround(2.0 * C.Lbox / C.h);
+  C.Lres = C.N / n;
+  C.dxi = kPi / C.Lbox;
+  C.dt = T / n_t;
+  double Mf = std::ceil(C.T_new0 / (c * C.dt) - 1e-9);
+  if (Mf > 1e8) { code = 2; return "T_new / (c dt) too large"; }
+  C.M = (int)Mf;
+  C.T_new = C.M * c * C.dt;
+  C.dlam = kPi / C.T_new;
+  C.lam_max = kPi / C.h;
+  C.J = (int)std::floor(C.lam_max / C.dlam + 1e-9);
+  C.NL = C.J + 1;
+  C.wJ = (std::fabs(C.J * C.dlam - C.lam_max) <= 1e-9 * C.lam_max) ? 0.5 : 1.0;
+
+  // canonical ring (reading G3): smallest multiple of 4 >= n_det holding every angle
+  code = 2;
+  int start = std::max(4, 4 * ((n_det + 3) / 4));
+  std::vector<int> ring(n_det);
+  int n_ring = 0;
+  for (int cand = start; cand <= 65536 && !n_ring; cand += 4) {
+    bool ok = true;
+    for (int d = 0; d < n_det && ok; ++d) {
+      double x = angles[d] * cand / (2.0 * kPi);
+      double r = std::nearbyint(x);
+      if (std::fabs(x - r) * (2.0 * kPi / cand) >= 1e-9) ok = false;
+      else {
+        long ri = (long)r % cand;
+        if (ri < 0) ri += cand;
+        ring[d] = (int)ri;
+      }
+    }
+    if (ok) n_ring = cand;
+  }
+  if (!n_ring) return "detector angles are not on a canonical uniform ring 2*pi*r/n_ring";
+  {
+    std::vector<int> s(ring);
+    std::sort(s.begin(), s.end());
+    if (std::adjacent_find(s.begin(), s.end()) != s.end())
+      return "two detectors share one ring position";
+  }
+  C.n_ring = n_ring;
+  ring_out = ring;
+  C.K = n_ring / 2;
+  C.Kp = C.K + 1;
+  C.half = n_ring / 2;
+  C.ncols = C.N / 2 + 1;
+  C.omega = C.dt * 2.0 * kPi * R / (n_ring * C.h * C.h);
+  code = 0;
+  return "";
+}
+
+static bool smooth23(long v) {   // v = 2^a 3^b (radix-4/2/3 Stockham passes)
+  while (v % 3 == 0) v /= 3;
+  return is_pow2(v);
+}
+
+std::string gpu_support(const Consts& C) {
+  if (C.n < 32 || C.n > 1024) return fmt("n=%g outside the implemented range [32, 1024]", C.n);
+  if (!is_pow2(C.Lres) || C.Lres < 2 || C.Lres > 16)
+    return fmt("oversampling N/n=%g unsupported", C.Lres);
+  if (!is_pow2(C.n_ring) || C.n_ring < 8 || C.n_ring > 2048)
+    return fmt("n_ring=%g: kernels implement powers of two in [8, 2048]", C.n_ring);
+  if (!smooth23(2L * C.M)) return fmt("2M=%g is not of the form 2^a 3^b", 2.0 * C.M);
+  if (C.NL > 2 * C.M) return "J+1 > 2M (time step coarser than twice the pixel pitch)";
+  if (C.n_t > 2 * C.M - 1) return "n_t too large for the DCT length";
+  if (max_smem_needed(C) > 227 * 1024) return fmt("shared memory need %g KB > 227 KB",
+                                                  max_smem_needed(C) / 1024.0);
+  return "";
+}
+
+// Miller's downward recurrence for J_0..J_kmax(x), normalised by J_0 + 2 sum J_2m = 1.
+// Start index kmax + max(20, 1.5 x) + 20 (made even); rescales to avoid overflow.
+void bessel_row(double x, int kmax, double* out) {
+  if (x == 0.0) {
+    out[0] = 1.0;
+    for (int k = 1; k <= kmax; ++k) out[k] = 0.0;
+    return;
+  }
+  int start = kmax + std::max(20, (int)(1.5 * x)) + 20;
+  if (start & 1) ++start;
+  for (int k = 0; k <= kmax; ++k) out[k] = 0.0;
+  double bjp = 0.0, bj = 1e-30, sum = 0.0;
+  for (int k = start; k > 0; --k) {
+    double bjm = (2.0 * k / x) * bj - bjp;     // J_{k-1}
+    bjp = bj;
+    bj = bjm;
+    int km1 = k - 1;
+    if (std::fabs(bj) > 1e250) {
+      bj *= 1e-250; bjp *= 1e-250; sum *= 1e-250;
+      for (int i = km1 + 1; i <= kmax; ++i) out[i] *= 1e-250;
+    }
+    if (km1 <= kmax) out[km1] = bj;
+    if (km1 == 0) sum += bj;
+    else if ((km1 & 1) == 0) sum += 2.0 * bj;
+  }
+  double inv = 1.0 / sum;
+  for (int k = 0; k <= kmax; ++k) out[k] *= inv;
+}
+
+static float2 root(long r, long Nr, int sign) {   // exp(sign 2 pi i r / Nr), r reduced
+  r %= Nr;
+  if (r < 0) r += Nr;
+  double a = 2.0 * kPi * (double)r / (double)Nr;
+  return make_float2((float)std::cos(a), (float)(sign * std::sin(a)));
+}
+
+static void unit_circle(int l, int n_phi, double& cs, double& sn) {
+  // quadrant-reduced (cos, sin)(2 pi l / n_phi): multiples of pi/2 are exact
+  int Q = n_phi / 4;
+  int qd = l / Q, rem = l % Q;
+  double b = 2.0 * kPi * rem / n_phi;
+  double c0 = std::cos(b), s0 = std::sin(b);
+  switch (qd) {
+    case 0: cs = c0; sn = s0; break;
+    case 1: cs = -s0; sn = c0; break;
+    case 2: cs = -c0; sn = -s0; break;
+    default: cs = s0; sn = -c0; break;
+  }
+}
+
+static inline int fbits(float f) { int i; std::memcpy(&i, &f, 4); return i; }
+
+void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) {
+  const int n = C.n, N = C.N, L = C.Lres, NL = C.NL, Kp = C.Kp, nphi = C.n_ring;
+  // ---- multiplier m'[k][j] (E:eq2 P:L463-466 + trapezoid in lambda; scale of D1 and D3)
+  H.mult.assign((size_t)Kp * NL, 0.f);
+  {
+    std::vector<double> row(Kp);
+    const double scale = (C.h * C.h / (2.0 * kPi)) / nphi;
+    for (int j = 0; j < NL; ++j) {
+      double lam = j * C.dlam;
+      double w = (j == 0) ? 0.5 : (j == C.J ? C.wJ : 1.0);
+      bessel_row(C.R * lam, C.K, row.data());
+      double wl = scale * w * C.dlam * lam;
+      for (int k = 0; k < Kp; ++k) H.mult[(size_t)k * NL + j] = (float)(wl * row[k]);
+    }
+  }
+  // ---- twiddles
+  H.tw_n.resize(n);
+  for (int k = 0; k < n; ++k) H.tw_n[k] = root(k, n, -1);
+  H.tw_pre.resize((size_t)L * n);
+  for (int s = 0; s < L; ++s)
+    for (int yp = 0; yp < n; ++yp) {
+      long ypp = (yp < n / 2) ? yp : yp - n;        // y'' in [-n/2, n/2)
+      H.tw_pre[(size_t)s * n + yp] = root((long)s * ypp, N, -1);
+    }
+  H.tw_ring.resize(nphi);
+  for (int k = 0; k < nphi; ++k) H.tw_ring[k] = root(k, nphi, -1);
+  H.tw_dct.resize(2 * (size_t)C.M);
+  for (int k = 0; k < 2 * C.M; ++k) H.tw_dct[k] = root(k, 2L * C.M, -1);
+  H.ring = ring;
+
+  // ---- half-plane polar nodes (Alg. 1 step 3; readings G12, G13)
+  const int half = C.half;
+  const long nodes = (long)half * NL;
+  std::vector<int> p0v(nodes), q0v(nodes);
+  std::vector<double> av(nodes), bv(nodes);
+  for (int lp = 0; lp < half; ++lp) {
+    int l = ((lp - nphi / 4) % nphi + nphi) % nphi;
+    double cs, sn;
+    unit_circle(l, nphi, cs, sn);
+    for (int j = 0; j < NL; ++j) {
+      double rho = (j * C.Lbox) / C.T_new;        // lambda_j / dxi
+      double u = rho * cs, v = rho * sn;
+      double fu = std::floor(u), fv = std::floor(v);
+      long i = (long)lp * NL + j;
+      int p0 = (int)fu;
+      double a = u - fu;
+      if (p0 >= N / 2) { p0 = N / 2; a = 0.0; }   // edge: the p0+1 column does not exist
+      if (p0 < 0) { p0 = 0; a = 0.0; }            // u >= 0 on the half plane (cos >= 0)
+      p0v[i] = p0; av[i] = a;
+      q0v[i] = (int)fv; bv[i] = v - fv;
+    }
+  }
+  // K2 forward: counting sort by p0, stable in (l', j)
+  H.k2_colptr.assign(C.ncols + 1, 0);
+  for (long i = 0; i < nodes; ++i) H.k2_colptr[p0v[i] + 1]++;
+  for (int p = 0; p < C.ncols; ++p) H.k2_colptr[p + 1] += H.k2_colptr[p];
+  H.k2_nodes.resize(nodes);
+  {
+    std::vector<int> pos(H.k2_colptr.begin(), H.k2_colptr.end() - 1);
+    for (long i = 0; i < nodes; ++i) {
+      int4 e;
+      e.x = (int)i;
+      e.y = q0v[i];
+      e.z = fbits((float)av[i]);
+      e.w = fbits((float)bv[i]);
+      H.k2_nodes[pos[p0v[i]]++] = e;
+    }
+  }
+  // K2T: entries (p, q mod N, src, w) for corners with non-zero weight; group by (p, q)
+  struct Ent { int p, q, src; float w; };
+  std::vector<Ent> ent;
+  ent.reserve(nodes * 4);
+  for (long i = 0; i < nodes; ++i) {
+    double a = av[i], b = bv[i];
+    int p0 = p0v[i], q0 = q0v[i];
+    const double w[4] = {(1 - a) * (1 - b), a * (1 - b), (1 - a) * b, a * b};
+    const int pp[4] = {p0, p0 + 1, p0, p0 + 1};
+    const int qq[4] = {q0, q0, q0 + 1, q0 + 1};
+    for (int c4 = 0; c4 < 4; ++c4) {
+      if (w[c4] == 0.0) continue;
+      int qm = ((qq[c4] % N) + N) % N;
+      ent.push_back({pp[c4], qm, (int)i, (float)w[c4]});
+    }
+  }
+  // two-pass stable counting sort: by q, then by p
+  {
+    std::vector<int> cnt(N + 1, 0);
+    for (auto& e : ent) cnt[e.q + 1]++;
+    for (int q = 0; q < N; ++q) cnt[q + 1] += cnt[q];
+    std::vector<Ent> tmp(ent.size());
+    for (auto& e : ent) tmp[cnt[e.q]++] = e;
+    std::vector<int> cp(C.ncols + 1, 0);
+    for (auto& e : tmp) cp[e.p + 1]++;
+    for (int p = 0; p < C.ncols; ++p) cp[p + 1] += cp[p];
+    for (auto& e : tmp) ent[cp[e.p]++] = e;
+  }
+  H.k2t_colptr.assign(C.ncols + 1, 0);
+  H.k2t_tq.clear();
+  H.k2t_tstart.clear();
+  H.k2t_ent.resize(ent.size());
+  for (size_t e = 0; e < ent.size(); ++e) {
+    if (e == 0 || ent[e].p != ent[e - 1].p || ent[e].q != ent[e - 1].q) {
+      H.k2t_tq.push_back(ent[e].q);
+      H.k2t_tstart.push_back((int)e);
+      H.k2t_colptr[ent[e].p + 1]++;
+    }
+    H.k2t_ent[e] = make_int2(ent[e].src, fbits(ent[e].w));
+  }
+  H.k2t_tstart.push_back((int)ent.size());
+  for (int p = 0; p < C.ncols; ++p) H.k2t_colptr[p + 1] += H.k2t_colptr[p];
+}
+
+}  // namespace tat

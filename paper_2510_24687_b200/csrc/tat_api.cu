@@ -1,0 +1,317 @@
+// C ABI of libtat (include/tat.h): plan lifetime, argument validation, dispatch.
+#include "tat.h"
+#include "tat_internal.h"
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+using namespace tat;
+
+struct tat_plan {
+  DevPlan P;
+  std::vector<int> ring;
+  std::vector<void*> allocs;
+  size_t workspace_bytes = 0, table_bytes = 0;
+  float* stage_in = nullptr;    // host-variant staging: [B][n][n]
+  float* stage_out = nullptr;   // [B][n_t][n_det]
+  // profiling
+  int prof_max = 0, prof_fwd = 0, prof_adj = 0;
+  std::vector<cudaEvent_t> prof_ev;   // (prof_max) sets of 6 events
+  std::vector<char> prof_kind;        // 1 = forward, 0 = adjoint, per used slot
+};
+
+static thread_local std::string g_last_error;
+
+static tat_status fail(tat_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+static tat_status cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? TAT_ERR_OUT_OF_MEMORY : TAT_ERR_CUDA;
+}
+
+template <class T>
+static cudaError_t upload(tat_plan* p, const std::vector<T>& h, const T** dst, size_t& bytes) {
+  void* d = nullptr;
+  size_t nb = h.size() * sizeof(T);
+  if (nb == 0) nb = sizeof(T);
+  cudaError_t e = cudaMalloc(&d, nb);
+  if (e != cudaSuccess) return e;
+  p->allocs.push_back(d);
+  bytes += nb;
+  if (!h.empty()) e = cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+  *dst = static_cast<const T*>(d);
+  return e;
+}
+
+static cudaError_t alloc_ws(tat_plan* p, size_t nb, void** dst) {
+  cudaError_t e = cudaMalloc(dst, nb);
+  if (e == cudaSuccess) { p->allocs.push_back(*dst); p->workspace_bytes += nb; }
+  return e;
+}
+
+static void free_all(tat_plan* p) {
+  for (void* a : p->allocs) cudaFree(a);
+  p->allocs.clear();
+  for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
+  p->prof_ev.clear();
+}
+
+extern "C" {
+
+const char* tat_status_string(tat_status s) {
+  switch (s) {
+    case TAT_OK: return "TAT_OK";
+    case TAT_ERR_INVALID_ARGUMENT: return "TAT_ERR_INVALID_ARGUMENT";
+    case TAT_ERR_UNSUPPORTED_GEOMETRY: return "TAT_ERR_UNSUPPORTED_GEOMETRY";
+    case TAT_ERR_OUT_OF_MEMORY: return "TAT_ERR_OUT_OF_MEMORY";
+    case TAT_ERR_CUDA: return "TAT_ERR_CUDA";
+  }
+  return "TAT_ERR_UNKNOWN";
+}
+
+const char* tat_last_error(void) { return g_last_error.c_str(); }
+
+static void fill_info(const Consts& C, tat_plan_info_t* o) {
+  std::memset(o, 0, sizeof *o);
+  o->n = C.n; o->n_det = C.n_det; o->n_t = C.n_t; o->batch = C.batch;
+  o->N = C.N; o->J = C.J; o->M = C.M; o->n_ring = C.n_ring; o->K = C.K;
+  o->n_nodes_half = C.half * C.NL;
+  o->L = C.Lbox; o->T_new = C.T_new; o->dxi = C.dxi; o->dlam = C.dlam; o->omega = C.omega;
+  o->dt = C.dt; o->h = C.h; o->wJ = C.wJ;
+  o->launches_forward = kLaunchesForward;
+  o->launches_adjoint = kLaunchesAdjoint;
+}
+
+// Host-only: derive the plan constants without touching the device (used by CPU tests).
+tat_status tat_plan_derive(int n, int n_det, int n_t, double R, double c, double T, int batch,
+                           const double* detector_angles, tat_plan_info_t* out, int* ring_index) {
+  if (!out) return fail(TAT_ERR_INVALID_ARGUMENT, "out is NULL");
+  Consts C;
+  std::vector<int> ring;
+  int code = 0;
+  std::string err = derive_consts(n, n_det, n_t, R, c, T, batch, detector_angles, C, ring, code);
+  if (!err.empty()) return fail(code == 2 ? TAT_ERR_UNSUPPORTED_GEOMETRY : TAT_ERR_INVALID_ARGUMENT, err);
+  std::string sup = gpu_support(C);
+  fill_info(C, out);
+  if (ring_index) for (int d = 0; d < C.n_det; ++d) ring_index[d] = ring[d];
+  if (!sup.empty()) return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, sup);
+  return TAT_OK;
+}
+
+// Host-only: the multiplier table m'[k][j] (float32, [K+1][J+1]) the plan would upload.
+tat_status tat_plan_host_multiplier(int n, int n_det, int n_t, double R, double c, double T,
+                                    const double* detector_angles, float* out, size_t out_len) {
+  Consts C;
+  std::vector<int> ring;
+  int code = 0;
+  std::string err = derive_consts(n, n_det, n_t, R, c, T, 1, detector_angles, C, ring, code);
+  if (!err.empty()) return fail(code == 2 ? TAT_ERR_UNSUPPORTED_GEOMETRY : TAT_ERR_INVALID_ARGUMENT, err);
+  if (!out || out_len < (size_t)C.Kp * C.NL) return fail(TAT_ERR_INVALID_ARGUMENT, "out too small");
+  HostTables H;
+  build_tables(C, ring, H);
+  std::memcpy(out, H.mult.data(), H.mult.size() * sizeof(float));
+  return TAT_OK;
+}
+
+tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R, double c,
+                           double T, int batch, const double* detector_angles) {
+  if (!plan) return fail(TAT_ERR_INVALID_ARGUMENT, "plan is NULL");
+  Consts C;
+  std::vector<int> ring;
+  int code = 0;
+  std::string err = derive_consts(n, n_det, n_t, R, c, T, batch, detector_angles, C, ring, code);
+  if (!err.empty()) return fail(code == 2 ? TAT_ERR_UNSUPPORTED_GEOMETRY : TAT_ERR_INVALID_ARGUMENT, err);
+  std::string sup = gpu_support(C);
+  if (!sup.empty()) return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, sup);
+
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+
+  HostTables H;
+  build_tables(C, ring, H);
+
+  tat_plan* p = new (std::nothrow) tat_plan();
+  if (!p) return fail(TAT_ERR_OUT_OF_MEMORY, "host allocation");
+  DevPlan& P = p->P;
+  P.C = C;
+  p->ring = ring;
+  size_t tb = 0;
+  do {
+    if ((e = upload(p, H.mult, &P.mult, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.tw_n, &P.tw_n, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.tw_pre, &P.tw_pre, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.tw_ring, &P.tw_ring, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.tw_dct, &P.tw_dct, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2_colptr, &P.k2_colptr, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2_nodes, &P.k2_nodes, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2t_colptr, &P.k2t_colptr, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2t_tq, &P.k2t_tq, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2t_tstart, &P.k2t_tstart, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2t_ent, &P.k2t_ent, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.ring, &P.ring, tb)) != cudaSuccess) break;
+    const size_t B = (size_t)C.batch;
+    void* d;
+    if ((e = alloc_ws(p, B * C.ncols * C.n * sizeof(float2), &d)) != cudaSuccess) break;
+    P.S1 = (float2*)d;
+    if ((e = alloc_ws(p, B * C.half * C.NL * sizeof(float2), &d)) != cudaSuccess) break;
+    P.S2 = (float2*)d;
+    if ((e = alloc_ws(p, B * C.Kp * C.NL * sizeof(float2), &d)) != cudaSuccess) break;
+    P.S3 = (float2*)d;
+    if ((e = alloc_ws(p, B * C.Kp * C.n_t * sizeof(float2), &d)) != cudaSuccess) break;
+    P.S4 = (float2*)d;
+    e = configure_kernels(P);
+  } while (false);
+  p->table_bytes = tb;
+  if (e != cudaSuccess) {
+    tat_status st = cuda_fail(e, "tat_plan_create");
+    free_all(p);
+    delete p;
+    return st;
+  }
+  *plan = p;
+  return TAT_OK;
+}
+
+void tat_plan_destroy(tat_plan* plan) {
+  if (!plan) return;
+  free_all(plan);
+  delete plan;
+}
+
+tat_status tat_plan_info(const tat_plan* plan, tat_plan_info_t* out, int* ring_index) {
+  if (!plan || !out) return fail(TAT_ERR_INVALID_ARGUMENT, "plan or out is NULL");
+  fill_info(plan->P.C, out);
+  out->workspace_bytes = plan->workspace_bytes;
+  out->table_bytes = plan->table_bytes;
+  if (ring_index)
+    for (int d = 0; d < plan->P.C.n_det; ++d) ring_index[d] = plan->ring[d];
+  return TAT_OK;
+}
+
+static cudaEvent_t* prof_slot(tat_plan* p, bool fwd) {
+  if (p->prof_max <= 0) return nullptr;
+  int used = p->prof_fwd + p->prof_adj;
+  if (used >= p->prof_max) return nullptr;
+  (fwd ? p->prof_fwd : p->prof_adj)++;
+  p->prof_kind.push_back(fwd ? 1 : 0);
+  return &p->prof_ev[(size_t)used * 6];
+}
+
+tat_status tat_forward(const tat_plan* plan, const float* f, float* g, cudaStream_t stream) {
+  if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  tat_plan* p = const_cast<tat_plan*>(plan);
+  cudaEvent_t* ev = prof_slot(p, true);
+  cudaError_t e = launch_forward(plan->P, f, g, stream, ev);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_forward launch");
+  return TAT_OK;
+}
+
+tat_status tat_adjoint(const tat_plan* plan, const float* g, float* f, cudaStream_t stream) {
+  if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  tat_plan* p = const_cast<tat_plan*>(plan);
+  cudaEvent_t* ev = prof_slot(p, false);
+  cudaError_t e = launch_adjoint(plan->P, g, f, stream, ev);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_adjoint launch");
+  return TAT_OK;
+}
+
+static tat_status ensure_staging(tat_plan* p) {
+  if (p->stage_in) return TAT_OK;
+  const Consts& C = p->P.C;
+  void *a = nullptr, *b = nullptr;
+  cudaError_t e = cudaMalloc(&a, (size_t)C.batch * C.n * C.n * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&b, (size_t)C.batch * C.n_t * C.n_det * sizeof(float));
+  if (e != cudaSuccess) {
+    if (a) cudaFree(a);
+    return cuda_fail(e, "staging allocation");
+  }
+  p->allocs.push_back(a);
+  p->allocs.push_back(b);
+  p->stage_in = (float*)a;
+  p->stage_out = (float*)b;
+  return TAT_OK;
+}
+
+tat_status tat_forward_host(const tat_plan* plan, const float* f_host, float* g_host,
+                            cudaStream_t stream) {
+  if (!plan || !f_host || !g_host) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  tat_plan* p = const_cast<tat_plan*>(plan);
+  tat_status st = ensure_staging(p);
+  if (st != TAT_OK) return st;
+  const Consts& C = p->P.C;
+  size_t nin = (size_t)C.batch * C.n * C.n * sizeof(float);
+  size_t nout = (size_t)C.batch * C.n_t * C.n_det * sizeof(float);
+  cudaError_t e = cudaMemcpyAsync(p->stage_in, f_host, nin, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  st = tat_forward(plan, p->stage_in, p->stage_out, stream);
+  if (st != TAT_OK) return st;
+  e = cudaMemcpyAsync(g_host, p->stage_out, nout, cudaMemcpyDeviceToHost, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H");
+  return TAT_OK;
+}
+
+tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_host,
+                            cudaStream_t stream) {
+  if (!plan || !f_host || !g_host) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  tat_plan* p = const_cast<tat_plan*>(plan);
+  tat_status st = ensure_staging(p);
+  if (st != TAT_OK) return st;
+  const Consts& C = p->P.C;
+  size_t nimg = (size_t)C.batch * C.n * C.n * sizeof(float);
+  size_t ndat = (size_t)C.batch * C.n_t * C.n_det * sizeof(float);
+  cudaError_t e = cudaMemcpyAsync(p->stage_out, g_host, ndat, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  st = tat_adjoint(plan, p->stage_out, p->stage_in, stream);
+  if (st != TAT_OK) return st;
+  e = cudaMemcpyAsync(f_host, p->stage_in, nimg, cudaMemcpyDeviceToHost, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H");
+  return TAT_OK;
+}
+
+tat_status tat_profile_begin(tat_plan* plan, int max_calls) {
+  if (!plan || max_calls < 0) return fail(TAT_ERR_INVALID_ARGUMENT, "bad arguments");
+  for (cudaEvent_t e : plan->prof_ev) cudaEventDestroy(e);
+  plan->prof_ev.assign((size_t)max_calls * 6, nullptr);
+  plan->prof_kind.clear();
+  for (auto& e : plan->prof_ev) {
+    cudaError_t r = cudaEventCreate(&e);
+    if (r != cudaSuccess) return cuda_fail(r, "cudaEventCreate");
+  }
+  plan->prof_max = max_calls;
+  plan->prof_fwd = plan->prof_adj = 0;
+  return TAT_OK;
+}
+
+tat_status tat_profile_end(tat_plan* plan, float* stage_ms, int* n_forward, int* n_adjoint) {
+  if (!plan || !stage_ms) return fail(TAT_ERR_INVALID_ARGUMENT, "bad arguments");
+  for (int i = 0; i < 10; ++i) stage_ms[i] = 0.f;
+  int used = plan->prof_fwd + plan->prof_adj;
+  for (int u = 0; u < used; ++u) {
+    cudaEvent_t* ev = &plan->prof_ev[(size_t)u * 6];
+    cudaError_t r = cudaEventSynchronize(ev[5]);
+    if (r != cudaSuccess) return cuda_fail(r, "cudaEventSynchronize");
+    bool fwd = plan->prof_kind[u] != 0;
+    for (int s = 0; s < 5; ++s) {
+      float ms = 0.f;
+      r = cudaEventElapsedTime(&ms, ev[s], ev[s + 1]);
+      if (r != cudaSuccess) return cuda_fail(r, "cudaEventElapsedTime");
+      stage_ms[(fwd ? 0 : 5) + s] += ms;
+    }
+  }
+  if (n_forward) *n_forward = plan->prof_fwd;
+  if (n_adjoint) *n_adjoint = plan->prof_adj;
+  for (cudaEvent_t e : plan->prof_ev) cudaEventDestroy(e);
+  plan->prof_ev.clear();
+  plan->prof_kind.clear();
+  plan->prof_max = 0;
+  plan->prof_fwd = plan->prof_adj = 0;
+  return TAT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// Internal declarations shared by the host plan builder and the sm_100a kernels.
+// Nothing here is part of the public ABI (see include/tat.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+namespace tat {
+
+// Derived constants of the discretisation (D0).
+struct Consts {
+  int n = 0, n_det = 0, n_t = 0, batch = 0;
+  double R = 1, c = 1, T = 1;
+  double h = 0, T_new0 = 0, T_new = 0, Lbox = 0, dxi = 0, dt = 0, dlam = 0, lam_max = 0;
+  double wJ = 1, omega = 0;
+  int N = 0;        // Cartesian FFT size
+  int Lres = 0;     // residues N / n (oversampling factor, power of two)
+  int M = 0;        // DCT-I length; 2M-point FFT
+  int J = 0, NL = 0;
+  int n_ring = 0, K = 0, Kp = 0, half = 0;
+  int ncols = 0;    // N/2 + 1 Cartesian columns kept (p in [0, N/2])
+};  // plain data: passed by value to kernels inside DevPlan
+
+// Host-side tables (float64 built, float32/int stored), uploaded by tat_plan_create.
+struct HostTables {
+  std::vector<float> mult;          // [Kp][NL]: (h^2/2pi)(1/n_phi) w_j dlam lam_j J_k(R lam_j)
+  std::vector<float2> tw_n;         // n roots exp(-2 pi i k / n)
+  std::vector<float2> tw_pre;       // [Lres][n]: exp(-2 pi i s y'' / N) at FFT slot y' = y'' mod n
+  std::vector<float2> tw_ring;      // n_ring roots
+  std::vector<float2> tw_dct;       // 2M roots
+  // K2 forward gather: half-plane nodes sorted by p0
+  std::vector<int> k2_colptr;       // [ncols + 1]
+  std::vector<int4> k2_nodes;       // (target = l'*NL + j, q0, alpha bits, beta bits)
+  // K2T transposed gather: per column p, targets (q mod N) with entry ranges
+  std::vector<int> k2t_colptr;      // [ncols + 1] into targets
+  std::vector<int> k2t_tq;          // [T] q mod N
+  std::vector<int> k2t_tstart;      // [T + 1] into entries
+  std::vector<int2> k2t_ent;        // [E] (src target index, weight bits)
+  std::vector<int> ring;            // [n_det]
+};
+
+// returns "" on success, else an error message; code receives 1 (invalid) or 2 (unsupported)
+std::string derive_consts(int n, int n_det, int n_t, double R, double c, double T, int batch,
+                          const double* angles, Consts& out, std::vector<int>& ring, int& code);
+std::string gpu_support(const Consts& C);    // "" if the sm_100a kernels implement C
+void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H);
+void bessel_row(double x, int kmax, double* out);   // J_0..J_kmax(x), Miller recurrence
+
+// Device-side view of a plan (pointers into device memory).
+struct DevPlan {
+  Consts C;
+  // tables
+  const float* mult = nullptr;
+  const float2* tw_n = nullptr;
+  const float2* tw_pre = nullptr;
+  const float2* tw_ring = nullptr;
+  const float2* tw_dct = nullptr;
+  const int* k2_colptr = nullptr;
+  const int4* k2_nodes = nullptr;
+  const int* k2t_colptr = nullptr;
+  const int* k2t_tq = nullptr;
+  const int* k2t_tstart = nullptr;
+  const int2* k2t_ent = nullptr;
+  const int* ring = nullptr;
+  // workspace
+  float2* S1 = nullptr;   // [B][ncols][n]
+  float2* S2 = nullptr;   // [B][half][NL]
+  float2* S3 = nullptr;   // [B][Kp][NL]
+  float2* S4 = nullptr;   // [B][Kp][n_t]
+};
+
+// Launchers (kernels.cu).  ev != nullptr: record ev[i] before stage i and ev[5] at the end.
+cudaError_t launch_forward(const DevPlan& P, const float* f, float* g, cudaStream_t s,
+                           cudaEvent_t* ev);
+cudaError_t launch_adjoint(const DevPlan& P, const float* g, float* f, cudaStream_t s,
+                           cudaEvent_t* ev);
+cudaError_t configure_kernels(const DevPlan& P);   // smem attributes
+size_t max_smem_needed(const Consts& C);
+
+constexpr int kLaunchesForward = 5;
+constexpr int kLaunchesAdjoint = 5;
+
+}  // namespace tat

@@ -1,0 +1,223 @@
+"""Thin ctypes binding of libtat (include/tat.h).  Argument marshalling only: every step of
+A and A* runs in the sm_100a kernels of libtat.so.  There is no CPU fallback: if the library
+is missing or a call fails, an exception is raised.
+
+    plan = Plan(n=512, n_det=512, n_t=1024, batch=16, angles=angles)   # R=c=1, T=2 defaults
+    g = plan.forward(f)        # f: float32 CUDA tensor [B, n, n]  -> g [B, n_t, n_det]
+    u = plan.adjoint(g)        # A* = omega A^T (L2 adjoint, eqn:innerProducts P:L217-222)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtat.so")
+
+TAT_OK = 0
+STATUS = {0: "TAT_OK", 1: "TAT_ERR_INVALID_ARGUMENT", 2: "TAT_ERR_UNSUPPORTED_GEOMETRY",
+          3: "TAT_ERR_OUT_OF_MEMORY", 4: "TAT_ERR_CUDA"}
+
+# every symbol include/tat.h declares
+EXPORTS = ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
+           "tat_adjoint_host", "tat_plan_destroy", "tat_plan_info", "tat_plan_derive",
+           "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
+           "tat_status_string", "tat_last_error")
+
+
+class TatError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        self.status = status
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("n_det", ctypes.c_int), ("n_t", ctypes.c_int),
+                ("batch", ctypes.c_int), ("N", ctypes.c_int), ("J", ctypes.c_int),
+                ("M", ctypes.c_int), ("n_ring", ctypes.c_int), ("K", ctypes.c_int),
+                ("n_nodes_half", ctypes.c_int),
+                ("L", ctypes.c_double), ("T_new", ctypes.c_double), ("dxi", ctypes.c_double),
+                ("dlam", ctypes.c_double), ("omega", ctypes.c_double), ("dt", ctypes.c_double),
+                ("h", ctypes.c_double), ("wJ", ctypes.c_double),
+                ("workspace_bytes", ctypes.c_size_t), ("table_bytes", ctypes.c_size_t),
+                ("launches_forward", ctypes.c_int), ("launches_adjoint", ctypes.c_int)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libtat.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libtat.so not found at {path}; run __graft_entry__.build() "
+                          "or python -m paper_2510_24687_b200.build_lib")
+    lib = ctypes.CDLL(path)
+    vp, i, d, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
+    dp = ctypes.POINTER(ctypes.c_double)
+    ip = ctypes.POINTER(ctypes.c_int)
+    lib.tat_plan_create.argtypes = [ctypes.POINTER(vp), i, i, i, d, d, d, i, dp]
+    lib.tat_forward.argtypes = [vp, vp, vp, vp]
+    lib.tat_adjoint.argtypes = [vp, vp, vp, vp]
+    lib.tat_forward_host.argtypes = [vp, vp, vp, vp]
+    lib.tat_adjoint_host.argtypes = [vp, vp, vp, vp]
+    lib.tat_plan_destroy.argtypes = [vp]
+    lib.tat_plan_destroy.restype = None
+    lib.tat_plan_info.argtypes = [vp, ctypes.POINTER(PlanInfo), ip]
+    lib.tat_plan_derive.argtypes = [i, i, i, d, d, d, i, dp, ctypes.POINTER(PlanInfo), ip]
+    lib.tat_plan_host_multiplier.argtypes = [i, i, i, d, d, d, dp, ctypes.POINTER(ctypes.c_float), sz]
+    lib.tat_profile_begin.argtypes = [vp, i]
+    lib.tat_profile_end.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ip, ip]
+    lib.tat_status_string.argtypes = [i]
+    lib.tat_status_string.restype = ctypes.c_char_p
+    lib.tat_last_error.argtypes = []
+    lib.tat_last_error.restype = ctypes.c_char_p
+    for name in ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
+                 "tat_adjoint_host", "tat_plan_info", "tat_plan_derive",
+                 "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end"):
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != TAT_OK:
+        raise TatError(status, load_library().tat_last_error().decode())
+
+
+def _angles(angles, n_det):
+    a = np.ascontiguousarray(np.asarray(angles, dtype=np.float64))
+    if a.shape != (n_det,):
+        raise ValueError(f"angles must have shape ({n_det},)")
+    return a
+
+
+def derive(n, n_det, n_t, R=1.0, c=1.0, T=2.0, batch=1, angles=None):
+    """Host-only constants (tat_plan_derive).  Returns (info dict, ring indices, status)."""
+    lib = load_library()
+    a = _angles(angles, n_det)
+    info = PlanInfo()
+    ring = np.zeros(n_det, dtype=np.int32)
+    st = lib.tat_plan_derive(n, n_det, n_t, R, c, T, batch,
+                             a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                             ctypes.byref(info), ring.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+    return info.as_dict(), ring, st
+
+
+def host_multiplier(n, n_det, n_t, R=1.0, c=1.0, T=2.0, angles=None):
+    """The float32 multiplier table m'[k][j] the plan uploads (host-only)."""
+    info, _, st = derive(n, n_det, n_t, R, c, T, 1, angles)
+    if st not in (TAT_OK, 2):
+        _check(st)
+    out = np.zeros((info["K"] + 1, info["J"] + 1), dtype=np.float32)
+    lib = load_library()
+    a = _angles(angles, n_det)
+    _check(lib.tat_plan_host_multiplier(n, n_det, n_t, R, c, T,
+                                        a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                        out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), out.size))
+    return out
+
+
+class Plan:
+    """A tat_plan: device tables + workspace for one geometry and batch size."""
+
+    def __init__(self, n, n_det, n_t, R=1.0, c=1.0, T=2.0, batch=1, angles=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libtat needs a CUDA device (no CPU fallback)")
+        self._lib = load_library()
+        torch.cuda.current_device()          # make sure a context exists on this thread
+        a = _angles(angles, n_det)
+        h = ctypes.c_void_p()
+        _check(self._lib.tat_plan_create(ctypes.byref(h), n, n_det, n_t, R, c, T, batch,
+                                         a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        self._h = h
+        self.n, self.n_det, self.n_t, self.batch = n, n_det, n_t, batch
+        self.info = self._info()
+
+    def _info(self):
+        info = PlanInfo()
+        ring = np.zeros(self.n_det, dtype=np.int32)
+        _check(self._lib.tat_plan_info(self._h, ctypes.byref(info),
+                                       ring.ctypes.data_as(ctypes.POINTER(ctypes.c_int))))
+        d = info.as_dict()
+        d["ring"] = ring
+        return d
+
+    @property
+    def omega(self) -> float:
+        return self.info["omega"]
+
+    def _stream(self, stream):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def _chk(self, t, shape, name):
+        import torch
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+                and tuple(t.shape) == shape):
+            raise ValueError(f"{name} must be a contiguous float32 CUDA tensor of shape {shape}")
+
+    def forward(self, f, out=None, stream=None):
+        """g = A f on the current (or given) torch stream; no host synchronisation."""
+        import torch
+        self._chk(f, (self.batch, self.n, self.n), "f")
+        g = out if out is not None else torch.empty((self.batch, self.n_t, self.n_det),
+                                                    device=f.device, dtype=torch.float32)
+        self._chk(g, (self.batch, self.n_t, self.n_det), "g")
+        _check(self._lib.tat_forward(self._h, ctypes.c_void_p(f.data_ptr()),
+                                     ctypes.c_void_p(g.data_ptr()), self._stream(stream)))
+        return g
+
+    def adjoint(self, g, out=None, stream=None):
+        """f = A* g (= omega A^T g) on the current (or given) torch stream."""
+        import torch
+        self._chk(g, (self.batch, self.n_t, self.n_det), "g")
+        f = out if out is not None else torch.empty((self.batch, self.n, self.n),
+                                                    device=g.device, dtype=torch.float32)
+        self._chk(f, (self.batch, self.n, self.n), "f")
+        _check(self._lib.tat_adjoint(self._h, ctypes.c_void_p(g.data_ptr()),
+                                     ctypes.c_void_p(f.data_ptr()), self._stream(stream)))
+        return f
+
+    def forward_host(self, f_host: np.ndarray, g_host: np.ndarray, stream=None):
+        """Host-buffer variant (H2D + A + D2H on the stream); caller synchronises."""
+        assert f_host.dtype == np.float32 and f_host.flags.c_contiguous
+        assert g_host.dtype == np.float32 and g_host.flags.c_contiguous
+        _check(self._lib.tat_forward_host(self._h, ctypes.c_void_p(f_host.ctypes.data),
+                                          ctypes.c_void_p(g_host.ctypes.data), self._stream(stream)))
+
+    def adjoint_host(self, g_host: np.ndarray, f_host: np.ndarray, stream=None):
+        assert f_host.dtype == np.float32 and f_host.flags.c_contiguous
+        assert g_host.dtype == np.float32 and g_host.flags.c_contiguous
+        _check(self._lib.tat_adjoint_host(self._h, ctypes.c_void_p(g_host.ctypes.data),
+                                          ctypes.c_void_p(f_host.ctypes.data), self._stream(stream)))
+
+    def profile_begin(self, max_calls: int):
+        _check(self._lib.tat_profile_begin(self._h, max_calls))
+
+    def profile_end(self):
+        """(stage_ms[10] summed, n_forward, n_adjoint); stages K1..K5, K5T..K1T."""
+        ms = (ctypes.c_float * 10)()
+        nf, na = ctypes.c_int(), ctypes.c_int()
+        _check(self._lib.tat_profile_end(self._h, ms, ctypes.byref(nf), ctypes.byref(na)))
+        return list(ms), nf.value, na.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.tat_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
