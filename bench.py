@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark: A + A* pairs per second at n=512, batch 16 (BASELINE.json metric, config C3).
+
+One step = one forward A and one adjoint A* over the whole batch (all SURVEY §8(a) rows),
+through libtat's C ABI (ctypes binding), inputs resident in HBM.  L2 (126 MB) is flushed
+between timed steps (outside the per-step CUDA events); the step's own working set (~300 MB
+at C3) exceeds L2 as well.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+--impl reference times the float64 oracle (tests' reference; a deliberately slow CPU program)
+on bounded samples of the same workload.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "A+A* pairs/sec at n=512, batch 16 (fp32); achieved % of HBM roofline"
+UNIT = "image-pairs/s"
+STAGES = ["K1", "K2", "K3", "K4", "K5", "K5T", "K4T", "K3T", "K2T", "K1T"]
+
+
+def workload_desc(name: str) -> str:
+    g = synth.geometry(name)
+    kind = {"C1": "8 Gaussians", "C2": "20 ellipses", "C3": "20 random ellipses",
+            "C4": "8 Gaussians + 20 ellipses", "C5": "20 ellipses, 270-degree arc"}[name]
+    return (f"{name}: n={g.n}, {g.n_det} detectors (R=1, c=1), n_t={g.n_t} on (0,{g.T:g}], "
+            f"batch {g.batch}, {kind}")
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- models
+def model(info: dict) -> dict:
+    """Algorithmic bytes and flops per launch (whole batch), DESIGN.md "Roofline model".
+    Bytes: each intermediate written once and read once at its stored size, inputs/outputs
+    once, plan tables once per launch.  Flops: 5 m log2 m per m-point complex FFT, 6 per
+    complex twiddle, 14 per bilinear node (3 complex lerps), 2 per real multiply."""
+    n, N, B = info["n"], info["N"], info["batch"]
+    L = N // n
+    ncols = N // 2 + 1
+    NL = info["J"] + 1
+    Kp = info["K"] + 1
+    half = info["n_ring"] // 2
+    nphi = info["n_ring"]
+    n_t, n_det = info["n_t"], info["n_det"]
+    M2 = 2 * info["M"]
+    c8 = 8
+    f_b, g_b = 4 * n * n, 4 * n_t * n_det
+    S1, S2, S3, S4 = c8 * n * ncols, c8 * half * NL, c8 * Kp * NL, c8 * Kp * n_t
+    nodes = half * NL
+    lg = math.log2
+    fft = lambda m: 5 * m * lg(m)
+    by = {
+        "K1": B * (f_b + S1), "K2": B * (S1 + S2) + 16 * nodes, "K3": B * (S2 + S3) + 4 * Kp * NL,
+        "K4": B * (S3 + S4), "K5": B * (S4 + g_b) + 4 * n_det,
+        "K5T": B * (g_b + S4) + 4 * n_det, "K4T": B * (S4 + S3) + 4 * Kp * NL,
+        "K3T": B * (S3 + S2), "K2T": B * (S2 + S1) + 12 * 4 * nodes, "K1T": B * (S1 + f_b),
+    }
+    fl = {
+        "K1": B * (n / 2) * L * (fft(n) + 6 * n),
+        "K2": B * ncols * L * (fft(n) + 6 * n) + B * nodes * 14,
+        "K3": B * NL * (fft(nphi) + 6 * Kp),
+        "K4": B * Kp * fft(M2),
+        "K5": B * n_t * fft(nphi),
+    }
+    fl.update({"K5T": fl["K5"], "K4T": fl["K4"] + B * Kp * NL * 6, "K3T": fl["K3"],
+               "K2T": fl["K2"], "K1T": fl["K1"]})
+    pair_bytes = sum(by.values())
+    return {"bytes": by, "flops": fl, "pair_bytes": pair_bytes}
+
+
+BOUND = {"K1": "hbm", "K2": "alu", "K3": "hbm", "K4": "hbm", "K5": "hbm",
+         "K5T": "hbm", "K4T": "hbm", "K3T": "hbm", "K2T": "alu", "K1T": "hbm"}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample(name: str, budget_s: float, min_pairs: int = 1, max_pairs: int = 64):
+    """Time the float64 oracle (as it stands) on images of the workload until budget_s."""
+    from oracle import tat_oracle as O
+    geo = synth.geometry(name)
+    C = O.derive_geom(geo)
+    t0 = time.perf_counter()
+    O.forward(np.zeros((geo.n, geo.n)), C)          # untimed warm-up (table caches)
+    setup = time.perf_counter() - t0
+    done, t_work = 0, 0.0
+    while done < max_pairs and (done < min_pairs or t_work < budget_s):
+        f = synth.phantom(name, done % geo.batch).astype(np.float64)
+        t1 = time.perf_counter()
+        g = O.forward(f, C)
+        O.adjoint(g, C)
+        t_work += time.perf_counter() - t1
+        done += 1
+    return done, t_work, setup
+
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        th = [d.get("num_threads", 0) for d in threadpool_info() if d.get("user_api") == "blas"]
+        return max(th) if th else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return 0
+    name = args.config
+    budget = float(os.environ.get("TAT_ORACLE_STEP_S", "2.0"))
+    oracle_sample(name, 0.0, min_pairs=1, max_pairs=1) if args.warmup > 0 else None
+    times, pairs = [], 0
+    for _ in range(args.steps):
+        done, t, _ = oracle_sample(name, budget, min_pairs=1, max_pairs=4)
+        times.append(t)
+        pairs += done
+    total = sum(times)
+    value = pairs / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": workload_desc(name), "parallelism": "cpu (float64 oracle)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+                         "sample": f"{pairs} image pairs (A then A*) of {name}, float64 direct sums"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+    from paper_2510_24687_b200 import Plan
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    name = args.config
+    geo = synth.geometry(name)
+    B = geo.batch
+    plan = Plan(geo.n, geo.n_det, geo.n_t, geo.R, geo.c, geo.T, B, geo.angles_array())
+    info = plan.info
+    f_host = synth.phantom_batch(name)                      # identical batch on every rank
+    f = torch.from_numpy(f_host).to(dev)
+    g = torch.empty((B, geo.n_t, geo.n_det), device=dev)
+    u = torch.empty((B, geo.n, geo.n), device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        plan.forward(f, out=g)
+        plan.adjoint(g, out=u)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    plan.profile_begin(2 * args.steps)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stage_ms, nf, na = plan.profile_end()
+    clocks = sampler.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * B * args.steps / (total_ms / 1000.0)
+
+    # ---- end to end: pinned H2D of f, A, A*, D2H of the result, every step
+    f_pin = torch.from_numpy(f_host).pin_memory()
+    u_pin = torch.empty((B, geo.n, geo.n), dtype=torch.float32).pin_memory()
+    f_dev = torch.empty_like(f)
+    for _ in range(2):
+        f_dev.copy_(f_pin, non_blocking=True)
+        plan.forward(f_dev, out=g)
+        plan.adjoint(g, out=u)
+        u_pin.copy_(u, non_blocking=True)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(3, args.steps // 2)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        f_dev.copy_(f_pin, non_blocking=True)
+        plan.forward(f_dev, out=g)
+        plan.adjoint(g, out=u)
+        u_pin.copy_(u, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * B * e2e_steps / (e2e_ms / 1000.0)
+
+    if rank != 0:
+        return 0
+
+    pk, pk_kind = peaks()
+    mdl = model(info)
+    per_stage_us = {s: 1000.0 * stage_ms[i] / max(1, (nf if i < 5 else na))
+                    for i, s in enumerate(STAGES)}
+    dom = max(per_stage_us, key=per_stage_us.get)
+    dur_s = per_stage_us[dom] * 1e-6
+    clk = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    alu_peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12    # TFLOP/s
+    if BOUND[dom] == "alu":
+        ach = mdl["flops"][dom] / dur_s / 1e12
+        roof = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
+                "frac": ach / alu_peak, "traffic": None,
+                "kernel": dom, "algorithmic_flops": mdl["flops"][dom],
+                "hbm_achieved_gbs": mdl["bytes"][dom] / dur_s / 1e9,
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md)"}
+    else:
+        ach = mdl["bytes"][dom] / dur_s / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / pk["hbm_gbs"], "traffic": None, "kernel": dom,
+                "algorithmic_bytes": mdl["bytes"][dom], "peak_source": pk_kind}
+    eff_hbm = mdl["pair_bytes"] / (ms_per_step * 1e-3) / 1e9     # GB/s, whole batch
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        pairs, t_work, setup = oracle_sample(name, float(os.environ.get("TAT_ORACLE_BUDGET_S", "10")),
+                                             min_pairs=1, max_pairs=64)
+        cpu = {"value": pairs / t_work, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+               "sample": f"{pairs} image pair(s) (A then A*) of {name} in float64 direct sums; "
+                         f"table setup {setup:.1f}s excluded"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_desc(name), "batch_per_gpu": B,
+                   "parallelism": f"replicas x{world} (batch-sharded, no collective)",
+                   "l2": "flushed (256 MB write) between timed steps, outside the step events"},
+        "hbm_roofline_effective": {"model_bytes_per_step": mdl["pair_bytes"],
+                                   "achieved_gbs": eff_hbm, "peak_gbs": pk["hbm_gbs"],
+                                   "frac": eff_hbm / pk["hbm_gbs"]},
+        "roofline": roof,
+        "stage_us": {k: round(v, 2) for k, v in per_stage_us.items()},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(f_host.nbytes),
+                "d2h_bytes_per_step": int(u_pin.numel() * 4)},
+        "gpu_launches": (info["launches_forward"] + info["launches_adjoint"]) * args.steps,
+        "clocks": clocks,
+        "paper_context": "A alone: 0.0055 s at 257^2, 360x513, batch 1 on an Nvidia A2000 "
+                         "(PAPER.md L822-825); not this workload",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3", choices=list(synth.CONFIGS))
+    ap.add_argument("--impl", default="tat", choices=["tat", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
+        return run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

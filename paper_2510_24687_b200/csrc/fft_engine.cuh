@@ -1,0 +1,165 @@
+// Register/shared-memory FFT engine for the L residue transforms of the zero-padded 2-D DFT.
+//
+// The N = L n point DFT of a column with n non-zero samples (Alg. 1 step 2, the zero-extended
+// 2-D FFT of PAPER.md L545-548) is split into L residue classes q = L a + s:
+//   F[L a + s] = sum_{y''} (x[y''] W_N^{s y''}) W_n^{a y''},  y'' in [-n/2, n/2),
+// i.e. a pre-twiddle and an n-point FFT per residue.  Each thread owns one radix-8 butterfly
+// (8 complex points) of RPT residues; passes are Stockham (natural-order output) with radix
+// 8, 8, ..., and a final radix 2 or 4 (n = 8^a * {1, 2, 4}).  Data moves between passes
+// through shared memory with an XOR swizzle that makes every pass's 8-byte accesses
+// bank-conflict free.  Complex arithmetic maps to FADD2 / FMUL2 / FFMA2 (two fp32 lanes
+// per instruction: {re, im}).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace tat {
+namespace fe {
+
+// ------------------------------------------------------------------ packed complex ops
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+// a * w  (FMUL2 + FFMA2)
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {
+  float2 t = __fmul2_rn(w, make_float2(a.x, a.x));
+  return __ffma2_rn(make_float2(-w.y, w.x), make_float2(a.y, a.y), t);
+}
+// a * conj(w)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 w) {
+  float2 t = __fmul2_rn(make_float2(w.x, -w.y), make_float2(a.x, a.x));
+  return __ffma2_rn(make_float2(w.y, w.x), make_float2(a.y, a.y), t);
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+// a + S i b  (S = +1 or -1)
+template <int S>
+__device__ __forceinline__ float2 add_ib(float2 a, float2 b) {
+  return (S > 0) ? __fadd2_rn(a, make_float2(-b.y, b.x)) : __fadd2_rn(a, make_float2(b.y, -b.x));
+}
+
+// ------------------------------------------------------------------ small DFTs (in place)
+// X[k] = sum_r a[r] e^{S 2 pi i r k / R}, natural order.
+template <int S>
+__device__ __forceinline__ void dft2(float2* a) {
+  float2 t = cadd(a[0], a[1]);
+  a[1] = csub(a[0], a[1]);
+  a[0] = t;
+}
+template <int S>
+__device__ __forceinline__ void dft4(float2* a) {
+  float2 s02 = cadd(a[0], a[2]), d02 = csub(a[0], a[2]);
+  float2 s13 = cadd(a[1], a[3]), d13 = csub(a[1], a[3]);
+  a[0] = cadd(s02, s13);
+  a[2] = csub(s02, s13);
+  a[1] = add_ib<S>(d02, d13);
+  a[3] = add_ib<-S>(d02, d13);
+}
+template <int S>
+__device__ __forceinline__ void dft8(float2* a) {
+  const float h = 0.70710678118654752440f;
+  float2 t0 = cadd(a[0], a[4]), u0 = csub(a[0], a[4]);
+  float2 t1 = cadd(a[1], a[5]), u1 = csub(a[1], a[5]);
+  float2 t2 = cadd(a[2], a[6]), u2 = csub(a[2], a[6]);
+  float2 t3 = cadd(a[3], a[7]), u3 = csub(a[3], a[7]);
+  // odd half twiddles: u1 (1 + S i)/sqrt2, u2 (S i), u3 (-1 + S i)/sqrt2 = S i (1 + S i)/sqrt2 u3
+  float2 v1 = cscale(add_ib<S>(u1, u1), h);
+  float2 v3 = cscale(add_ib<S>(u3, u3), h);
+  // even: DFT4(t0, t1, t2, t3)
+  float2 s02 = cadd(t0, t2), d02 = csub(t0, t2);
+  float2 s13 = cadd(t1, t3), d13 = csub(t1, t3);
+  a[0] = cadd(s02, s13);
+  a[4] = csub(s02, s13);
+  a[2] = add_ib<S>(d02, d13);
+  a[6] = add_ib<-S>(d02, d13);
+  // odd: DFT4(u0, v1, S i u2, S i v3)
+  float2 os02 = add_ib<S>(u0, u2), od02 = add_ib<-S>(u0, u2);
+  float2 os13 = add_ib<S>(v1, v3), od13 = add_ib<-S>(v1, v3);
+  a[1] = cadd(os02, os13);
+  a[5] = csub(os02, os13);
+  a[3] = add_ib<S>(od02, od13);
+  a[7] = add_ib<-S>(od02, od13);
+}
+template <int R, int S>
+__device__ __forceinline__ void dft(float2* a) {
+  if constexpr (R == 8) dft8<S>(a);
+  else if constexpr (R == 4) dft4<S>(a);
+  else dft2<S>(a);
+}
+
+// ------------------------------------------------------------------ pass plan for size n
+template <int n>
+struct Plan {
+  static constexpr int P = (n == 32 || n == 64) ? 2 : (n == 1024 ? 4 : 3);
+  static constexpr int Rlast = (n == 32) ? 4 : (n == 128 ? 2 : (n == 256 ? 4 : (n == 1024 ? 2 : 8)));
+  template <int p> __host__ __device__ static constexpr int R() { return p == P - 1 ? Rlast : 8; }
+  template <int p> __host__ __device__ static constexpr int Ns() { return p == 0 ? 1 : (p == 1 ? 8 : (p == 2 ? 64 : 512)); }
+  static constexpr int NTW = 7;   // twiddles per thread per pass (nb * (R - 1) <= 7)
+  static_assert(n == 32 || n == 64 || n == 128 || n == 256 || n == 512 || n == 1024, "n");
+};
+
+// conflict-free swizzle of an element index inside one residue region (bijection on [0, n))
+__device__ __forceinline__ int swz(int e) { return e ^ ((e >> 4) & 15) ^ (((e >> 6) & 1) << 3); }
+
+// Twiddles of pass p for butterfly index j (S = -1: e^{-2pi i ...}, S = +1: conjugate).
+template <int n, int p, int S>
+__device__ __forceinline__ void load_tw(float2* tw, int j, const float2* __restrict__ tw_n) {
+  constexpr int R = Plan<n>::template R<p>();
+  constexpr int Ns = Plan<n>::template Ns<p>();
+  constexpr int nb = 8 / R;
+#pragma unroll
+  for (int u = 0; u < nb; ++u) {
+    const int jb = j * nb + u;
+    const int k = jb % Ns;
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      float2 w = __ldg(&tw_n[(k * r * (n / (Ns * R))) & (n - 1)]);
+      if (S > 0) w.y = -w.y;
+      tw[u * (R - 1) + r - 1] = w;
+    }
+  }
+}
+
+// One Stockham pass on registers v[8] of one residue: optional read from src (smem region),
+// twiddle (p > 0), DFT_R, optional write to dst (smem region).
+template <int n, int p, int S, bool READ, bool WRITE>
+__device__ __forceinline__ void pass(float2 (&v)[8], const float2* src, float2* dst, int j,
+                                     const float2* tw) {
+  constexpr int R = Plan<n>::template R<p>();
+  constexpr int Ns = Plan<n>::template Ns<p>();
+  constexpr int nb = 8 / R;
+  constexpr int stride = n / R;
+  if constexpr (READ) {
+#pragma unroll
+    for (int u = 0; u < nb; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[u * R + r] = src[swz(j * nb + u + r * stride)];
+  }
+  if constexpr (p > 0) {
+#pragma unroll
+    for (int u = 0; u < nb; ++u)
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[u * R + r] = cmul(v[u * R + r], tw[u * (R - 1) + r - 1]);
+  }
+#pragma unroll
+  for (int u = 0; u < nb; ++u) dft<R, S>(&v[u * R]);
+  if constexpr (WRITE) {
+#pragma unroll
+    for (int u = 0; u < nb; ++u) {
+      const int jb = j * nb + u;
+      const int base = (jb / Ns) * Ns * R + (jb % Ns);
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[swz(base + r * Ns)] = v[u * R + r];
+    }
+  }
+}
+
+// Output position (natural order) of register element e after the LAST pass.
+template <int n>
+__device__ __forceinline__ int last_pos(int j, int e) {
+  constexpr int R = Plan<n>::Rlast;
+  constexpr int nb = 8 / R;
+  return j * nb + e / R + (e % R) * (n / R);
+}
+
+}  // namespace fe
+}  // namespace tat

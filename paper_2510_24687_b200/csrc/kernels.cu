@@ -433,16 +433,14 @@ cudaError_t configure_kernels(const DevPlan& P) {
 #define SETSM(kern, bytes)                                                                   \
   if (e == cudaSuccess)                                                                      \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes));
-  SETSM(k1_row_dft, smem_ln2(C));
-  SETSM(k2_col_dft_gather, smem_k2(C));
+  if (e == cudaSuccess) e = configure_fft_kernels(C);
   SETSM(k3_angular_mult, smem_ring(C));
   SETSM(k4_dct, smem_dct(C));
   SETSM(k5_synth_restrict, smem_ring(C));
   SETSM(k5t_analysis, smem_ring(C));
   SETSM(k4t_dct, smem_dct(C));
   SETSM(k3t_angular, smem_ring(C));
-  SETSM(k2t_gather_col_idft, smem_ln2(C));
-  SETSM(k1t_row_idft, smem_ln2(C));
+
 #undef SETSM
   return e;
 }
@@ -453,9 +451,11 @@ cudaError_t launch_forward(const DevPlan& P, const float* f, float* g, cudaStrea
   const int B = C.batch;
   const int JT = tile_ring(C.n_ring);
   if (ev) cudaEventRecord(ev[0], s);
-  k1_row_dft<<<dim3(C.n / 2, B), kThreads, smem_ln2(C), s>>>(P, f);
+  cudaError_t e = launch_k1(P, f, s);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
-  k2_col_dft_gather<<<dim3((C.ncols + kK2Strip - 1) / kK2Strip, B), kThreads, smem_k2(C), s>>>(P);
+  e = launch_k2(P, s);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[2], s);
   k3_angular_mult<<<dim3((C.NL + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P);
   if (ev) cudaEventRecord(ev[3], s);
@@ -478,9 +478,11 @@ cudaError_t launch_adjoint(const DevPlan& P, const float* g, float* f, cudaStrea
   if (ev) cudaEventRecord(ev[2], s);
   k3t_angular<<<dim3((C.NL + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P);
   if (ev) cudaEventRecord(ev[3], s);
-  k2t_gather_col_idft<<<dim3(C.ncols, B), kThreads, smem_ln2(C), s>>>(P);
+  cudaError_t e = launch_k2t(P, s);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[4], s);
-  k1t_row_idft<<<dim3(C.n / 2, B), kThreads, smem_ln2(C), s>>>(P, f);
+  e = launch_k1t(P, f, s);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[5], s);
   return cudaGetLastError();
 }

@@ -77,6 +77,12 @@ cudaError_t launch_forward(const DevPlan& P, const float* f, float* g, cudaStrea
 cudaError_t launch_adjoint(const DevPlan& P, const float* g, float* f, cudaStream_t s,
                            cudaEvent_t* ev);
 cudaError_t configure_kernels(const DevPlan& P);   // smem attributes
+// kernels_fft.cu: residue-FFT kernels K1, K2, K2T, K1T
+cudaError_t configure_fft_kernels(const Consts& C);
+cudaError_t launch_k1(const DevPlan& P, const float* f, cudaStream_t s);
+cudaError_t launch_k2(const DevPlan& P, cudaStream_t s);
+cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s);
+cudaError_t launch_k1t(const DevPlan& P, float* f, cudaStream_t s);
 size_t max_smem_needed(const Consts& C);
 
 constexpr int kLaunchesForward = 5;
