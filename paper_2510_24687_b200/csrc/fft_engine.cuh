@@ -89,20 +89,25 @@ __device__ __forceinline__ void dft(float2* a) {
 // ------------------------------------------------------------------ pass plan for size n
 template <int n>
 struct Plan {
-  static constexpr int P = (n == 32 || n == 64) ? 2 : (n == 1024 ? 4 : 3);
-  static constexpr int Rlast = (n == 32) ? 4 : (n == 128 ? 2 : (n == 256 ? 4 : (n == 1024 ? 2 : 8)));
+  static constexpr int P = (n == 32 || n == 64) ? 2 : ((n >= 1024) ? 4 : 3);
+  static constexpr int Rlast =
+      (n == 32) ? 4 : (n == 128 ? 2 : (n == 256 ? 4 : (n == 1024 ? 2 : (n == 2048 ? 4 : 8))));
   template <int p> __host__ __device__ static constexpr int R() { return p == P - 1 ? Rlast : 8; }
   template <int p> __host__ __device__ static constexpr int Ns() { return p == 0 ? 1 : (p == 1 ? 8 : (p == 2 ? 64 : 512)); }
   static constexpr int NTW = 7;   // twiddles per thread per pass (nb * (R - 1) <= 7)
-  static_assert(n == 32 || n == 64 || n == 128 || n == 256 || n == 512 || n == 1024, "n");
+  static_assert(n == 32 || n == 64 || n == 128 || n == 256 || n == 512 || n == 1024 ||
+                    n == 2048 || n == 4096,
+                "n");
 };
 
 // conflict-free swizzle of an element index inside one residue region (bijection on [0, n))
 __device__ __forceinline__ int swz(int e) { return e ^ ((e >> 4) & 15) ^ (((e >> 6) & 1) << 3); }
 
 // Twiddles of pass p for butterfly index j (S = -1: e^{-2pi i ...}, S = +1: conjugate).
+// tw_n[stride * k] = exp(-2 pi i k / n) (stride > 1 when the table holds a multiple of n roots).
 template <int n, int p, int S>
-__device__ __forceinline__ void load_tw(float2* tw, int j, const float2* __restrict__ tw_n) {
+__device__ __forceinline__ void load_tw(float2* tw, int j, const float2* __restrict__ tw_n,
+                                        int stride = 1) {
   constexpr int R = Plan<n>::template R<p>();
   constexpr int Ns = Plan<n>::template Ns<p>();
   constexpr int nb = 8 / R;
@@ -112,7 +117,7 @@ __device__ __forceinline__ void load_tw(float2* tw, int j, const float2* __restr
     const int k = jb % Ns;
 #pragma unroll
     for (int r = 1; r < R; ++r) {
-      float2 w = __ldg(&tw_n[(k * r * (n / (Ns * R))) & (n - 1)]);
+      float2 w = __ldg(&tw_n[((k * r * (n / (Ns * R))) & (n - 1)) * stride]);
       if (S > 0) w.y = -w.y;
       tw[u * (R - 1) + r - 1] = w;
     }
@@ -151,6 +156,42 @@ __device__ __forceinline__ void pass(float2 (&v)[8], const float2* src, float2* 
       for (int r = 0; r < R; ++r) dst[swz(base + r * Ns)] = v[u * R + r];
     }
   }
+}
+
+// Per-thread twiddles of passes 1..P-1 (depend only on the butterfly index j).
+template <int n, int S>
+struct PassTw {
+  float2 tw[3][7];
+  __device__ __forceinline__ void load(int j, const float2* __restrict__ tw_n, int stride = 1) {
+    constexpr int P = Plan<n>::P;
+    if constexpr (P > 1) load_tw<n, 1, S>(tw[0], j, tw_n, stride);
+    if constexpr (P > 2) load_tw<n, 2, S>(tw[1], j, tw_n, stride);
+    if constexpr (P > 3) load_tw<n, 3, S>(tw[2], j, tw_n, stride);
+  }
+};
+
+// CTA-cooperative FFT of G = blockDim.x / (n/8) transforms stored in smem buffer A
+// ([G][n], element e of transform g at A[g*n + swz(e)], natural order), scratch B.
+// Output natural order; returns the buffer holding it.  Starts and ends with __syncthreads().
+template <int n, int S>
+__device__ __forceinline__ float2* cta_fft(float2* A, float2* B, const PassTw<n, S>& T) {
+  constexpr int P = Plan<n>::P;
+  const int g = threadIdx.x / (n / 8), j = threadIdx.x % (n / 8);
+  float2 v[8];
+  __syncthreads();
+  pass<n, 0, S, true, true>(v, A + g * n, B + g * n, j, nullptr);
+  __syncthreads();
+  pass<n, 1, S, true, true>(v, B + g * n, A + g * n, j, T.tw[0]);
+  __syncthreads();
+  if constexpr (P > 2) {
+    pass<n, 2, S, true, true>(v, A + g * n, B + g * n, j, T.tw[1]);
+    __syncthreads();
+  }
+  if constexpr (P > 3) {
+    pass<n, 3, S, true, true>(v, B + g * n, A + g * n, j, T.tw[2]);
+    __syncthreads();
+  }
+  return (P & 1) ? B : A;
 }
 
 // Output position (natural order) of register element e after the LAST pass.

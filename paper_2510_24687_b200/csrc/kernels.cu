@@ -106,8 +106,10 @@ constexpr int kThreads = 256;
 size_t max_smem_needed(const Consts& C) {
   size_t ln = (size_t)C.Lres * C.n * sizeof(float2);
   size_t s = 3 * ln;                                               // K2
-  s = std::max(s, (size_t)2 * 2 * C.M * sizeof(float2));           // K4 / K4T
-  s = std::max(s, (size_t)2 * tile_ring(C.n_ring) * C.n_ring * sizeof(float2));   // K3/K5
+  if (dct_fast_r(C)) s = std::max(s, smem_dct_fast(C));            // K4 / K4T
+  else s = std::max(s, (size_t)2 * 2 * C.M * sizeof(float2));
+  if (ring_fast_ok(C)) s = std::max(s, smem_ring_fast(C));           // K3/K5
+  else s = std::max(s, (size_t)2 * tile_ring(C.n_ring) * C.n_ring * sizeof(float2));
   return s;
 }
 
@@ -434,6 +436,8 @@ cudaError_t configure_kernels(const DevPlan& P) {
   if (e == cudaSuccess)                                                                      \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes));
   if (e == cudaSuccess) e = configure_fft_kernels(C);
+  if (e == cudaSuccess) e = configure_ring_kernels(C);
+  if (e == cudaSuccess) e = configure_dct_kernels(C);
   SETSM(k3_angular_mult, smem_ring(C));
   SETSM(k4_dct, smem_dct(C));
   SETSM(k5_synth_restrict, smem_ring(C));
@@ -457,11 +461,17 @@ cudaError_t launch_forward(const DevPlan& P, const float* f, float* g, cudaStrea
   e = launch_k2(P, s);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[2], s);
-  k3_angular_mult<<<dim3((C.NL + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P);
+  if (ring_fast_ok(C)) e = launch_k3(P, s);
+  else k3_angular_mult<<<dim3((C.NL + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[3], s);
-  k4_dct<<<dim3(C.Kp, B), kThreads, smem_dct(C), s>>>(P);
+  if (dct_fast_r(C)) e = launch_k4_fast(P, false, s);
+  else k4_dct<<<dim3(C.Kp, B), kThreads, smem_dct(C), s>>>(P);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[4], s);
-  k5_synth_restrict<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);
+  if (ring_fast_ok(C)) e = launch_k5(P, g, s);
+  else k5_synth_restrict<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[5], s);
   return cudaGetLastError();
 }
@@ -472,13 +482,20 @@ cudaError_t launch_adjoint(const DevPlan& P, const float* g, float* f, cudaStrea
   const int B = C.batch;
   const int JT = tile_ring(C.n_ring);
   if (ev) cudaEventRecord(ev[0], s);
-  k5t_analysis<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);
+  cudaError_t e = cudaSuccess;
+  if (ring_fast_ok(C)) e = launch_k5t(P, g, s);
+  else k5t_analysis<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
-  k4t_dct<<<dim3(C.Kp, B), kThreads, smem_dct(C), s>>>(P);
+  if (dct_fast_r(C)) e = launch_k4_fast(P, true, s);
+  else k4t_dct<<<dim3(C.Kp, B), kThreads, smem_dct(C), s>>>(P);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[2], s);
-  k3t_angular<<<dim3((C.NL + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P);
+  if (ring_fast_ok(C)) e = launch_k3t(P, s);
+  else k3t_angular<<<dim3((C.NL + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P);
+  if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[3], s);
-  cudaError_t e = launch_k2t(P, s);
+  e = launch_k2t(P, s);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[4], s);
   e = launch_k1t(P, f, s);

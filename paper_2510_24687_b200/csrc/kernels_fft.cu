@@ -22,17 +22,6 @@ struct Geo {
 };
 
 // ------------------------------------------------------------------ helpers
-template <int n, int S>
-struct PassTw {
-  float2 tw[3][7];
-  __device__ __forceinline__ void load(int j, const float2* __restrict__ tw_n) {
-    constexpr int P = Plan<n>::P;
-    if constexpr (P > 1) load_tw<n, 1, S>(tw[0], j, tw_n);
-    if constexpr (P > 2) load_tw<n, 2, S>(tw[1], j, tw_n);
-    if constexpr (P > 3) load_tw<n, 3, S>(tw[2], j, tw_n);
-  }
-};
-
 // Run passes 1..P-1 of the thread's residues, ping-ponging between b0 (holding the pass-0
 // output) and b1.  WLAST: write the last pass to smem (forward); otherwise the result stays in
 // registers at positions last_pos<n>(j, e).  Returns 0 if a written result ends in b0, 1 if in

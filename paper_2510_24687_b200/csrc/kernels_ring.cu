@@ -1,0 +1,241 @@
+// Angular-harmonic kernels on the register FFT engine (n_phi-point transforms):
+//
+//   K3   S2 [B][n_phi/2][NL] -> S3 [B][K+1][NL]  angular DFT (E:eq3) of the polar
+//        samples, completed from the half plane by P(phi + pi) = conj P(phi) (reading G12), times
+//        i^k m'[k][j] (E:eq2; 1/n_phi and h^2/2pi folded into m').
+//   K3T  S3 -> S2  transpose: P~[l] = sum_{k=-K}^{K-1} H~_k e^{i k phi_l} on the half plane, with
+//        H~_{-k} = (-1)^k conj(H~_k) and H~_{-K} = H~_K.
+//   K5   S4 [B][K+1][n_t] -> g [B][n_t][n_det]  C2R angular synthesis (E:FourSerForg)
+//        restricted to the detectors (Alg.1 steps 6-7); two time samples per complex FFT.
+//   K5T  g -> S4  zero-extension to the ring + R2C analysis (Alg.2 steps 1-2).
+//
+// Each CTA stages its tile through shared memory so that every global access is a contiguous
+// run along the fastest axis, then runs G transforms with cta_fft (G = blockDim.x / (n_phi/8)).
+#include "fft_engine.cuh"
+#include "tat_internal.h"
+
+namespace tat {
+
+using namespace fe;
+
+template <int nf>
+__host__ __device__ constexpr int ring_G() {
+  return (4096 / nf) < 16 ? (4096 / nf) : 16;   // transforms per CTA (<= 512 threads)
+}
+
+__device__ __forceinline__ float2 mul_ipow_(float2 a, int e) {
+  switch (e & 3) {
+    case 0: return a;
+    case 1: return make_float2(-a.y, a.x);
+    case 2: return make_float2(-a.x, -a.y);
+    default: return make_float2(a.y, -a.x);
+  }
+}
+
+// ------------------------------------------------------------------ K3
+template <int nf>
+__global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
+  extern __shared__ float2 sm[];
+  constexpr int G = ring_G<nf>();
+  const Consts& C = P.C;
+  const int NL = C.NL, half = nf / 2;
+  const int b = blockIdx.y, j0 = blockIdx.x * G;
+  float2* A = sm;
+  float2* B = sm + G * nf;
+  PassTw<nf, -1> T;
+  T.load(threadIdx.x % (nf / 8), P.tw_ring);
+  const float2* S2 = P.S2 + (size_t)b * half * NL;
+  for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
+    const int lp = idx / G, jj = idx - lp * G;
+    const float2 v = (j0 + jj < NL) ? S2[(size_t)lp * NL + j0 + jj] : make_float2(0.f, 0.f);
+    const int l = (lp - nf / 4) & (nf - 1);
+    A[jj * nf + swz(l)] = v;
+    A[jj * nf + swz((l + half) & (nf - 1))] = make_float2(v.x, -v.y);
+  }
+  const float2* X = cta_fft<nf, -1>(A, B, T);
+  float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
+  for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
+    const int k = idx / G, jj = idx - k * G, j = j0 + jj;
+    if (j < NL) {
+      const float m = __ldg(&P.mult[(size_t)k * NL + j]);
+      S3[(size_t)k * NL + j] = mul_ipow_(cscale(X[jj * nf + swz(k)], m), k);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K3T
+template <int nf>
+__global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
+  extern __shared__ float2 sm[];
+  constexpr int G = ring_G<nf>();
+  const Consts& C = P.C;
+  const int NL = C.NL, half = nf / 2, K = nf / 2;
+  const int b = blockIdx.y, j0 = blockIdx.x * G;
+  float2* A = sm;
+  float2* B = sm + G * nf;
+  PassTw<nf, 1> T;
+  T.load(threadIdx.x % (nf / 8), P.tw_ring);
+  const float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
+  for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
+    const int k = idx / G, jj = idx - k * G;
+    const float2 v = (j0 + jj < NL) ? S3[(size_t)k * NL + j0 + jj] : make_float2(0.f, 0.f);
+    A[jj * nf + swz(k)] = v;                       // k in [0, K]; slot K is k = -K
+    if (k >= 1 && k < K) {
+      const float sg = (k & 1) ? -1.f : 1.f;
+      A[jj * nf + swz(nf - k)] = make_float2(sg * v.x, -sg * v.y);
+    }
+  }
+  const float2* X = cta_fft<nf, 1>(A, B, T);
+  float2* S2 = P.S2 + (size_t)b * half * NL;
+  for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
+    const int lp = idx / G, jj = idx - lp * G;
+    if (j0 + jj < NL) {
+      const int l = (lp - nf / 4) & (nf - 1);
+      S2[(size_t)lp * NL + j0 + jj] = X[jj * nf + swz(l)];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K5
+// transform g carries time samples t0 + 2g (real part) and t0 + 2g + 1 (imaginary part)
+template <int nf>
+__global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ gout) {
+  extern __shared__ float2 sm[];
+  constexpr int G = ring_G<nf>();
+  const Consts& C = P.C;
+  const int K = nf / 2, n_t = C.n_t, n_det = C.n_det;
+  const int b = blockIdx.y, t0 = blockIdx.x * (2 * G);
+  float2* A = sm;
+  float2* B = sm + G * nf;
+  PassTw<nf, 1> T;
+  T.load(threadIdx.x % (nf / 8), P.tw_ring);
+  const float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
+  for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
+    const int k = idx / G, gg = idx - k * G;
+    const int t = t0 + 2 * gg;
+    const float2 v0 = (t < n_t) ? S4[(size_t)k * n_t + t] : make_float2(0.f, 0.f);
+    const float2 v1 = (t + 1 < n_t) ? S4[(size_t)k * n_t + t + 1] : make_float2(0.f, 0.f);
+    if (k >= 1 && k < K) {
+      A[gg * nf + swz(k)] = make_float2(v0.x - v1.y, v0.y + v1.x);          // v0 + i v1
+      A[gg * nf + swz(nf - k)] = make_float2(v0.x + v1.y, -v0.y + v1.x);   // conj v0 + i conj v1
+    } else {   // k = 0 and the Nyquist k = K enter through their real parts (C2R convention)
+      A[gg * nf + swz(k)] = make_float2(v0.x, v1.x);
+    }
+  }
+  const float2* X = cta_fft<nf, 1>(A, B, T);
+  const int tt_n = min(2 * G, n_t - t0);
+  for (int idx = threadIdx.x; idx < tt_n * n_det; idx += blockDim.x) {
+    const int tt = idx / n_det, d = idx - tt * n_det;
+    const float2 z = X[(tt >> 1) * nf + swz(__ldg(&P.ring[d]))];
+    gout[((size_t)b * n_t + t0 + tt) * n_det + d] = (tt & 1) ? z.y : z.x;
+  }
+}
+
+// ------------------------------------------------------------------ K5T
+template <int nf>
+__global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restrict__ gin) {
+  extern __shared__ float2 sm[];
+  constexpr int G = ring_G<nf>();
+  const Consts& C = P.C;
+  const int n_t = C.n_t, n_det = C.n_det;
+  const int b = blockIdx.y, t0 = blockIdx.x * (2 * G);
+  float2* A = sm;
+  float2* B = sm + G * nf;
+  PassTw<nf, -1> T;
+  T.load(threadIdx.x % (nf / 8), P.tw_ring);
+  for (int i = threadIdx.x; i < G * nf; i += blockDim.x) A[i] = make_float2(0.f, 0.f);
+  __syncthreads();
+  const int tt_n = min(2 * G, n_t - t0);
+  float* Af = reinterpret_cast<float*>(A);
+  for (int idx = threadIdx.x; idx < tt_n * n_det; idx += blockDim.x) {
+    const int tt = idx / n_det, d = idx - tt * n_det;
+    const float v = gin[((size_t)b * n_t + t0 + tt) * n_det + d];
+    Af[2 * ((tt >> 1) * nf + swz(__ldg(&P.ring[d]))) + (tt & 1)] = v;
+  }
+  const float2* X = cta_fft<nf, -1>(A, B, T);
+  float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
+  for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
+    const int k = idx / G, gg = idx - k * G;
+    const int t = t0 + 2 * gg;
+    const float2 zk = X[gg * nf + swz(k)];
+    const float2 zm = X[gg * nf + swz((nf - k) & (nf - 1))];
+    // even sample: (Z[k] + conj Z[-k]) / 2 ; odd sample: (Z[k] - conj Z[-k]) / (2i)
+    const float2 ge = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+    const float2 go = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+    if (t < n_t) S4[(size_t)k * n_t + t] = ge;
+    if (t + 1 < n_t) S4[(size_t)k * n_t + t + 1] = go;
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+bool ring_fast_ok(const Consts& C) { return C.n_ring >= 32 && C.n_ring <= 2048; }
+
+size_t smem_ring_fast(const Consts& C) {
+  const int nf = C.n_ring;
+  const int G = (4096 / nf) < 16 ? (4096 / nf) : 16;
+  return (size_t)2 * G * nf * sizeof(float2);
+}
+
+#define TAT_RING_SWITCH(...)                      \
+  switch (C.n_ring) {                              \
+    case 32: { constexpr int NF = 32; __VA_ARGS__; } break;     \
+    case 64: { constexpr int NF = 64; __VA_ARGS__; } break;     \
+    case 128: { constexpr int NF = 128; __VA_ARGS__; } break;   \
+    case 256: { constexpr int NF = 256; __VA_ARGS__; } break;   \
+    case 512: { constexpr int NF = 512; __VA_ARGS__; } break;   \
+    case 1024: { constexpr int NF = 1024; __VA_ARGS__; } break; \
+    case 2048: { constexpr int NF = 2048; __VA_ARGS__; } break; \
+    default: return cudaErrorInvalidValue;          \
+  }
+
+cudaError_t configure_ring_kernels(const Consts& C) {
+  if (!ring_fast_ok(C)) return cudaSuccess;
+  const int sm = (int)smem_ring_fast(C);
+  cudaError_t e = cudaSuccess;
+  TAT_RING_SWITCH({
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k3_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k3t_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5t_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  });
+  return e;
+}
+
+cudaError_t launch_k3(const DevPlan& P, cudaStream_t s) {
+  const Consts& C = P.C;
+  const size_t sm = smem_ring_fast(C);
+  TAT_RING_SWITCH({
+    constexpr int G = ring_G<NF>();
+    k3_ring<NF><<<dim3((C.NL + G - 1) / G, C.batch), G * NF / 8, sm, s>>>(P);
+  });
+  return cudaGetLastError();
+}
+cudaError_t launch_k3t(const DevPlan& P, cudaStream_t s) {
+  const Consts& C = P.C;
+  const size_t sm = smem_ring_fast(C);
+  TAT_RING_SWITCH({
+    constexpr int G = ring_G<NF>();
+    k3t_ring<NF><<<dim3((C.NL + G - 1) / G, C.batch), G * NF / 8, sm, s>>>(P);
+  });
+  return cudaGetLastError();
+}
+cudaError_t launch_k5(const DevPlan& P, float* g, cudaStream_t s) {
+  const Consts& C = P.C;
+  const size_t sm = smem_ring_fast(C);
+  TAT_RING_SWITCH({
+    constexpr int G = ring_G<NF>();
+    k5_ring<NF><<<dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), G * NF / 8, sm, s>>>(P, g);
+  });
+  return cudaGetLastError();
+}
+cudaError_t launch_k5t(const DevPlan& P, const float* g, cudaStream_t s) {
+  const Consts& C = P.C;
+  const size_t sm = smem_ring_fast(C);
+  TAT_RING_SWITCH({
+    constexpr int G = ring_G<NF>();
+    k5t_ring<NF><<<dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), G * NF / 8, sm, s>>>(P, g);
+  });
+  return cudaGetLastError();
+}
+
+}  // namespace tat

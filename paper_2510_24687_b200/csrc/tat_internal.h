@@ -83,6 +83,19 @@ cudaError_t launch_k1(const DevPlan& P, const float* f, cudaStream_t s);
 cudaError_t launch_k2(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k1t(const DevPlan& P, float* f, cudaStream_t s);
+// kernels_ring.cu: K3, K3T, K5, K5T on n_phi-point register FFTs
+bool ring_fast_ok(const Consts& C);
+size_t smem_ring_fast(const Consts& C);
+cudaError_t configure_ring_kernels(const Consts& C);
+cudaError_t launch_k3(const DevPlan& P, cudaStream_t s);
+cudaError_t launch_k3t(const DevPlan& P, cudaStream_t s);
+cudaError_t launch_k5(const DevPlan& P, float* g, cudaStream_t s);
+cudaError_t launch_k5t(const DevPlan& P, const float* g, cudaStream_t s);
+// kernels_dct.cu: K4, K4T as r residue FFTs of size 2M / r
+int dct_fast_r(const Consts& C);
+size_t smem_dct_fast(const Consts& C);
+cudaError_t configure_dct_kernels(const Consts& C);
+cudaError_t launch_k4_fast(const DevPlan& P, bool adj, cudaStream_t s);
 size_t max_smem_needed(const Consts& C);
 
 constexpr int kLaunchesForward = 5;
