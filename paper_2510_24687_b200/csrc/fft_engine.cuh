@@ -194,6 +194,78 @@ __device__ __forceinline__ float2* cta_fft(float2* A, float2* B, const PassTw<n,
   return (P & 1) ? B : A;
 }
 
+// ---- low-register variant: twiddles generated from one table value per butterfly
+// w^r for r = 1..7 from w by repeated multiplication (error ~3 ulp at r = 7).
+__device__ __forceinline__ void tw_powers(float2 w, float2* t) {   // t[0..6] = w^1..w^7
+  t[0] = w;
+  t[1] = cmul(w, w);
+  t[2] = cmul(t[1], w);
+  t[3] = cmul(t[1], t[1]);
+  t[4] = cmul(t[3], w);
+  t[5] = cmul(t[2], t[2]);
+  t[6] = cmul(t[3], t[2]);
+}
+
+// Same as pass<> but the twiddles of pass p (p > 0) are generated from tw_n on the fly.
+template <int n, int p, int S, bool READ, bool WRITE>
+__device__ __forceinline__ void pass_g(float2 (&v)[8], const float2* src, float2* dst, int j,
+                                       const float2* __restrict__ tw_n, int stride = 1) {
+  constexpr int R = Plan<n>::template R<p>();
+  constexpr int Ns = Plan<n>::template Ns<p>();
+  constexpr int nb = 8 / R;
+  constexpr int strd = n / R;
+  float2 wb[nb];
+  if constexpr (p > 0) {
+#pragma unroll
+    for (int u = 0; u < nb; ++u) {
+      const int k = (j * nb + u) % Ns;
+      float2 w = __ldg(&tw_n[((k * (n / (Ns * R))) & (n - 1)) * stride]);
+      if (S > 0) w.y = -w.y;
+      wb[u] = w;
+    }
+  }
+  if constexpr (READ) {
+#pragma unroll
+    for (int u = 0; u < nb; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[u * R + r] = src[swz(j * nb + u + r * strd)];
+  }
+  if constexpr (p > 0) {
+#pragma unroll
+    for (int u = 0; u < nb; ++u) {
+      if constexpr (R == 8) {
+        float2 t[7];
+        tw_powers(wb[u], t);
+#pragma unroll
+        for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], t[r - 1]);
+      } else if constexpr (R == 4) {
+        const float2 w2 = cmul(wb[u], wb[u]);
+        v[u * 4 + 1] = cmul(v[u * 4 + 1], wb[u]);
+        v[u * 4 + 2] = cmul(v[u * 4 + 2], w2);
+        v[u * 4 + 3] = cmul(v[u * 4 + 3], cmul(w2, wb[u]));
+      } else {
+        v[u * 2 + 1] = cmul(v[u * 2 + 1], wb[u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < nb; ++u) dft<R, S>(&v[u * R]);
+  if constexpr (WRITE) {
+#pragma unroll
+    for (int u = 0; u < nb; ++u) {
+      const int jb = j * nb + u;
+      const int base = (jb / Ns) * Ns * R + (jb % Ns);
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[swz(base + r * Ns)] = v[u * R + r];
+    }
+  }
+}
+
+// Named barrier over `count` threads (id 1..15; id 0 is __syncthreads).
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // Output position (natural order) of register element e after the LAST pass.
 template <int n>
 __device__ __forceinline__ int last_pos(int j, int e) {

@@ -113,97 +113,6 @@ size_t max_smem_needed(const Consts& C) {
   return s;
 }
 
-// ================================================================== forward kernels
-// K1: row pair (y, y+1) packed as z = f_y + i f_{y+1}; Z[p] = sum_x z[x] e^{-2 pi i p (x-n/2)/N}
-// for all p, as L residue FFTs; split into the two rows' half spectra p in [0, N/2].
-__global__ void k1_row_dft(DevPlan P, const float* __restrict__ f) {
-  extern __shared__ float2 sm[];
-  const Consts& C = P.C;
-  const int n = C.n, L = C.Lres, N = C.N;
-  const int b = blockIdx.y, y = 2 * blockIdx.x;
-  float2* A = sm;
-  float2* Bf = sm + (size_t)L * n;
-  const float* f0 = f + ((size_t)b * n + y) * n;
-  for (int idx = threadIdx.x; idx < L * n; idx += blockDim.x) {
-    int s = idx / n, yp = idx - s * n;
-    int x = (yp + n / 2) & (n - 1);
-    float2 z = make_float2(__ldg(&f0[x]), __ldg(&f0[n + x]));
-    A[idx] = cmul(z, __ldg(&P.tw_pre[idx]));
-  }
-  __syncthreads();
-  float2* X = smem_fft<-1>(A, Bf, n, L, P.tw_n);
-  float4* out = reinterpret_cast<float4*>(P.S1 + (size_t)b * C.ncols * n);
-  for (int p = threadIdx.x; p < C.ncols; p += blockDim.x) {
-    int pm = (N - p) & (N - 1);
-    float2 zp = X[(p % L) * n + p / L];
-    float2 zm = conjf2(X[(pm % L) * n + pm / L]);
-    float2 s = cadd(zp, zm), d = csub(zp, zm);
-    // row y: (zp + conj zm)/2 ; row y+1: (zp - conj zm)/(2i) = -i d / 2
-    out[((size_t)p * n + y) >> 1] = make_float4(0.5f * s.x, 0.5f * s.y, 0.5f * d.y, -0.5f * d.x);
-  }
-}
-
-// column DFT of S1 column p into smem: X[s*n + a] = F[p][q], q mod N = L a + s (unscaled)
-__device__ float2* column_dft(const DevPlan& P, const float2* __restrict__ col, float2* A,
-                              float2* Bf) {
-  const int n = P.C.n, L = P.C.Lres;
-  for (int idx = threadIdx.x; idx < L * n; idx += blockDim.x) {
-    int s = idx / n, yp = idx - s * n;
-    int y = (yp + n / 2) & (n - 1);
-    A[idx] = cmul(__ldg(&col[y]), __ldg(&P.tw_pre[idx]));
-  }
-  __syncthreads();
-  return smem_fft<-1>(A, Bf, n, L, P.tw_n);
-}
-
-__device__ __forceinline__ float2 fq(const float2* X, int q, int n, int L, int N) {
-  int qm = q & (N - 1);
-  return X[(qm % L) * n + qm / L];
-}
-
-// K2: strip of kK2Strip columns, sliding window of two column spectra (one halo recompute).
-__global__ void k2_col_dft_gather(DevPlan P) {
-  extern __shared__ float2 sm[];
-  const Consts& C = P.C;
-  const int n = C.n, L = C.Lres, N = C.N, ln = L * n;
-  const int b = blockIdx.y;
-  const int P0 = blockIdx.x * kK2Strip;
-  const int Pend = min(P0 + kK2Strip, C.ncols);           // owned p0 in [P0, Pend)
-  const float2* S1 = P.S1 + (size_t)b * C.ncols * n;
-  float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
-  float2* buf[3] = {sm, sm + ln, sm + 2 * ln};
-  int prev = -1;
-  const int plast = min(Pend, C.ncols - 1);                // last column to compute
-  for (int p = P0; p <= plast; ++p) {
-    int i0 = (prev + 1) % 3, i1 = (prev + 2) % 3;
-    float2* X = column_dft(P, S1 + (size_t)p * n, buf[i0], buf[i1]);
-    int cur = (X == buf[i0]) ? i0 : i1;
-    if (p > P0) {
-      const float2* Xa = buf[prev];
-      const float2* Xb = buf[cur];
-      for (int e = P.k2_colptr[p - 1] + threadIdx.x; e < P.k2_colptr[p]; e += blockDim.x) {
-        int4 nd = __ldg(&P.k2_nodes[e]);
-        float a = __int_as_float(nd.z), bb = __int_as_float(nd.w);
-        float2 f00 = fq(Xa, nd.y, n, L, N), f01 = fq(Xa, nd.y + 1, n, L, N);
-        float2 f10 = fq(Xb, nd.y, n, L, N), f11 = fq(Xb, nd.y + 1, n, L, N);
-        float2 c0 = make_float2((1.f - a) * f00.x + a * f10.x, (1.f - a) * f00.y + a * f10.y);
-        float2 c1 = make_float2((1.f - a) * f01.x + a * f11.x, (1.f - a) * f01.y + a * f11.y);
-        S2[nd.x] = make_float2((1.f - bb) * c0.x + bb * c1.x, (1.f - bb) * c0.y + bb * c1.y);
-      }
-    }
-    __syncthreads();
-    prev = cur;
-  }
-  if (Pend == C.ncols) {   // last column p0 = N/2: alpha == 0, only F[N/2] is used
-    const float2* Xa = buf[prev];
-    for (int e = P.k2_colptr[C.ncols - 1] + threadIdx.x; e < P.k2_colptr[C.ncols]; e += blockDim.x) {
-      int4 nd = __ldg(&P.k2_nodes[e]);
-      float bb = __int_as_float(nd.w);
-      float2 f00 = fq(Xa, nd.y, n, L, N), f01 = fq(Xa, nd.y + 1, n, L, N);
-      S2[nd.x] = make_float2((1.f - bb) * f00.x + bb * f01.x, (1.f - bb) * f00.y + bb * f01.y);
-    }
-  }
-}
 
 // K3: angular DFT over the full ring (half plane + conjugate mirror), times i^k m'[k][j].
 __global__ void k3_angular_mult(DevPlan P) {
@@ -217,7 +126,7 @@ __global__ void k3_angular_mult(DevPlan P) {
   const float2* S2 = P.S2 + (size_t)b * half * NL;
   for (int idx = threadIdx.x; idx < half * JT; idx += blockDim.x) {
     int lp = idx / JT, jj = idx - lp * JT;
-    float2 v = (jj < jt) ? S2[(size_t)lp * NL + j0 + jj] : make_float2(0.f, 0.f);
+    float2 v = (jj < jt) ? S2[P.node_perm[(size_t)(j0 + jj) * half + lp]] : make_float2(0.f, 0.f);
     int l = (lp - nphi / 4) & (nphi - 1);
     A[jj * nphi + l] = v;
     A[jj * nphi + ((l + half) & (nphi - 1))] = conjf2(v);
@@ -347,86 +256,12 @@ __global__ void k3t_angular(DevPlan P) {
     int lp = idx / JT, jj = idx - lp * JT;
     if (jj >= jt) continue;
     int l = (lp - nphi / 4) & (nphi - 1);
-    S2[(size_t)lp * NL + j0 + jj] = X[jj * nphi + l];
-  }
-}
-
-// K2T: per column p: R[q] = sum of w * P~ over the CSR (deterministic order), then
-// S~1[y][p] = sum_q R[q] e^{+2 pi i q (y-n/2)/N} via L inverse residue FFTs.
-__global__ void k2t_gather_col_idft(DevPlan P) {
-  extern __shared__ float2 sm[];
-  const Consts& C = P.C;
-  const int n = C.n, L = C.Lres, ln = L * n;
-  const int b = blockIdx.y, p = blockIdx.x;
-  float2* A = sm;
-  float2* Bf = sm + ln;
-  const float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
-  for (int i = threadIdx.x; i < ln; i += blockDim.x) A[i] = make_float2(0.f, 0.f);
-  __syncthreads();
-  for (int t = P.k2t_colptr[p] + threadIdx.x; t < P.k2t_colptr[p + 1]; t += blockDim.x) {
-    int qm = __ldg(&P.k2t_tq[t]);
-    float2 acc = make_float2(0.f, 0.f);
-    for (int e = __ldg(&P.k2t_tstart[t]); e < __ldg(&P.k2t_tstart[t + 1]); ++e) {
-      int2 en = __ldg(&P.k2t_ent[e]);
-      float w = __int_as_float(en.y);
-      float2 v = S2[en.x];
-      acc.x = fmaf(w, v.x, acc.x);
-      acc.y = fmaf(w, v.y, acc.y);
-    }
-    A[(qm % L) * n + qm / L] = acc;
-  }
-  __syncthreads();
-  float2* X = smem_fft<1>(A, Bf, n, L, P.tw_n);
-  float2* out = P.S1 + ((size_t)b * C.ncols + p) * n;
-  for (int y = threadIdx.x; y < n; y += blockDim.x) {
-    int yp = (y + n / 2) & (n - 1);
-    float2 acc = make_float2(0.f, 0.f);
-    for (int s = 0; s < L; ++s)
-      acc = cadd(acc, cmulc(X[s * n + yp], __ldg(&P.tw_pre[s * n + yp])));
-    out[y] = acc;
-  }
-}
-
-// K1T: rows (y, y+1) from their half spectra (Hermitian completion, C[0] and C[N/2] = 2 Re),
-// packed Z = C_y + i C_{y+1}; f~_y + i f~_{y+1} = sum_p Z[p] e^{+2 pi i p (x-n/2)/N}.
-__global__ void k1t_row_idft(DevPlan P, float* __restrict__ fout) {
-  extern __shared__ float2 sm[];
-  const Consts& C = P.C;
-  const int n = C.n, L = C.Lres, N = C.N, ln = L * n;
-  const int b = blockIdx.y, y = 2 * blockIdx.x;
-  float2* A = sm;
-  float2* Bf = sm + ln;
-  const float4* in = reinterpret_cast<const float4*>(P.S1 + (size_t)b * C.ncols * n);
-  for (int p = threadIdx.x; p < C.ncols; p += blockDim.x) {
-    float4 v = in[((size_t)p * n + y) >> 1];        // (S~1[y][p], S~1[y+1][p])
-    float2 cy = make_float2(v.x, v.y), cy1 = make_float2(v.z, v.w);
-    if (p == 0 || p == N / 2) {
-      float2 z = make_float2(2.f * cy.x, 2.f * cy1.x);    // 2Re + i 2Re
-      A[(p % L) * n + p / L] = z;
-    } else {
-      // Z[p] = cy + i cy1 ; Z[N-p] = conj(cy) + i conj(cy1)
-      A[(p % L) * n + p / L] = make_float2(cy.x - cy1.y, cy.y + cy1.x);
-      int pm = N - p;
-      A[(pm % L) * n + pm / L] = make_float2(cy.x + cy1.y, -cy.y + cy1.x);
-    }
-  }
-  __syncthreads();
-  float2* X = smem_fft<1>(A, Bf, n, L, P.tw_n);
-  float* o0 = fout + ((size_t)b * n + y) * n;
-  for (int x = threadIdx.x; x < n; x += blockDim.x) {
-    int xp = (x + n / 2) & (n - 1);
-    float2 acc = make_float2(0.f, 0.f);
-    for (int s = 0; s < L; ++s)
-      acc = cadd(acc, cmulc(X[s * n + xp], __ldg(&P.tw_pre[s * n + xp])));
-    o0[x] = acc.x;
-    o0[n + x] = acc.y;
+    S2[P.node_perm[(size_t)(j0 + jj) * half + lp]] = X[jj * nphi + l];
   }
 }
 
 // ================================================================== launchers
 static size_t smem_ring(const Consts& C) { return (size_t)2 * tile_ring(C.n_ring) * C.n_ring * sizeof(float2); }
-static size_t smem_ln2(const Consts& C) { return (size_t)2 * C.Lres * C.n * sizeof(float2); }
-static size_t smem_k2(const Consts& C) { return (size_t)3 * C.Lres * C.n * sizeof(float2); }
 static size_t smem_dct(const Consts& C) { return (size_t)2 * 2 * C.M * sizeof(float2); }
 
 cudaError_t configure_kernels(const DevPlan& P) {

@@ -46,8 +46,9 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
   T.load(threadIdx.x % (nf / 8), P.tw_ring);
   const float2* S2 = P.S2 + (size_t)b * half * NL;
   for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
-    const int lp = idx / G, jj = idx - lp * G;
-    const float2 v = (j0 + jj < NL) ? S2[(size_t)lp * NL + j0 + jj] : make_float2(0.f, 0.f);
+    const int jj = idx / half, lp = idx - jj * half;   // S2 is in K2 node order: gather by perm
+    const float2 v = (j0 + jj < NL) ? S2[__ldg(&P.node_perm[(size_t)(j0 + jj) * half + lp])]
+                                    : make_float2(0.f, 0.f);
     const int l = (lp - nf / 4) & (nf - 1);
     A[jj * nf + swz(l)] = v;
     A[jj * nf + swz((l + half) & (nf - 1))] = make_float2(v.x, -v.y);
@@ -88,10 +89,10 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
   const float2* X = cta_fft<nf, 1>(A, B, T);
   float2* S2 = P.S2 + (size_t)b * half * NL;
   for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
-    const int lp = idx / G, jj = idx - lp * G;
+    const int jj = idx / half, lp = idx - jj * half;
     if (j0 + jj < NL) {
       const int l = (lp - nf / 4) & (nf - 1);
-      S2[(size_t)lp * NL + j0 + jj] = X[jj * nf + swz(l)];
+      S2[__ldg(&P.node_perm[(size_t)(j0 + jj) * half + lp])] = X[jj * nf + swz(l)];
     }
   }
 }

@@ -110,6 +110,7 @@ std::string gpu_support(const Consts& C) {
   if (!smooth23(2L * C.M)) return fmt("2M=%g is not of the form 2^a 3^b", 2.0 * C.M);
   if (C.NL > 2 * C.M) return "J+1 > 2M (time step coarser than twice the pixel pitch)";
   if (C.n_t > 2 * C.M - 1) return "n_t too large for the DCT length";
+  if ((long)C.Lres * C.n > 8192) return fmt("L n = %g > 8192 (threads per CTA)", (double)C.Lres * C.n);
   if (max_smem_needed(C) > 227 * 1024) return fmt("shared memory need %g KB > 227 KB",
                                                   max_smem_needed(C) / 1024.0);
   return "";
@@ -219,11 +220,14 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
       q0v[i] = (int)fv; bv[i] = v - fv;
     }
   }
-  // K2 forward: counting sort by p0, stable in (l', j)
+  // K2 forward: counting sort by p0, stable in (l', j).  S2 is stored in this node order
+  // (K2 writes it contiguously); node_perm maps (j, l') -> sorted position for K3 / K3T.
   H.k2_colptr.assign(C.ncols + 1, 0);
   for (long i = 0; i < nodes; ++i) H.k2_colptr[p0v[i] + 1]++;
   for (int p = 0; p < C.ncols; ++p) H.k2_colptr[p + 1] += H.k2_colptr[p];
   H.k2_nodes.resize(nodes);
+  H.node_perm.assign(nodes, 0);
+  std::vector<int> sorted_pos(nodes);
   {
     std::vector<int> pos(H.k2_colptr.begin(), H.k2_colptr.end() - 1);
     for (long i = 0; i < nodes; ++i) {
@@ -232,7 +236,11 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
       e.y = q0v[i];
       e.z = fbits((float)av[i]);
       e.w = fbits((float)bv[i]);
-      H.k2_nodes[pos[p0v[i]]++] = e;
+      const int sp = pos[p0v[i]]++;
+      H.k2_nodes[sp] = e;
+      sorted_pos[i] = sp;
+      const int lp = (int)(i / NL), j = (int)(i % NL);
+      H.node_perm[(size_t)j * half + lp] = sp;
     }
   }
   // K2T: entries (p, q mod N, src, w) for corners with non-zero weight; group by (p, q)
@@ -248,7 +256,7 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
     for (int c4 = 0; c4 < 4; ++c4) {
       if (w[c4] == 0.0) continue;
       int qm = ((qq[c4] % N) + N) % N;
-      ent.push_back({pp[c4], qm, (int)i, (float)w[c4]});
+      ent.push_back({pp[c4], qm, sorted_pos[i], (float)w[c4]});
     }
   }
   // two-pass stable counting sort: by q, then by p

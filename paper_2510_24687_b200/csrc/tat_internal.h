@@ -32,12 +32,13 @@ struct HostTables {
   std::vector<float2> tw_dct;       // 2M roots
   // K2 forward gather: half-plane nodes sorted by p0
   std::vector<int> k2_colptr;       // [ncols + 1]
-  std::vector<int4> k2_nodes;       // (target = l'*NL + j, q0, alpha bits, beta bits)
+  std::vector<int4> k2_nodes;       // (l'*NL + j, q0, alpha bits, beta bits), sorted by p0
+  std::vector<int> node_perm;       // [NL][n_ring/2]: (j, l') -> position in the sorted order
   // K2T transposed gather: per column p, targets (q mod N) with entry ranges
   std::vector<int> k2t_colptr;      // [ncols + 1] into targets
   std::vector<int> k2t_tq;          // [T] q mod N
   std::vector<int> k2t_tstart;      // [T + 1] into entries
-  std::vector<int2> k2t_ent;        // [E] (src target index, weight bits)
+  std::vector<int2> k2t_ent;        // [E] (src sorted node position, weight bits)
   std::vector<int> ring;            // [n_det]
 };
 
@@ -59,6 +60,7 @@ struct DevPlan {
   const float2* tw_dct = nullptr;
   const int* k2_colptr = nullptr;
   const int4* k2_nodes = nullptr;
+  const int* node_perm = nullptr;
   const int* k2t_colptr = nullptr;
   const int* k2t_tq = nullptr;
   const int* k2t_tstart = nullptr;
@@ -66,7 +68,7 @@ struct DevPlan {
   const int* ring = nullptr;
   // workspace
   float2* S1 = nullptr;   // [B][ncols][n]
-  float2* S2 = nullptr;   // [B][half][NL]
+  float2* S2 = nullptr;   // [B][half * NL] in K2 node order (sorted by p0)
   float2* S3 = nullptr;   // [B][Kp][NL]
   float2* S4 = nullptr;   // [B][Kp][n_t]
 };
