@@ -206,7 +206,16 @@ __device__ __forceinline__ void tw_powers(float2 w, float2* t) {   // t[0..6] = 
   t[6] = cmul(t[3], t[2]);
 }
 
-// Same as pass<> but the twiddles of pass p (p > 0) are generated from tw_n on the fly.
+// ---- padded layout: element e of a region lives at e + (e >> 4) (one pad slot per 16).
+// Every access pattern of a pass is phys(base) + compile-time offset (no carries out of the
+// low 4 bits), so a pass needs one address computation per butterfly.
+__host__ __device__ constexpr int padded(int n) { return n + n / 16; }
+__device__ __forceinline__ int phys(int e) { return e + (e >> 4); }
+template <int c>
+__device__ __forceinline__ constexpr int poff() { return c + (c >> 4); }
+
+// Stockham pass p of one n-point transform (8 points per thread, padded smem layout);
+// twiddles of p > 0 generated from one table value per butterfly.
 template <int n, int p, int S, bool READ, bool WRITE>
 __device__ __forceinline__ void pass_g(float2 (&v)[8], const float2* src, float2* dst, int j,
                                        const float2* __restrict__ tw_n, int stride = 1) {
@@ -226,9 +235,11 @@ __device__ __forceinline__ void pass_g(float2 (&v)[8], const float2* src, float2
   }
   if constexpr (READ) {
 #pragma unroll
-    for (int u = 0; u < nb; ++u)
+    for (int u = 0; u < nb; ++u) {
+      const float2* sb = src + phys(j * nb + u);
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[u * R + r] = src[swz(j * nb + u + r * strd)];
+      for (int r = 0; r < R; ++r) v[u * R + r] = sb[r * strd + ((r * strd) >> 4)];
+    }
   }
   if constexpr (p > 0) {
 #pragma unroll
@@ -254,9 +265,9 @@ __device__ __forceinline__ void pass_g(float2 (&v)[8], const float2* src, float2
 #pragma unroll
     for (int u = 0; u < nb; ++u) {
       const int jb = j * nb + u;
-      const int base = (jb / Ns) * Ns * R + (jb % Ns);
+      float2* db = dst + phys((jb / Ns) * Ns * R + (jb % Ns));
 #pragma unroll
-      for (int r = 0; r < R; ++r) dst[swz(base + r * Ns)] = v[u * R + r];
+      for (int r = 0; r < R; ++r) db[r * Ns + ((r * Ns) >> 4)] = v[u * R + r];
     }
   }
 }

@@ -104,8 +104,7 @@ constexpr int kK2Strip = 16;
 constexpr int kThreads = 256;
 
 size_t max_smem_needed(const Consts& C) {
-  size_t ln = (size_t)C.Lres * C.n * sizeof(float2);
-  size_t s = 3 * ln;                                               // K2
+  size_t s = smem_fft4(C);                                         // K1/K2/K2T/K1T
   if (dct_fast_r(C)) s = std::max(s, smem_dct_fast(C));            // K4 / K4T
   else s = std::max(s, (size_t)2 * 2 * C.M * sizeof(float2));
   if (ring_fast_ok(C)) s = std::max(s, smem_ring_fast(C));           // K3/K5

@@ -54,24 +54,27 @@ template <int n>
 __global__ void __launch_bounds__(1024) k2_fwd(DevPlan P) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
-  const int L = C.Lres, ln = L * n, N = C.N;
+  constexpr int pn = padded(n);
+  const int L = C.Lres, ln = L * pn, N = C.N;
   const int b = blockIdx.y;
   const int P0 = blockIdx.x * kStrip;
   const int Pend = min(P0 + kStrip, C.ncols);
   const int plast = min(Pend, C.ncols - 1);
   const int g = threadIdx.x / (n / 8), j = threadIdx.x % (n / 8);
-  const int so = g * n;
+  const int so = g * pn;
   float2 pre[8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) pre[r] = __ldg(&P.tw_pre[so + j + r * (n / 8)]);
+  for (int r = 0; r < 8; ++r) pre[r] = __ldg(&P.tw_pre[g * n + j + r * (n / 8)]);
   const float2* S1 = P.S1 + (size_t)b * C.ncols * n;
   float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
   int prev = 2;
   for (int p = P0; p <= plast; ++p) {
     const float2* col = S1 + (size_t)p * n;
     float2 v[8];
+    // FFT slot y' = j + r n/8 holds sample y = (y' + n/2) mod n
 #pragma unroll
-    for (int r = 0; r < 8; ++r) v[r] = cmul(__ldg(&col[(j + r * (n / 8) + n / 2) & (n - 1)]), pre[r]);
+    for (int r = 0; r < 8; ++r)
+      v[r] = cmul(__ldg(&col[j + (r < 4 ? n / 2 + r * (n / 8) : (r - 4) * (n / 8))]), pre[r]);
     const int i0 = prev == 0 ? 1 : 0, i1 = prev == 2 ? 1 : 2;
     float2* X = sm + i0 * ln;
     float2* Y = sm + i1 * ln;
@@ -86,8 +89,8 @@ __global__ void __launch_bounds__(1024) k2_fwd(DevPlan P) {
         const int4 nd = __ldg(&P.k2_nodes[e]);
         const float a = __int_as_float(nd.z), bb = __int_as_float(nd.w);
         const int q0 = nd.y & (N - 1), q1 = (nd.y + 1) & (N - 1);
-        const int i00 = (q0 & (L - 1)) * n + swz(q0 / L);
-        const int i01 = (q1 & (L - 1)) * n + swz(q1 / L);
+        const int i00 = (q0 & (L - 1)) * pn + phys(q0 / L);
+        const int i01 = (q1 & (L - 1)) * pn + phys(q1 / L);
         const float2 f00 = Xa[i00], f01 = Xa[i01], f10 = Xb[i00], f11 = Xb[i01];
         const float2 c0 = __ffma2_rn(make_float2(a, a), csub(f10, f00), f00);
         const float2 c1 = __ffma2_rn(make_float2(a, a), csub(f11, f01), f01);
@@ -103,8 +106,8 @@ __global__ void __launch_bounds__(1024) k2_fwd(DevPlan P) {
       const int4 nd = __ldg(&P.k2_nodes[e]);
       const float bb = __int_as_float(nd.w);
       const int q0 = nd.y & (N - 1), q1 = (nd.y + 1) & (N - 1);
-      const float2 f00 = Xa[(q0 & (L - 1)) * n + swz(q0 / L)];
-      const float2 f01 = Xa[(q1 & (L - 1)) * n + swz(q1 / L)];
+      const float2 f00 = Xa[(q0 & (L - 1)) * pn + phys(q0 / L)];
+      const float2 f01 = Xa[(q1 & (L - 1)) * pn + phys(q1 / L)];
       S2[e] = __ffma2_rn(make_float2(bb, bb), csub(f01, f00), f00);
     }
   }
@@ -117,13 +120,14 @@ template <int n>
 __global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const float* __restrict__ f) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
-  const int L = C.Lres, ln = L * n, N = C.N;
+  constexpr int pn = padded(n);
+  const int L = C.Lres, ln = L * pn, N = C.N;
   const int b = blockIdx.y, y0 = 4 * blockIdx.x;
   const int g = threadIdx.x / (n / 8), j = threadIdx.x % (n / 8);
-  const int so = g * n;
+  const int so = g * pn;
   float2 pre[8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) pre[r] = __ldg(&P.tw_pre[so + j + r * (n / 8)]);
+  for (int r = 0; r < 8; ++r) pre[r] = __ldg(&P.tw_pre[g * n + j + r * (n / 8)]);
   float2* ZA = nullptr;
   float2* ZB = nullptr;
 #pragma unroll 1
@@ -132,7 +136,7 @@ __global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const float* __restric
     float2 v[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const int xi = (j + r * (n / 8) + n / 2) & (n - 1);
+      const int xi = j + (r < 4 ? n / 2 + r * (n / 8) : (r - 4) * (n / 8));
       v[r] = cmul(make_float2(__ldg(&r0[xi]), __ldg(&r0[n + xi])), pre[r]);
     }
     float2* b0 = pr == 0 ? sm : sm + 2 * ln;
@@ -146,8 +150,8 @@ __global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const float* __restric
   float4* out = reinterpret_cast<float4*>(P.S1 + (size_t)b * C.ncols * n);
   for (int p = threadIdx.x; p < C.ncols; p += blockDim.x) {
     const int pm = (N - p) & (N - 1);
-    const int ip = (p & (L - 1)) * n + swz(p / L);
-    const int im = (pm & (L - 1)) * n + swz(pm / L);
+    const int ip = (p & (L - 1)) * pn + phys(p / L);
+    const int im = (pm & (L - 1)) * pn + phys(pm / L);
     const float2 za = ZA[ip], zam = ZA[im], zb = ZB[ip], zbm = ZB[im];
     // row y: (Z[p] + conj Z[-p]) / 2 ; row y+1: (Z[p] - conj Z[-p]) / (2 i)
     float4 o0, o1;
@@ -168,15 +172,16 @@ template <int n>
 __global__ void __launch_bounds__(1024) k2t_adj(DevPlan P) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
-  const int L = C.Lres, ln = L * n;
+  constexpr int pn = padded(n);
+  const int L = C.Lres, ln = L * pn;
   const int b = blockIdx.y;
   const int P0 = blockIdx.x * kStrip;
   const int Pend = min(P0 + kStrip, C.ncols);
   const int g = threadIdx.x / (n / 8), j = threadIdx.x % (n / 8);
-  const int so = g * n;
+  const int so = g * pn;
   float2 post[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) post[e] = __ldg(&P.tw_pre[so + last_pos<n>(j, e)]);
+  for (int e = 0; e < 8; ++e) post[e] = __ldg(&P.tw_pre[g * n + last_pos<n>(j, e)]);
   const float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
   float2* out = P.S1 + (size_t)b * C.ncols * n;
   float2* R = sm;            // gather target (kept zero outside the CSR targets)
@@ -193,16 +198,18 @@ __global__ void __launch_bounds__(1024) k2t_adj(DevPlan P) {
         const int2 en = __ldg(&P.k2t_ent[e]);
         acc = __ffma2_rn(make_float2(__int_as_float(en.y), __int_as_float(en.y)), __ldg(&S2[en.x]), acc);
       }
-      R[(qm & (L - 1)) * n + swz(qm / L)] = acc;
+      R[(qm & (L - 1)) * pn + phys(qm / L)] = acc;
     }
     __syncthreads();
     float2 v[8];
     // pass 0 reads R and re-zeroes what it read (each element is read by exactly one thread)
+    {
+      float2* a = R + so + phys(j);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      float2* a = R + so + swz(j + r * (n / 8));
-      v[r] = *a;
-      *a = make_float2(0.f, 0.f);
+      for (int r = 0; r < 8; ++r) {
+        v[r] = a[r * (n / 8) + ((r * (n / 8)) >> 4)];
+        a[r * (n / 8) + ((r * (n / 8)) >> 4)] = make_float2(0.f, 0.f);
+      }
     }
     pass_g<n, 0, 1, false, true>(v, nullptr, Xb + so, j, P.tw_n);
     passes_g<n, 1, false>(v, Xb + so, red + so, j, g, L, P.tw_n);   // result in registers
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(1024) k2t_adj(DevPlan P) {
     __syncthreads();
     for (int yp = threadIdx.x; yp < n; yp += blockDim.x) {
       float2 acc = red[yp];
-      for (int gg = 1; gg < L; ++gg) acc = cadd(acc, red[gg * n + yp]);
+      for (int gg = 1; gg < L; ++gg) acc = cadd(acc, red[gg * pn + yp]);
       out[(size_t)p * n + ((yp + n / 2) & (n - 1))] = acc;
     }
     __syncthreads();
@@ -226,13 +233,14 @@ template <int n>
 __global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, float* __restrict__ fout) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
-  const int L = C.Lres, ln = L * n, N = C.N;
+  constexpr int pn = padded(n);
+  const int L = C.Lres, ln = L * pn, N = C.N;
   const int b = blockIdx.y, y0 = 4 * blockIdx.x;
   const int g = threadIdx.x / (n / 8), j = threadIdx.x % (n / 8);
-  const int so = g * n;
+  const int so = g * pn;
   float2 post[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) post[e] = __ldg(&P.tw_pre[so + last_pos<n>(j, e)]);
+  for (int e = 0; e < 8; ++e) post[e] = __ldg(&P.tw_pre[g * n + last_pos<n>(j, e)]);
   float2* ZA = sm;
   float2* ZB = sm + ln;
   float2* X = sm + 2 * ln;
@@ -240,13 +248,13 @@ __global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, float* __restrict__ f
   for (int p = threadIdx.x; p < C.ncols; p += blockDim.x) {
     const float4* src = in + (((size_t)p * n + y0) >> 1);
     const float4 v0 = src[0], v1 = src[1];   // rows y0, y0+1 | y0+2, y0+3
-    const int ip = (p & (L - 1)) * n + swz(p / L);
+    const int ip = (p & (L - 1)) * pn + phys(p / L);
     if (p == 0 || p == N / 2) {
       ZA[ip] = make_float2(2.f * v0.x, 2.f * v0.z);
       ZB[ip] = make_float2(2.f * v1.x, 2.f * v1.z);
     } else {
       const int pm = N - p;
-      const int im = (pm & (L - 1)) * n + swz(pm / L);
+      const int im = (pm & (L - 1)) * pn + phys(pm / L);
       ZA[ip] = make_float2(v0.x - v0.w, v0.y + v0.z);
       ZA[im] = make_float2(v0.x + v0.w, -v0.y + v0.z);
       ZB[ip] = make_float2(v1.x - v1.w, v1.y + v1.z);
@@ -268,7 +276,7 @@ __global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, float* __restrict__ f
     float* o = fout + ((size_t)b * n + y0 + 2 * pr) * n;
     for (int xp = threadIdx.x; xp < n; xp += blockDim.x) {
       float2 acc = red[xp];
-      for (int gg = 1; gg < L; ++gg) acc = cadd(acc, red[gg * n + xp]);
+      for (int gg = 1; gg < L; ++gg) acc = cadd(acc, red[gg * pn + xp]);
       const int x = (xp + n / 2) & (n - 1);
       o[x] = acc.x;
       o[n + x] = acc.y;
@@ -278,13 +286,13 @@ __global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, float* __restrict__ f
 }
 
 // ================================================================== dispatch
-size_t smem_fft4(const Consts& C) { return (size_t)3 * C.Lres * C.n * sizeof(float2); }
+size_t smem_fft4(const Consts& C) { return (size_t)3 * C.Lres * (C.n + C.n / 16) * sizeof(float2); }
 int fft_threads(const Consts& C) { return C.Lres * (C.n / 8); }
 
 template <int n>
 static cudaError_t cfg_one() {
   cudaError_t e = cudaSuccess;
-  const int big = 3 * 16 * n * (int)sizeof(float2);
+  const int big = 3 * 16 * padded(n) * (int)sizeof(float2);
   const int lim = big > 227 * 1024 ? 227 * 1024 : big;
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k2_fwd<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k1_fwd<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);

@@ -81,6 +81,7 @@ cudaError_t launch_adjoint(const DevPlan& P, const float* g, float* f, cudaStrea
 cudaError_t configure_kernels(const DevPlan& P);   // smem attributes
 // kernels_fft.cu: residue-FFT kernels K1, K2, K2T, K1T
 cudaError_t configure_fft_kernels(const Consts& C);
+size_t smem_fft4(const Consts& C);
 cudaError_t launch_k1(const DevPlan& P, const float* f, cudaStream_t s);
 cudaError_t launch_k2(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s);
