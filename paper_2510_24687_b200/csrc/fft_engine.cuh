@@ -210,14 +210,17 @@ __device__ __forceinline__ void tw_powers(float2 w, float2* t) {   // t[0..6] = 
 // Every access pattern of a pass is phys(base) + compile-time offset (no carries out of the
 // low 4 bits), so a pass needs one address computation per butterfly.
 __host__ __device__ constexpr int padded(int n) { return n + n / 16; }
+// stride between residue regions: padded(n) rounded up to 2 mod 16 (8-byte words), so that
+// accesses running across residues (consecutive q = L a + s) hit distinct bank pairs
+__host__ __device__ constexpr int rstride(int n) { return padded(n) + ((18 - padded(n) % 16) % 16); }
 __device__ __forceinline__ int phys(int e) { return e + (e >> 4); }
 template <int c>
 __device__ __forceinline__ constexpr int poff() { return c + (c >> 4); }
 
 // Stockham pass p of one n-point transform (8 points per thread, padded smem layout);
 // twiddles of p > 0 generated from one table value per butterfly.
-template <int n, int p, int S, bool READ, bool WRITE>
-__device__ __forceinline__ void pass_g(float2 (&v)[8], const float2* src, float2* dst, int j,
+template <int n, int p, int S, bool READ, bool WRITE, bool ZERO = false>
+__device__ __forceinline__ void pass_g(float2 (&v)[8], float2* src, float2* dst, int j,
                                        const float2* __restrict__ tw_n, int stride = 1) {
   constexpr int R = Plan<n>::template R<p>();
   constexpr int Ns = Plan<n>::template Ns<p>();
@@ -236,9 +239,12 @@ __device__ __forceinline__ void pass_g(float2 (&v)[8], const float2* src, float2
   if constexpr (READ) {
 #pragma unroll
     for (int u = 0; u < nb; ++u) {
-      const float2* sb = src + phys(j * nb + u);
+      float2* sb = src + phys(j * nb + u);
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[u * R + r] = sb[r * strd + ((r * strd) >> 4)];
+      for (int r = 0; r < R; ++r) {
+        v[u * R + r] = sb[r * strd + ((r * strd) >> 4)];
+        if constexpr (ZERO) sb[r * strd + ((r * strd) >> 4)] = make_float2(0.f, 0.f);
+      }
     }
   }
   if constexpr (p > 0) {

@@ -47,6 +47,8 @@ std::string derive_consts(int n, int n_det, int n_t, double R, double c, double 
   C.Lbox = std::pow(2.0, std::ceil(std::log2(C.T_new0 + 2.0) - 1e-12));
   C.N = (int)std::lround(2.0 * C.Lbox / C.h);
   C.Lres = C.N / n;
+  C.log2L = 0;
+  while ((1 << C.log2L) < C.Lres) ++C.log2L;
   C.dxi = kPi / C.Lbox;
   C.dt = T / n_t;
   double Mf = std::ceil(C.T_new0 / (c * C.dt) - 1e-9);

@@ -166,6 +166,9 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     P.S3 = (float2*)d;
     if ((e = alloc_ws(p, B * C.Kp * C.n_t * sizeof(float2), &d)) != cudaSuccess) break;
     P.S4 = (float2*)d;
+    P.C.ntargets = (int)H.k2t_tq.size();
+    if ((e = alloc_ws(p, B * (size_t)P.C.ntargets * sizeof(float2), &d)) != cudaSuccess) break;
+    P.Rc = (float2*)d;
     e = configure_kernels(P);
   } while (false);
   p->table_bytes = tb;

@@ -17,10 +17,12 @@ struct Consts {
   double wJ = 1, omega = 0;
   int N = 0;        // Cartesian FFT size
   int Lres = 0;     // residues N / n (oversampling factor, power of two)
+  int log2L = 0;
   int M = 0;        // DCT-I length; 2M-point FFT
   int J = 0, NL = 0;
   int n_ring = 0, K = 0, Kp = 0, half = 0;
   int ncols = 0;    // N/2 + 1 Cartesian columns kept (p in [0, N/2])
+  int ntargets = 0; // K2T: distinct Cartesian targets (p, q) of the transposed bilinear
 };  // plain data: passed by value to kernels inside DevPlan
 
 // Host-side tables (float64 built, float32/int stored), uploaded by tat_plan_create.
@@ -71,6 +73,7 @@ struct DevPlan {
   float2* S2 = nullptr;   // [B][half * NL] in K2 node order (sorted by p0)
   float2* S3 = nullptr;   // [B][Kp][NL]
   float2* S4 = nullptr;   // [B][Kp][n_t]
+  float2* Rc = nullptr;   // [B][ntargets]: K2T target sums (transposed bilinear), column order
 };
 
 // Launchers (kernels.cu).  ev != nullptr: record ev[i] before stage i and ev[5] at the end.
@@ -84,7 +87,7 @@ cudaError_t configure_fft_kernels(const Consts& C);
 size_t smem_fft4(const Consts& C);
 cudaError_t launch_k1(const DevPlan& P, const float* f, cudaStream_t s);
 cudaError_t launch_k2(const DevPlan& P, cudaStream_t s);
-cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s);
+cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s);   // target sums + column IDFT
 cudaError_t launch_k1t(const DevPlan& P, float* f, cudaStream_t s);
 // kernels_ring.cu: K3, K3T, K5, K5T on n_phi-point register FFTs
 bool ring_fast_ok(const Consts& C);
