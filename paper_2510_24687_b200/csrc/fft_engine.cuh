@@ -283,6 +283,44 @@ __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// Barrier of the n/8 threads of transform group g (G groups in the CTA).
+template <int n>
+__device__ __forceinline__ void group_sync(int g, int G) {
+  if constexpr (n / 8 <= 32) {
+    __syncwarp();
+  } else {
+    if (G <= 15) named_bar(1 + g, n / 8);
+    else __syncthreads();
+  }
+}
+
+// CTA-cooperative transforms, padded layout: G = blockDim.x / (n/8) transforms, transform g in
+// A + g * rstride(n) (natural order, element e at phys(e)), scratch B of the same shape.  The
+// output (natural order, padded) is returned; starts and ends with __syncthreads().
+template <int n, int S>
+__device__ __forceinline__ float2* cta_fft_g(float2* A, float2* B, const float2* __restrict__ tw_n,
+                                             int stride = 1) {
+  constexpr int P = Plan<n>::P;
+  constexpr int rs = rstride(n);
+  const int g = threadIdx.x / (n / 8), j = threadIdx.x & (n / 8 - 1);
+  const int G = blockDim.x / (n / 8);
+  float2 v[8];
+  __syncthreads();
+  pass_g<n, 0, S, true, true>(v, A + g * rs, B + g * rs, j, tw_n, stride);
+  group_sync<n>(g, G);
+  pass_g<n, 1, S, true, true>(v, B + g * rs, A + g * rs, j, tw_n, stride);
+  if constexpr (P > 2) {
+    group_sync<n>(g, G);
+    pass_g<n, 2, S, true, true>(v, A + g * rs, B + g * rs, j, tw_n, stride);
+  }
+  if constexpr (P > 3) {
+    group_sync<n>(g, G);
+    pass_g<n, 3, S, true, true>(v, B + g * rs, A + g * rs, j, tw_n, stride);
+  }
+  __syncthreads();
+  return (P & 1) ? B : A;
+}
+
 // Output position (natural order) of register element e after the LAST pass.
 template <int n>
 __device__ __forceinline__ int last_pos(int j, int e) {

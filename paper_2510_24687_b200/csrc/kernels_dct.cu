@@ -29,42 +29,41 @@ __device__ __forceinline__ float2 mul_ipow_d(float2 a, int e) {
 template <int nf, bool ADJ>
 __global__ void __launch_bounds__(512) k4_dct_fast(DevPlan P, int r) {
   extern __shared__ float2 sm[];
+  constexpr int rs = rstride(nf);
+  constexpr int PP = Plan<nf>::P;
   const Consts& C = P.C;
   const int M2 = 2 * C.M, NL = C.NL, n_t = C.n_t;
   const int b = blockIdx.y, k = blockIdx.x;
   const int j = threadIdx.x;                 // butterfly index, blockDim.x == nf / 8
-  PassTw<nf, -1> T;
-  T.load(j, P.tw_dct, r);                    // nf roots = every r-th of the 2M roots
   const float2* in = ADJ ? P.S4 + ((size_t)b * C.Kp + k) * n_t : P.S3 + ((size_t)b * C.Kp + k) * NL;
   const int lo = ADJ ? 1 : 0;                // input index of in[0]
   const int cnt = ADJ ? n_t : NL;
-  // pool of 4 buffers: r results + scratch; pass p writes A for even p, B for odd p
-  float2* pool[4] = {sm, sm + nf, sm + 2 * nf, sm + 3 * nf};
-  constexpr bool finB = (Plan<nf>::P % 2) == 0;
+  // buffer pool: r results + one scratch; pass p writes A for even p, B for odd p
+  constexpr bool finB = (PP % 2) == 0;
   int res_slot[3] = {0, 0, 0};
   int fa = 0, fb = 1, fresh = 2;
   for (int v = 0; v < r; ++v) {
-    float2* A = pool[fa];
-    float2* B = pool[fb];
+    float2* A = sm + fa * rs;
+    float2* B = sm + fb * rs;
     float2 x[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int i = j + e * (nf / 8);
       const int src = i - lo;
-      float2 val = (src >= 0 && src < cnt) ? in[src] : make_float2(0.f, 0.f);
+      float2 val = (src >= 0 && src < cnt) ? __ldg(&in[src]) : make_float2(0.f, 0.f);
       if (v) val = cmul(val, __ldg(&P.tw_dct[(int)(((long long)i * v) % M2)]));
       x[e] = val;
     }
-    pass<nf, 0, -1, false, true>(x, nullptr, A, j, nullptr);
+    pass_g<nf, 0, -1, false, true>(x, nullptr, A, j, P.tw_dct, r);
     __syncthreads();
-    pass<nf, 1, -1, true, (Plan<nf>::P > 2) || true>(x, A, B, j, T.tw[0]);
+    pass_g<nf, 1, -1, true, true>(x, A, B, j, P.tw_dct, r);
     __syncthreads();
-    if constexpr (Plan<nf>::P > 2) {
-      pass<nf, 2, -1, true, true>(x, B, A, j, T.tw[1]);
+    if constexpr (PP > 2) {
+      pass_g<nf, 2, -1, true, true>(x, B, A, j, P.tw_dct, r);
       __syncthreads();
     }
-    if constexpr (Plan<nf>::P > 3) {
-      pass<nf, 3, -1, true, true>(x, A, B, j, T.tw[2]);
+    if constexpr (PP > 3) {
+      pass_g<nf, 3, -1, true, true>(x, A, B, j, P.tw_dct, r);
       __syncthreads();
     }
     if (finB) { res_slot[v] = fb; fb = fresh++; }
@@ -73,7 +72,7 @@ __global__ void __launch_bounds__(512) k4_dct_fast(DevPlan P, int r) {
   // gather X[u] and X[-u] from the residue results
   auto X = [&](int u) -> float2 {
     const int vv = u % r, a = u / r;
-    return pool[res_slot[vv]][swz(a)];
+    return sm[res_slot[vv] * rs + phys(a)];
   };
   if (!ADJ) {
     float2* out = P.S4 + ((size_t)b * C.Kp + k) * n_t;
@@ -105,7 +104,7 @@ int dct_fast_r(const Consts& C) {
   return 0;
 }
 int dct_fast_nf(const Consts& C) { const int r = dct_fast_r(C); return r ? (2 * C.M) / r : 0; }
-size_t smem_dct_fast(const Consts& C) { return (size_t)4 * dct_fast_nf(C) * sizeof(float2); }
+size_t smem_dct_fast(const Consts& C) { return (size_t)4 * rstride(dct_fast_nf(C)) * sizeof(float2); }
 
 #define TAT_DCT_SWITCH(NFV, ...)                        \
   switch (NFV) {                                         \

@@ -40,26 +40,25 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
   const Consts& C = P.C;
   const int NL = C.NL, half = nf / 2;
   const int b = blockIdx.y, j0 = blockIdx.x * G;
+  constexpr int rs = rstride(nf);
   float2* A = sm;
-  float2* B = sm + G * nf;
-  PassTw<nf, -1> T;
-  T.load(threadIdx.x % (nf / 8), P.tw_ring);
+  float2* B = sm + G * rs;
   const float2* S2 = P.S2 + (size_t)b * half * NL;
   for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
     const int jj = idx / half, lp = idx - jj * half;   // S2 is in K2 node order: gather by perm
     const float2 v = (j0 + jj < NL) ? S2[__ldg(&P.node_perm[(size_t)(j0 + jj) * half + lp])]
                                     : make_float2(0.f, 0.f);
     const int l = (lp - nf / 4) & (nf - 1);
-    A[jj * nf + swz(l)] = v;
-    A[jj * nf + swz((l + half) & (nf - 1))] = make_float2(v.x, -v.y);
+    A[jj * rs + phys(l)] = v;
+    A[jj * rs + phys((l + half) & (nf - 1))] = make_float2(v.x, -v.y);
   }
-  const float2* X = cta_fft<nf, -1>(A, B, T);
+  const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
   float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
   for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
     const int k = idx / G, jj = idx - k * G, j = j0 + jj;
     if (j < NL) {
       const float m = __ldg(&P.mult[(size_t)k * NL + j]);
-      S3[(size_t)k * NL + j] = mul_ipow_(cscale(X[jj * nf + swz(k)], m), k);
+      S3[(size_t)k * NL + j] = mul_ipow_(cscale(X[jj * rs + phys(k)], m), k);
     }
   }
 }
@@ -72,27 +71,26 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
   const Consts& C = P.C;
   const int NL = C.NL, half = nf / 2, K = nf / 2;
   const int b = blockIdx.y, j0 = blockIdx.x * G;
+  constexpr int rs = rstride(nf);
   float2* A = sm;
-  float2* B = sm + G * nf;
-  PassTw<nf, 1> T;
-  T.load(threadIdx.x % (nf / 8), P.tw_ring);
+  float2* B = sm + G * rs;
   const float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
   for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
     const int k = idx / G, jj = idx - k * G;
     const float2 v = (j0 + jj < NL) ? S3[(size_t)k * NL + j0 + jj] : make_float2(0.f, 0.f);
-    A[jj * nf + swz(k)] = v;                       // k in [0, K]; slot K is k = -K
+    A[jj * rs + phys(k)] = v;                       // k in [0, K]; slot K is k = -K
     if (k >= 1 && k < K) {
       const float sg = (k & 1) ? -1.f : 1.f;
-      A[jj * nf + swz(nf - k)] = make_float2(sg * v.x, -sg * v.y);
+      A[jj * rs + phys(nf - k)] = make_float2(sg * v.x, -sg * v.y);
     }
   }
-  const float2* X = cta_fft<nf, 1>(A, B, T);
+  const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
   float2* S2 = P.S2 + (size_t)b * half * NL;
   for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
     const int jj = idx / half, lp = idx - jj * half;
     if (j0 + jj < NL) {
       const int l = (lp - nf / 4) & (nf - 1);
-      S2[__ldg(&P.node_perm[(size_t)(j0 + jj) * half + lp])] = X[jj * nf + swz(l)];
+      S2[__ldg(&P.node_perm[(size_t)(j0 + jj) * half + lp])] = X[jj * rs + phys(l)];
     }
   }
 }
@@ -106,10 +104,9 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
   const Consts& C = P.C;
   const int K = nf / 2, n_t = C.n_t, n_det = C.n_det;
   const int b = blockIdx.y, t0 = blockIdx.x * (2 * G);
+  constexpr int rs = rstride(nf);
   float2* A = sm;
-  float2* B = sm + G * nf;
-  PassTw<nf, 1> T;
-  T.load(threadIdx.x % (nf / 8), P.tw_ring);
+  float2* B = sm + G * rs;
   const float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
   for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
     const int k = idx / G, gg = idx - k * G;
@@ -117,17 +114,17 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
     const float2 v0 = (t < n_t) ? S4[(size_t)k * n_t + t] : make_float2(0.f, 0.f);
     const float2 v1 = (t + 1 < n_t) ? S4[(size_t)k * n_t + t + 1] : make_float2(0.f, 0.f);
     if (k >= 1 && k < K) {
-      A[gg * nf + swz(k)] = make_float2(v0.x - v1.y, v0.y + v1.x);          // v0 + i v1
-      A[gg * nf + swz(nf - k)] = make_float2(v0.x + v1.y, -v0.y + v1.x);   // conj v0 + i conj v1
+      A[gg * rs + phys(k)] = make_float2(v0.x - v1.y, v0.y + v1.x);          // v0 + i v1
+      A[gg * rs + phys(nf - k)] = make_float2(v0.x + v1.y, -v0.y + v1.x);   // conj v0 + i conj v1
     } else {   // k = 0 and the Nyquist k = K enter through their real parts (C2R convention)
-      A[gg * nf + swz(k)] = make_float2(v0.x, v1.x);
+      A[gg * rs + phys(k)] = make_float2(v0.x, v1.x);
     }
   }
-  const float2* X = cta_fft<nf, 1>(A, B, T);
+  const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
   const int tt_n = min(2 * G, n_t - t0);
   for (int idx = threadIdx.x; idx < tt_n * n_det; idx += blockDim.x) {
     const int tt = idx / n_det, d = idx - tt * n_det;
-    const float2 z = X[(tt >> 1) * nf + swz(__ldg(&P.ring[d]))];
+    const float2 z = X[(tt >> 1) * rs + phys(__ldg(&P.ring[d]))];
     gout[((size_t)b * n_t + t0 + tt) * n_det + d] = (tt & 1) ? z.y : z.x;
   }
 }
@@ -140,26 +137,25 @@ __global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restri
   const Consts& C = P.C;
   const int n_t = C.n_t, n_det = C.n_det;
   const int b = blockIdx.y, t0 = blockIdx.x * (2 * G);
+  constexpr int rs = rstride(nf);
   float2* A = sm;
-  float2* B = sm + G * nf;
-  PassTw<nf, -1> T;
-  T.load(threadIdx.x % (nf / 8), P.tw_ring);
-  for (int i = threadIdx.x; i < G * nf; i += blockDim.x) A[i] = make_float2(0.f, 0.f);
+  float2* B = sm + G * rs;
+  for (int i = threadIdx.x; i < G * rs; i += blockDim.x) A[i] = make_float2(0.f, 0.f);
   __syncthreads();
   const int tt_n = min(2 * G, n_t - t0);
   float* Af = reinterpret_cast<float*>(A);
   for (int idx = threadIdx.x; idx < tt_n * n_det; idx += blockDim.x) {
     const int tt = idx / n_det, d = idx - tt * n_det;
     const float v = gin[((size_t)b * n_t + t0 + tt) * n_det + d];
-    Af[2 * ((tt >> 1) * nf + swz(__ldg(&P.ring[d]))) + (tt & 1)] = v;
+    Af[2 * ((tt >> 1) * rs + phys(__ldg(&P.ring[d]))) + (tt & 1)] = v;
   }
-  const float2* X = cta_fft<nf, -1>(A, B, T);
+  const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
   float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
   for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
     const int k = idx / G, gg = idx - k * G;
     const int t = t0 + 2 * gg;
-    const float2 zk = X[gg * nf + swz(k)];
-    const float2 zm = X[gg * nf + swz((nf - k) & (nf - 1))];
+    const float2 zk = X[gg * rs + phys(k)];
+    const float2 zm = X[gg * rs + phys((nf - k) & (nf - 1))];
     // even sample: (Z[k] + conj Z[-k]) / 2 ; odd sample: (Z[k] - conj Z[-k]) / (2i)
     const float2 ge = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
     const float2 go = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
@@ -174,7 +170,7 @@ bool ring_fast_ok(const Consts& C) { return C.n_ring >= 32 && C.n_ring <= 2048; 
 size_t smem_ring_fast(const Consts& C) {
   const int nf = C.n_ring;
   const int G = (4096 / nf) < 16 ? (4096 / nf) : 16;
-  return (size_t)2 * G * nf * sizeof(float2);
+  return (size_t)2 * G * rstride(nf) * sizeof(float2);
 }
 
 #define TAT_RING_SWITCH(...)                      \
