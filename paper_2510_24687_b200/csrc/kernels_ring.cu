@@ -33,64 +33,110 @@ __device__ __forceinline__ float2 mul_ipow_(float2 a, int e) {
 }
 
 // ------------------------------------------------------------------ K3
+// Two rings per complex FFT: Z = P_1 + i P_2 (each ring completed from the half plane by
+// P(l + n/2) = conj P(l)); since F(-k) = (-1)^k conj F(k) for each ring,
+//   F_1[k] = (Z[k] + (-1)^k conj Z[-k]) / 2,  F_2[k] = (Z[k] - (-1)^k conj Z[-k]) / (2i).
 template <int nf>
 __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
   extern __shared__ float2 sm[];
-  constexpr int G = ring_G<nf>();
+  constexpr int G = ring_G<nf>();   // transforms per CTA (2G rings)
+  constexpr int rs = rstride(nf);
   const Consts& C = P.C;
   const int NL = C.NL, half = nf / 2;
-  const int b = blockIdx.y, j0 = blockIdx.x * G;
-  constexpr int rs = rstride(nf);
+  const int b = blockIdx.y, j0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S2 = P.S2 + (size_t)b * half * NL;
-  for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
-    const int jj = idx / half, lp = idx - jj * half;   // S2 is in K2 node order: gather by perm
-    const float2 v = (j0 + jj < NL) ? S2[__ldg(&P.node_perm[(size_t)(j0 + jj) * half + lp])]
-                                    : make_float2(0.f, 0.f);
-    const int l = (lp - nf / 4) & (nf - 1);
-    A[jj * rs + phys(l)] = v;
-    A[jj * rs + phys((l + half) & (nf - 1))] = make_float2(v.x, -v.y);
+  constexpr int PER = 4;   // items per thread: (nf/2) G / (G nf / 8)
+  const int T = blockDim.x;
+  int idxs[PER];
+  int pa[PER], pb[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {   // issue every perm load first (memory-level parallelism)
+    const int idx = threadIdx.x + u * T;
+    idxs[u] = idx;
+    pa[u] = -1;
+    pb[u] = -1;
+    if (idx < half * G) {
+      const int gg = idx / half, lp = idx - gg * half;
+      const int ja = j0 + 2 * gg, jb = ja + 1;
+      if (ja < NL) pa[u] = __ldg(&P.node_perm[(size_t)ja * half + lp]);
+      if (jb < NL) pb[u] = __ldg(&P.node_perm[(size_t)jb * half + lp]);
+    }
+  }
+  float2 va[PER], vb[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    va[u] = pa[u] >= 0 ? S2[pa[u]] : make_float2(0.f, 0.f);
+    vb[u] = pb[u] >= 0 ? S2[pb[u]] : make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int idx = idxs[u];
+    if (idx < half * G) {
+      const int gg = idx / half, lp = idx - gg * half;
+      const int l = (lp - nf / 4) & (nf - 1);
+      A[gg * rs + phys(l)] = make_float2(va[u].x - vb[u].y, va[u].y + vb[u].x);   // va + i vb
+      A[gg * rs + phys((l + half) & (nf - 1))] =
+          make_float2(va[u].x + vb[u].y, -va[u].y + vb[u].x);                    // conj va + i conj vb
+    }
   }
   const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
   float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
-  for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
-    const int k = idx / G, jj = idx - k * G, j = j0 + jj;
+  for (int idx = threadIdx.x; idx < C.Kp * 2 * G; idx += blockDim.x) {
+    const int k = idx / (2 * G), jj = idx - k * (2 * G), j = j0 + jj;
     if (j < NL) {
+      const int gg = jj >> 1;
+      const float2 zk = X[gg * rs + phys(k)];
+      float2 zm = X[gg * rs + phys((nf - k) & (nf - 1))];
+      if (k & 1) zm = make_float2(-zm.x, -zm.y);
+      // F1 = (zk + conj zm)/2 ; F2 = (zk - conj zm)/(2i)
+      const float2 F = (jj & 1) ? make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x))
+                                : make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
       const float m = __ldg(&P.mult[(size_t)k * NL + j]);
-      S3[(size_t)k * NL + j] = mul_ipow_(cscale(X[jj * rs + phys(k)], m), k);
+      S3[(size_t)k * NL + j] = mul_ipow_(cscale(F, m), k);
     }
   }
 }
 
 // ------------------------------------------------------------------ K3T
+// Two rings per complex inverse FFT: spectra completed by H~_{-k} = (-1)^k conj H~_k, packed
+// Z = E_1 + i E_2; the outputs satisfy P~(l + n/2) = conj P~(l), so
+//   P~_1[l] = (z[l] + conj z[l + n/2]) / 2,  P~_2[l] = (z[l] - conj z[l + n/2]) / (2i).
 template <int nf>
 __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
   extern __shared__ float2 sm[];
   constexpr int G = ring_G<nf>();
+  constexpr int rs = rstride(nf);
   const Consts& C = P.C;
   const int NL = C.NL, half = nf / 2, K = nf / 2;
-  const int b = blockIdx.y, j0 = blockIdx.x * G;
-  constexpr int rs = rstride(nf);
+  const int b = blockIdx.y, j0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
   for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
-    const int k = idx / G, jj = idx - k * G;
-    const float2 v = (j0 + jj < NL) ? S3[(size_t)k * NL + j0 + jj] : make_float2(0.f, 0.f);
-    A[jj * rs + phys(k)] = v;                       // k in [0, K]; slot K is k = -K
+    const int k = idx / G, gg = idx - k * G;
+    const int ja = j0 + 2 * gg;
+    const float2 e1 = (ja < NL) ? S3[(size_t)k * NL + ja] : make_float2(0.f, 0.f);
+    const float2 e2 = (ja + 1 < NL) ? S3[(size_t)k * NL + ja + 1] : make_float2(0.f, 0.f);
+    A[gg * rs + phys(k)] = make_float2(e1.x - e2.y, e1.y + e2.x);   // slot K is k = -K
     if (k >= 1 && k < K) {
-      const float sg = (k & 1) ? -1.f : 1.f;
-      A[jj * rs + phys(nf - k)] = make_float2(sg * v.x, -sg * v.y);
+      const float sg = (k & 1) ? -1.f : 1.f;   // E(-k) = (-1)^k conj E(k)
+      A[gg * rs + phys(nf - k)] = make_float2(sg * (e1.x + e2.y), sg * (-e1.y + e2.x));
     }
   }
   const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
   float2* S2 = P.S2 + (size_t)b * half * NL;
-  for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
-    const int jj = idx / half, lp = idx - jj * half;
-    if (j0 + jj < NL) {
+  for (int idx = threadIdx.x; idx < half * 2 * G; idx += blockDim.x) {
+    const int jj = idx / half, lp = idx - jj * half, j = j0 + jj;
+    if (j < NL) {
+      const int gg = jj >> 1;
       const int l = (lp - nf / 4) & (nf - 1);
-      S2[__ldg(&P.node_perm[(size_t)(j0 + jj) * half + lp])] = X[jj * rs + phys(l)];
+      const float2 z = X[gg * rs + phys(l)];
+      const float2 zh = X[gg * rs + phys((l + half) & (nf - 1))];
+      const float2 Pv = (jj & 1) ? make_float2(0.5f * (z.y + zh.y), -0.5f * (z.x - zh.x))
+                                 : make_float2(0.5f * (z.x + zh.x), 0.5f * (z.y - zh.y));
+      S2[__ldg(&P.node_perm[(size_t)j * half + lp])] = Pv;
     }
   }
 }
@@ -203,7 +249,7 @@ cudaError_t launch_k3(const DevPlan& P, cudaStream_t s) {
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
-    k3_ring<NF><<<dim3((C.NL + G - 1) / G, C.batch), G * NF / 8, sm, s>>>(P);
+    k3_ring<NF><<<dim3((C.NL + 2 * G - 1) / (2 * G), C.batch), G * NF / 8, sm, s>>>(P);
   });
   return cudaGetLastError();
 }
@@ -212,7 +258,7 @@ cudaError_t launch_k3t(const DevPlan& P, cudaStream_t s) {
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
-    k3t_ring<NF><<<dim3((C.NL + G - 1) / G, C.batch), G * NF / 8, sm, s>>>(P);
+    k3t_ring<NF><<<dim3((C.NL + 2 * G - 1) / (2 * G), C.batch), G * NF / 8, sm, s>>>(P);
   });
   return cudaGetLastError();
 }
