@@ -125,7 +125,7 @@ __global__ void k3_angular_mult(DevPlan P) {
   const float2* S2 = P.S2 + (size_t)b * half * NL;
   for (int idx = threadIdx.x; idx < half * JT; idx += blockDim.x) {
     int lp = idx / JT, jj = idx - lp * JT;
-    float2 v = (jj < jt) ? S2[P.node_perm[(size_t)(j0 + jj) * half + lp]] : make_float2(0.f, 0.f);
+    float2 v = (jj < jt) ? S2[(size_t)(j0 + jj) * half + lp] : make_float2(0.f, 0.f);
     int l = (lp - nphi / 4) & (nphi - 1);
     A[jj * nphi + l] = v;
     A[jj * nphi + ((l + half) & (nphi - 1))] = conjf2(v);
@@ -255,7 +255,7 @@ __global__ void k3t_angular(DevPlan P) {
     int lp = idx / JT, jj = idx - lp * JT;
     if (jj >= jt) continue;
     int l = (lp - nphi / 4) & (nphi - 1);
-    S2[P.node_perm[(size_t)(j0 + jj) * half + lp]] = X[jj * nphi + l];
+    S2[(size_t)(j0 + jj) * half + lp] = X[jj * nphi + l];
   }
 }
 

@@ -8,7 +8,7 @@
 //   K2Tb  Rc            -> S1                  scatter targets into the column + inverse DFT
 //   K1T   S1            -> f                   inverse row DFT (Hermitian completion)
 //
-// S1 is column-major ([p][y]); S2 is in K2's node order (sorted by the Cartesian column p0).
+// S1 is column-major ([p][y]); S2 is ring-major ([j][l'], half plane).
 // One thread = one radix-8 butterfly of one residue transform; L residues x n/8 threads.
 #include "async_copy.cuh"
 #include "fft_engine.cuh"
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(1024) k2_fwd(DevPlan P) {
         const float2 f00 = Xa[i00], f01 = Xa[i01], f10 = Xb[i00], f11 = Xb[i01];
         const float2 c0 = __ffma2_rn(make_float2(a, a), csub(f10, f00), f00);
         const float2 c1 = __ffma2_rn(make_float2(a, a), csub(f11, f01), f01);
-        S2[e] = __ffma2_rn(make_float2(bb, bb), csub(c1, c0), c0);
+        S2[nd.x] = __ffma2_rn(make_float2(bb, bb), csub(c1, c0), c0);
         e += blockDim.x;
         if (e < e1) nd = __ldg(&P.k2_nodes[e]);
       }
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(1024) k2_fwd(DevPlan P) {
       const float bb = __int_as_float(nd.w);
       const float2 f00 = Xa[fidx(nd.y & N1, L1, lg, rs)];
       const float2 f01 = Xa[fidx((nd.y + 1) & N1, L1, lg, rs)];
-      S2[e] = __ffma2_rn(make_float2(bb, bb), csub(f01, f00), f00);
+      S2[nd.x] = __ffma2_rn(make_float2(bb, bb), csub(f01, f00), f00);
     }
   }
 }

@@ -47,39 +47,15 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S2 = P.S2 + (size_t)b * half * NL;
-  constexpr int PER = 4;   // items per thread: (nf/2) G / (G nf / 8)
-  const int T = blockDim.x;
-  int idxs[PER];
-  int pa[PER], pb[PER];
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {   // issue every perm load first (memory-level parallelism)
-    const int idx = threadIdx.x + u * T;
-    idxs[u] = idx;
-    pa[u] = -1;
-    pb[u] = -1;
-    if (idx < half * G) {
-      const int gg = idx / half, lp = idx - gg * half;
-      const int ja = j0 + 2 * gg, jb = ja + 1;
-      if (ja < NL) pa[u] = __ldg(&P.node_perm[(size_t)ja * half + lp]);
-      if (jb < NL) pb[u] = __ldg(&P.node_perm[(size_t)jb * half + lp]);
-    }
-  }
-  float2 va[PER], vb[PER];
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    va[u] = pa[u] >= 0 ? S2[pa[u]] : make_float2(0.f, 0.f);
-    vb[u] = pb[u] >= 0 ? S2[pb[u]] : make_float2(0.f, 0.f);
-  }
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int idx = idxs[u];
-    if (idx < half * G) {
-      const int gg = idx / half, lp = idx - gg * half;
-      const int l = (lp - nf / 4) & (nf - 1);
-      A[gg * rs + phys(l)] = make_float2(va[u].x - vb[u].y, va[u].y + vb[u].x);   // va + i vb
-      A[gg * rs + phys((l + half) & (nf - 1))] =
-          make_float2(va[u].x + vb[u].y, -va[u].y + vb[u].x);                    // conj va + i conj vb
-    }
+  // S2 is ring-major: each ring's half plane is contiguous
+  for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
+    const int gg = idx / half, lp = idx - gg * half;
+    const int ja = j0 + 2 * gg, jb = ja + 1;
+    const float2 va = ja < NL ? S2[(size_t)ja * half + lp] : make_float2(0.f, 0.f);
+    const float2 vb = jb < NL ? S2[(size_t)jb * half + lp] : make_float2(0.f, 0.f);
+    const int l = (lp - nf / 4) & (nf - 1);
+    A[gg * rs + phys(l)] = make_float2(va.x - vb.y, va.y + vb.x);                  // va + i vb
+    A[gg * rs + phys((l + half) & (nf - 1))] = make_float2(va.x + vb.y, -va.y + vb.x);
   }
   const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
   float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
@@ -136,7 +112,7 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
       const float2 zh = X[gg * rs + phys((l + half) & (nf - 1))];
       const float2 Pv = (jj & 1) ? make_float2(0.5f * (z.y + zh.y), -0.5f * (z.x - zh.x))
                                  : make_float2(0.5f * (z.x + zh.x), 0.5f * (z.y - zh.y));
-      S2[__ldg(&P.node_perm[(size_t)j * half + lp])] = Pv;
+      S2[(size_t)j * half + lp] = Pv;
     }
   }
 }

@@ -222,8 +222,8 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
       q0v[i] = (int)fv; bv[i] = v - fv;
     }
   }
-  // K2 forward: counting sort by p0, stable in (l', j).  S2 is stored in this node order
-  // (K2 writes it contiguously); node_perm maps (j, l') -> sorted position for K3 / K3T.
+  // K2 forward: counting sort by p0, stable in (l', j).  S2 is stored ring-major [j][l']
+  // (contiguous rings for K3 / K3T); K2 writes its nodes to their ring slots.
   H.k2_colptr.assign(C.ncols + 1, 0);
   for (long i = 0; i < nodes; ++i) H.k2_colptr[p0v[i] + 1]++;
   for (int p = 0; p < C.ncols; ++p) H.k2_colptr[p + 1] += H.k2_colptr[p];
@@ -234,7 +234,7 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
     std::vector<int> pos(H.k2_colptr.begin(), H.k2_colptr.end() - 1);
     for (long i = 0; i < nodes; ++i) {
       int4 e;
-      e.x = (int)i;
+      e.x = (int)((i % NL) * half + i / NL);   // S2 slot, ring-major [j][l']
       e.y = q0v[i];
       e.z = fbits((float)av[i]);
       e.w = fbits((float)bv[i]);
@@ -258,7 +258,7 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
     for (int c4 = 0; c4 < 4; ++c4) {
       if (w[c4] == 0.0) continue;
       int qm = ((qq[c4] % N) + N) % N;
-      ent.push_back({pp[c4], qm, sorted_pos[i], (float)w[c4]});
+      ent.push_back({pp[c4], qm, (int)((i % NL) * half + i / NL), (float)w[c4]});
     }
   }
   // two-pass stable counting sort: by q, then by p
