@@ -38,22 +38,32 @@ __global__ void __launch_bounds__(512) k4_dct_fast(DevPlan P, int r) {
   const float2* in = ADJ ? P.S4 + ((size_t)b * C.Kp + k) * n_t : P.S3 + ((size_t)b * C.Kp + k) * NL;
   const int lo = ADJ ? 1 : 0;                // input index of in[0]
   const int cnt = ADJ ? n_t : NL;
+  float mloc[8];   // K4T multiplier row, loaded before the transforms
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int jj = threadIdx.x + u * (nf / 8);
+    mloc[u] = (ADJ && jj < NL) ? __ldg(&P.mult[(size_t)k * NL + jj]) : 0.f;
+  }
   // buffer pool: r results + one scratch; pass p writes A for even p, B for odd p
   constexpr bool finB = (PP % 2) == 0;
   int res_slot[3] = {0, 0, 0};
   int fa = 0, fb = 1, fresh = 2;
+  // inputs (shared by all residues) and the residue twiddles W_2M^{i v}, v = 1, 2, loaded at once
+  float2 xin[8], tw1[8], tw2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int i = j + e * (nf / 8);
+    const int src = i - lo;
+    xin[e] = (src >= 0 && src < cnt) ? __ldg(&in[src]) : make_float2(0.f, 0.f);
+    tw1[e] = r > 1 ? __ldg(&P.tw_dct[(int)((long long)i % M2)]) : make_float2(1.f, 0.f);
+    tw2[e] = r > 2 ? __ldg(&P.tw_dct[(int)(((long long)i * 2) % M2)]) : make_float2(1.f, 0.f);
+  }
   for (int v = 0; v < r; ++v) {
     float2* A = sm + fa * rs;
     float2* B = sm + fb * rs;
     float2 x[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int i = j + e * (nf / 8);
-      const int src = i - lo;
-      float2 val = (src >= 0 && src < cnt) ? __ldg(&in[src]) : make_float2(0.f, 0.f);
-      if (v) val = cmul(val, __ldg(&P.tw_dct[(int)(((long long)i * v) % M2)]));
-      x[e] = val;
-    }
+    for (int e = 0; e < 8; ++e) x[e] = v == 0 ? xin[e] : cmul(xin[e], v == 1 ? tw1[e] : tw2[e]);
     pass_g<nf, 0, -1, false, true>(x, nullptr, A, j, P.tw_dct, r);
     __syncthreads();
     pass_g<nf, 1, -1, true, true>(x, A, B, j, P.tw_dct, r);
@@ -83,10 +93,13 @@ __global__ void __launch_bounds__(512) k4_dct_fast(DevPlan P, int r) {
   } else {
     float2* out = P.S3 + ((size_t)b * C.Kp + k) * NL;
     const float om = (float)C.omega;
-    for (int jj = threadIdx.x; jj < NL; jj += blockDim.x) {
-      const float2 y = cscale(cadd(X(jj), X(jj == 0 ? 0 : M2 - jj)), 0.5f);
-      const float mm = om * __ldg(&P.mult[(size_t)k * NL + jj]);
-      out[jj] = mul_ipow_d(cscale(y, mm), -k);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {   // NL <= nf = 8 * blockDim.x
+      const int jj = threadIdx.x + u * (nf / 8);
+      if (jj < NL) {
+        const float2 y = cscale(cadd(X(jj), X(jj == 0 ? 0 : M2 - jj)), 0.5f);
+        out[jj] = mul_ipow_d(cscale(y, om * mloc[u]), -k);
+      }
     }
   }
 }

@@ -32,6 +32,9 @@ __device__ __forceinline__ float2 mul_ipow_(float2 a, int e) {
   }
 }
 
+// Global loads of each phase are issued together (unrolled item loops, registers) before any
+// dependent work, so a CTA pays one memory latency per phase.
+
 // ------------------------------------------------------------------ K3
 // Two rings per complex FFT: Z = P_1 + i P_2 (each ring completed from the half plane by
 // P(l + n/2) = conj P(l)); since F(-k) = (-1)^k conj F(k) for each ring,
@@ -41,27 +44,46 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
   extern __shared__ float2 sm[];
   constexpr int G = ring_G<nf>();   // transforms per CTA (2G rings)
   constexpr int rs = rstride(nf);
+  constexpr int T = G * nf / 8, Kp = nf / 2 + 1, half = nf / 2;
+  constexpr int NIN = half * G / T;                      // = 4
+  constexpr int NOUT = (Kp * 2 * G + T - 1) / T;         // <= 9
   const Consts& C = P.C;
-  const int NL = C.NL, half = nf / 2;
+  const int NL = C.NL;
   const int b = blockIdx.y, j0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S2 = P.S2 + (size_t)b * half * NL;
-  // S2 is ring-major: each ring's half plane is contiguous
-  for (int idx = threadIdx.x; idx < half * G; idx += blockDim.x) {
+  float2 va[NIN], vb[NIN];
+#pragma unroll
+  for (int u = 0; u < NIN; ++u) {
+    const int idx = threadIdx.x + u * T;
     const int gg = idx / half, lp = idx - gg * half;
-    const int ja = j0 + 2 * gg, jb = ja + 1;
-    const float2 va = ja < NL ? S2[(size_t)ja * half + lp] : make_float2(0.f, 0.f);
-    const float2 vb = jb < NL ? S2[(size_t)jb * half + lp] : make_float2(0.f, 0.f);
+    const int ja = j0 + 2 * gg;
+    va[u] = ja < NL ? S2[(size_t)ja * half + lp] : make_float2(0.f, 0.f);
+    vb[u] = ja + 1 < NL ? S2[(size_t)(ja + 1) * half + lp] : make_float2(0.f, 0.f);
+  }
+  float mo[NOUT];   // multiplier values of the output phase, loaded early
+#pragma unroll
+  for (int u = 0; u < NOUT; ++u) {
+    const int idx = threadIdx.x + u * T;
+    const int k = idx / (2 * G), j = j0 + (idx - k * (2 * G));
+    mo[u] = (idx < Kp * 2 * G && j < NL) ? __ldg(&P.mult[(size_t)k * NL + j]) : 0.f;
+  }
+#pragma unroll
+  for (int u = 0; u < NIN; ++u) {
+    const int idx = threadIdx.x + u * T;
+    const int gg = idx / half, lp = idx - gg * half;
     const int l = (lp - nf / 4) & (nf - 1);
-    A[gg * rs + phys(l)] = make_float2(va.x - vb.y, va.y + vb.x);                  // va + i vb
-    A[gg * rs + phys((l + half) & (nf - 1))] = make_float2(va.x + vb.y, -va.y + vb.x);
+    A[gg * rs + phys(l)] = make_float2(va[u].x - vb[u].y, va[u].y + vb[u].x);   // va + i vb
+    A[gg * rs + phys((l + half) & (nf - 1))] = make_float2(va[u].x + vb[u].y, -va[u].y + vb[u].x);
   }
   const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
   float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
-  for (int idx = threadIdx.x; idx < C.Kp * 2 * G; idx += blockDim.x) {
+#pragma unroll
+  for (int u = 0; u < NOUT; ++u) {
+    const int idx = threadIdx.x + u * T;
     const int k = idx / (2 * G), jj = idx - k * (2 * G), j = j0 + jj;
-    if (j < NL) {
+    if (idx < Kp * 2 * G && j < NL) {
       const int gg = jj >> 1;
       const float2 zk = X[gg * rs + phys(k)];
       float2 zm = X[gg * rs + phys((nf - k) & (nf - 1))];
@@ -69,8 +91,7 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
       // F1 = (zk + conj zm)/2 ; F2 = (zk - conj zm)/(2i)
       const float2 F = (jj & 1) ? make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x))
                                 : make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
-      const float m = __ldg(&P.mult[(size_t)k * NL + j]);
-      S3[(size_t)k * NL + j] = mul_ipow_(cscale(F, m), k);
+      S3[(size_t)k * NL + j] = mul_ipow_(cscale(F, mo[u]), k);
     }
   }
 }
@@ -84,26 +105,42 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
   extern __shared__ float2 sm[];
   constexpr int G = ring_G<nf>();
   constexpr int rs = rstride(nf);
+  constexpr int T = G * nf / 8, Kp = nf / 2 + 1, half = nf / 2, K = nf / 2;
+  constexpr int NIN = (Kp * G + T - 1) / T;   // <= 5
+  constexpr int NOUT = half * 2 * G / T;      // = 8
   const Consts& C = P.C;
-  const int NL = C.NL, half = nf / 2, K = nf / 2;
+  const int NL = C.NL;
   const int b = blockIdx.y, j0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
-  for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
+  float2 e1[NIN], e2[NIN];
+#pragma unroll
+  for (int u = 0; u < NIN; ++u) {
+    const int idx = threadIdx.x + u * T;
     const int k = idx / G, gg = idx - k * G;
     const int ja = j0 + 2 * gg;
-    const float2 e1 = (ja < NL) ? S3[(size_t)k * NL + ja] : make_float2(0.f, 0.f);
-    const float2 e2 = (ja + 1 < NL) ? S3[(size_t)k * NL + ja + 1] : make_float2(0.f, 0.f);
-    A[gg * rs + phys(k)] = make_float2(e1.x - e2.y, e1.y + e2.x);   // slot K is k = -K
-    if (k >= 1 && k < K) {
-      const float sg = (k & 1) ? -1.f : 1.f;   // E(-k) = (-1)^k conj E(k)
-      A[gg * rs + phys(nf - k)] = make_float2(sg * (e1.x + e2.y), sg * (-e1.y + e2.x));
+    const bool ok = idx < Kp * G;
+    e1[u] = (ok && ja < NL) ? S3[(size_t)k * NL + ja] : make_float2(0.f, 0.f);
+    e2[u] = (ok && ja + 1 < NL) ? S3[(size_t)k * NL + ja + 1] : make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < NIN; ++u) {
+    const int idx = threadIdx.x + u * T;
+    if (idx < Kp * G) {
+      const int k = idx / G, gg = idx - k * G;
+      A[gg * rs + phys(k)] = make_float2(e1[u].x - e2[u].y, e1[u].y + e2[u].x);   // slot K is -K
+      if (k >= 1 && k < K) {
+        const float sg = (k & 1) ? -1.f : 1.f;   // E(-k) = (-1)^k conj E(k)
+        A[gg * rs + phys(nf - k)] = make_float2(sg * (e1[u].x + e2[u].y), sg * (-e1[u].y + e2[u].x));
+      }
     }
   }
   const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
   float2* S2 = P.S2 + (size_t)b * half * NL;
-  for (int idx = threadIdx.x; idx < half * 2 * G; idx += blockDim.x) {
+#pragma unroll
+  for (int u = 0; u < NOUT; ++u) {
+    const int idx = threadIdx.x + u * T;
     const int jj = idx / half, lp = idx - jj * half, j = j0 + jj;
     if (j < NL) {
       const int gg = jj >> 1;
@@ -123,23 +160,37 @@ template <int nf>
 __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ gout) {
   extern __shared__ float2 sm[];
   constexpr int G = ring_G<nf>();
-  const Consts& C = P.C;
-  const int K = nf / 2, n_t = C.n_t, n_det = C.n_det;
-  const int b = blockIdx.y, t0 = blockIdx.x * (2 * G);
   constexpr int rs = rstride(nf);
+  constexpr int T = G * nf / 8, Kp = nf / 2 + 1, K = nf / 2;
+  constexpr int NIN = (Kp * G + T - 1) / T;   // <= 5
+  const Consts& C = P.C;
+  const int n_t = C.n_t, n_det = C.n_det;
+  const int b = blockIdx.y, t0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
-  for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
+  float2 w0[NIN], w1[NIN];
+#pragma unroll
+  for (int u = 0; u < NIN; ++u) {
+    const int idx = threadIdx.x + u * T;
     const int k = idx / G, gg = idx - k * G;
     const int t = t0 + 2 * gg;
-    const float2 v0 = (t < n_t) ? S4[(size_t)k * n_t + t] : make_float2(0.f, 0.f);
-    const float2 v1 = (t + 1 < n_t) ? S4[(size_t)k * n_t + t + 1] : make_float2(0.f, 0.f);
-    if (k >= 1 && k < K) {
-      A[gg * rs + phys(k)] = make_float2(v0.x - v1.y, v0.y + v1.x);          // v0 + i v1
-      A[gg * rs + phys(nf - k)] = make_float2(v0.x + v1.y, -v0.y + v1.x);   // conj v0 + i conj v1
-    } else {   // k = 0 and the Nyquist k = K enter through their real parts (C2R convention)
-      A[gg * rs + phys(k)] = make_float2(v0.x, v1.x);
+    const bool ok = idx < Kp * G;
+    w0[u] = (ok && t < n_t) ? S4[(size_t)k * n_t + t] : make_float2(0.f, 0.f);
+    w1[u] = (ok && t + 1 < n_t) ? S4[(size_t)k * n_t + t + 1] : make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int u = 0; u < NIN; ++u) {
+    const int idx = threadIdx.x + u * T;
+    if (idx < Kp * G) {
+      const int k = idx / G, gg = idx - k * G;
+      const float2 v0 = w0[u], v1 = w1[u];
+      if (k >= 1 && k < K) {
+        A[gg * rs + phys(k)] = make_float2(v0.x - v1.y, v0.y + v1.x);          // v0 + i v1
+        A[gg * rs + phys(nf - k)] = make_float2(v0.x + v1.y, -v0.y + v1.x);   // conj v0 + i conj v1
+      } else {   // k = 0 and the Nyquist k = K enter through their real parts (C2R convention)
+        A[gg * rs + phys(k)] = make_float2(v0.x, v1.x);
+      }
     }
   }
   const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
@@ -156,33 +207,52 @@ template <int nf>
 __global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restrict__ gin) {
   extern __shared__ float2 sm[];
   constexpr int G = ring_G<nf>();
+  constexpr int rs = rstride(nf);
+  constexpr int T = G * nf / 8, Kp = nf / 2 + 1;
+  constexpr int NIN = 16;                     // >= 2G n_det / T for n_det <= nf
+  constexpr int NOUT = (Kp * G + T - 1) / T;  // <= 5
   const Consts& C = P.C;
   const int n_t = C.n_t, n_det = C.n_det;
   const int b = blockIdx.y, t0 = blockIdx.x * (2 * G);
-  constexpr int rs = rstride(nf);
   float2* A = sm;
   float2* B = sm + G * rs;
+  const int tt_n = min(2 * G, n_t - t0);
+  const int tot = tt_n * n_det;
+  float gv[NIN];
+  int gp[NIN];
+#pragma unroll
+  for (int u = 0; u < NIN; ++u) {
+    const int idx = threadIdx.x + u * T;
+    gv[u] = 0.f;
+    gp[u] = -1;
+    if (idx < tot) {
+      const int tt = idx / n_det, d = idx - tt * n_det;
+      gv[u] = gin[((size_t)b * n_t + t0 + tt) * n_det + d];
+      gp[u] = 2 * ((tt >> 1) * rs + phys(__ldg(&P.ring[d]))) + (tt & 1);
+    }
+  }
   for (int i = threadIdx.x; i < G * rs; i += blockDim.x) A[i] = make_float2(0.f, 0.f);
   __syncthreads();
-  const int tt_n = min(2 * G, n_t - t0);
   float* Af = reinterpret_cast<float*>(A);
-  for (int idx = threadIdx.x; idx < tt_n * n_det; idx += blockDim.x) {
-    const int tt = idx / n_det, d = idx - tt * n_det;
-    const float v = gin[((size_t)b * n_t + t0 + tt) * n_det + d];
-    Af[2 * ((tt >> 1) * rs + phys(__ldg(&P.ring[d]))) + (tt & 1)] = v;
-  }
+#pragma unroll
+  for (int u = 0; u < NIN; ++u)
+    if (gp[u] >= 0) Af[gp[u]] = gv[u];
   const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
   float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
-  for (int idx = threadIdx.x; idx < C.Kp * G; idx += blockDim.x) {
-    const int k = idx / G, gg = idx - k * G;
-    const int t = t0 + 2 * gg;
-    const float2 zk = X[gg * rs + phys(k)];
-    const float2 zm = X[gg * rs + phys((nf - k) & (nf - 1))];
-    // even sample: (Z[k] + conj Z[-k]) / 2 ; odd sample: (Z[k] - conj Z[-k]) / (2i)
-    const float2 ge = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
-    const float2 go = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
-    if (t < n_t) S4[(size_t)k * n_t + t] = ge;
-    if (t + 1 < n_t) S4[(size_t)k * n_t + t + 1] = go;
+#pragma unroll
+  for (int u = 0; u < NOUT; ++u) {
+    const int idx = threadIdx.x + u * T;
+    if (idx < Kp * G) {
+      const int k = idx / G, gg = idx - k * G;
+      const int t = t0 + 2 * gg;
+      const float2 zk = X[gg * rs + phys(k)];
+      const float2 zm = X[gg * rs + phys((nf - k) & (nf - 1))];
+      // even sample: (Z[k] + conj Z[-k]) / 2 ; odd sample: (Z[k] - conj Z[-k]) / (2i)
+      const float2 ge = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+      const float2 go = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+      if (t < n_t) S4[(size_t)k * n_t + t] = ge;
+      if (t + 1 < n_t) S4[(size_t)k * n_t + t + 1] = go;
+    }
   }
 }
 
