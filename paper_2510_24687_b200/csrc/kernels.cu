@@ -255,7 +255,7 @@ __global__ void k3t_angular(DevPlan P) {
     int lp = idx / JT, jj = idx - lp * JT;
     if (jj >= jt) continue;
     int l = (lp - nphi / 4) & (nphi - 1);
-    S2[(size_t)(j0 + jj) * half + lp] = X[jj * nphi + l];
+    S2[P.node_perm[(size_t)(j0 + jj) * half + lp]] = X[jj * nphi + l];
   }
 }
 

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
       const float2 zh = X[gg * rs + phys((l + half) & (nf - 1))];
       const float2 Pv = (jj & 1) ? make_float2(0.5f * (z.y + zh.y), -0.5f * (z.x - zh.x))
                                  : make_float2(0.5f * (z.x + zh.x), 0.5f * (z.y - zh.y));
-      S2[(size_t)j * half + lp] = Pv;
+      S2[__ldg(&P.node_perm[(size_t)j * half + lp])] = Pv;   // adjoint S2: node order
     }
   }
 }

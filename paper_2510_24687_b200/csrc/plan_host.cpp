@@ -222,8 +222,9 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
       q0v[i] = (int)fv; bv[i] = v - fv;
     }
   }
-  // K2 forward: counting sort by p0, stable in (l', j).  S2 is stored ring-major [j][l']
-  // (contiguous rings for K3 / K3T); K2 writes its nodes to their ring slots.
+  // K2 forward: counting sort by p0, stable in (l', j).  Forward S2 is ring-major [j][l']
+  // (K2 scatters node values to ring slots, K3 reads rings); adjoint S2 is in this sorted node
+  // order (K3T scatters through node_perm, the K2T target sums read contiguous node ranges).
   H.k2_colptr.assign(C.ncols + 1, 0);
   for (long i = 0; i < nodes; ++i) H.k2_colptr[p0v[i] + 1]++;
   for (int p = 0; p < C.ncols; ++p) H.k2_colptr[p + 1] += H.k2_colptr[p];
@@ -258,7 +259,7 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
     for (int c4 = 0; c4 < 4; ++c4) {
       if (w[c4] == 0.0) continue;
       int qm = ((qq[c4] % N) + N) % N;
-      ent.push_back({pp[c4], qm, (int)((i % NL) * half + i / NL), (float)w[c4]});
+      ent.push_back({pp[c4], qm, sorted_pos[i], (float)w[c4]});
     }
   }
   // two-pass stable counting sort: by q, then by p

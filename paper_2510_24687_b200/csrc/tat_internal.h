@@ -70,7 +70,7 @@ struct DevPlan {
   const int* ring = nullptr;
   // workspace
   float2* S1 = nullptr;   // [B][ncols][n]
-  float2* S2 = nullptr;   // [B][half * NL] in K2 node order (sorted by p0)
+  float2* S2 = nullptr;   // [B][half * NL]: forward ring-major [j][l'], adjoint K2 node order
   float2* S3 = nullptr;   // [B][Kp][NL]
   float2* S4 = nullptr;   // [B][Kp][n_t]
   float2* Rc = nullptr;   // [B][ntargets]: K2T target sums (transposed bilinear), column order

@@ -42,6 +42,28 @@ __global__ void k_shfl(float* out, int stride) {
   float s = 0; for (int u = 0; u < 8; ++u) s += a[u];
   if (s == 1.234f) out[0] = s;
 }
+// LDS.64 and SHFL interleaved: if both reach their solo rate the datapaths are separate
+__global__ void k_mixed(float* out, int stride) {
+  __shared__ float2 s[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) s[i] = make_float2(i, i);
+  __syncthreads();
+  float2 acc = make_float2(0, 0);
+  float a[4];
+  for (int u = 0; u < 4; ++u) a[u] = threadIdx.x + u;
+  int idx = threadIdx.x;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float2 v = s[(idx + u * 256) & 4095];
+      acc.x += v.x; acc.y += v.y;
+      a[u] = __shfl_xor_sync(0xffffffff, a[u], 1 + u);
+      a[u] = __shfl_xor_sync(0xffffffff, a[u], 2 + u);
+    }
+    idx += 1;
+  }
+  float t = a[0] + a[1] + a[2] + a[3];
+  if (acc.x == 1.234f || t == 1.234f) out[0] = acc.y + t;
+}
 template <class K>
 void run(const char* name, K k, int inst_per_iter) {
   float* out; cudaMalloc(&out, 4);
@@ -61,5 +83,6 @@ int main() {
   run("LDS64", k_lds64, 8);
   run("STS64", k_sts64, 8);
   run("SHFL", k_shfl, 8);
+  run("MIXED(4 LDS.64 + 8 SHFL)", k_mixed, 12);
   return 0;
 }
