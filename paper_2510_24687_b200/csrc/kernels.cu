@@ -283,13 +283,13 @@ cudaError_t configure_kernels(const DevPlan& P) {
   return e;
 }
 
-cudaError_t launch_forward(const DevPlan& P, const float* f, float* g, cudaStream_t s,
-                           cudaEvent_t* ev) {
+cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float* f, float* g,
+                           cudaStream_t s, cudaEvent_t* ev) {
   const Consts& C = P.C;
   const int B = C.batch;
   const int JT = tile_ring(C.n_ring);
   if (ev) cudaEventRecord(ev[0], s);
-  cudaError_t e = launch_k1(P, f, s);
+  cudaError_t e = launch_k1(P, tm, f, s);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
   e = launch_k2(P, s);
@@ -310,8 +310,8 @@ cudaError_t launch_forward(const DevPlan& P, const float* f, float* g, cudaStrea
   return cudaGetLastError();
 }
 
-cudaError_t launch_adjoint(const DevPlan& P, const float* g, float* f, cudaStream_t s,
-                           cudaEvent_t* ev) {
+cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float* g, float* f,
+                           cudaStream_t s, cudaEvent_t* ev) {
   const Consts& C = P.C;
   const int B = C.batch;
   const int JT = tile_ring(C.n_ring);
@@ -332,7 +332,7 @@ cudaError_t launch_adjoint(const DevPlan& P, const float* g, float* f, cudaStrea
   e = launch_k2t(P, s);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[4], s);
-  e = launch_k1t(P, f, s);
+  e = launch_k1t(P, tm, f, s);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[5], s);
   return cudaGetLastError();

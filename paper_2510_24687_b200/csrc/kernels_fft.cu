@@ -14,6 +14,8 @@
 #include "fft_engine.cuh"
 #include "tat_internal.h"
 
+#include <cudaTypedefs.h>
+
 namespace tat {
 
 using namespace fe;
@@ -84,7 +86,7 @@ __device__ __forceinline__ int fidx(int q, int L1, int lg, int rs) {   // F[q] i
 // the first node record of each gather is prefetched into registers before the transform.
 template <int n>
 __global__ void __launch_bounds__(1024) k2_fwd(DevPlan P) {
-  extern __shared__ __align__(16) float2 sm[];
+  extern __shared__ __align__(128) float2 sm[];
   constexpr int rs = rstride(n);
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs, N1 = C.N - 1;
@@ -169,8 +171,9 @@ __global__ void __launch_bounds__(1024) k2_fwd(DevPlan P) {
 // z = f_y + i f_{y+1}; Z[p] = sum_x z e^{-2 pi i p (x-n/2)/N}; two row pairs per CTA so that
 // each p writes one full 32-byte sector S1[p][y0..y0+3].
 template <int n>
-__global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const float* __restrict__ f) {
-  extern __shared__ __align__(16) float2 sm[];
+__global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const __grid_constant__ CUtensorMap tm,
+                                                const float* __restrict__ f) {
+  extern __shared__ __align__(128) float2 sm[];
   constexpr int rs = rstride(n);
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs, N = C.N;
@@ -191,39 +194,56 @@ __global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const float* __restric
       xb[r] = make_float2(__ldg(&r0[2 * n + xi]), __ldg(&r0[3 * n + xi]));
     }
   }
-  float2* ZA;
-  float2* ZB;
+  int iA, iB;
   {
     float2 v[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = cmul(xa[r], pre[r]);
     pass_g<n, 0, -1, false, true>(v, nullptr, sm + so, j, P.tw_n);
-    ZA = passes_fwd<n, -1>(v, sm + so, sm + ln + so, j, g, L, P.tw_n) ? sm + ln : sm;
+    iA = passes_fwd<n, -1>(v, sm + so, sm + ln + so, j, g, L, P.tw_n) ? 1 : 0;
   }
   {
-    float2* b1 = (ZA == sm) ? sm + ln : sm;
+    const int i1 = iA == 0 ? 1 : 0;
     float2 v[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) v[r] = cmul(xb[r], pre[r]);
     pass_g<n, 0, -1, false, true>(v, nullptr, sm + 2 * ln + so, j, P.tw_n);
-    ZB = passes_fwd<n, -1>(v, sm + 2 * ln + so, b1 + so, j, g, L, P.tw_n) ? b1 : sm + 2 * ln;
+    iB = passes_fwd<n, -1>(v, sm + 2 * ln + so, sm + i1 * ln + so, j, g, L, P.tw_n) ? i1 : 2;
   }
   __syncthreads();
-  float4* out = reinterpret_cast<float4*>(P.S1 + (size_t)b * C.ncols * n);
-  for (int p = threadIdx.x; p < C.ncols; p += blockDim.x) {
-    const int pm = (N - p) & (N - 1);
-    const int ip = fidx(p, L1, lg, rs), im = fidx(pm, L1, lg, rs);
-    const float2 za = ZA[ip], zam = ZA[im], zb = ZB[ip], zbm = ZB[im];
-    // row y: (Z[p] + conj Z[-p]) / 2 ; row y+1: (Z[p] - conj Z[-p]) / (2 i)
-    float4 o0, o1;
-    o0.x = 0.5f * (za.x + zam.x); o0.y = 0.5f * (za.y - zam.y);
-    o0.z = 0.5f * (za.y + zam.y); o0.w = -0.5f * (za.x - zam.x);
-    o1.x = 0.5f * (zb.x + zbm.x); o1.y = 0.5f * (zb.y - zbm.y);
-    o1.z = 0.5f * (zb.y + zbm.y); o1.w = -0.5f * (zb.x - zbm.x);
-    float4* dst = out + (((size_t)p * n + y0) >> 1);
-    dst[0] = o0;
-    dst[1] = o1;
+  const float2* ZA = sm + iA * ln;
+  const float2* ZB = sm + iB * ln;
+  // output: S1[p][y0..y0+3] staged as [256 p][4 y] tiles in the free buffer, stored by TMA
+  float2* stg = sm + (3 - iA - iB) * ln;
+  const int BP = C.s1boxP, CH = BP * kS1BoxY;      // complex values per tile
+  const int nslot = (ln / CH) < 4 ? (ln / CH) : 4;  // >= 2 by construction of s1boxP
+  const int nch = (C.ncols + BP - 1) / BP;
+  for (int c = 0; c < nch; ++c) {
+    const int slot = c % nslot;
+    if (c >= nslot) {   // the store that used this slot must have finished reading it
+      if (threadIdx.x == 0) ac::bulk_wait_read<0>();
+      __syncthreads();
+    }
+    float2* t = stg + slot * CH;
+    for (int u = threadIdx.x; u < 2 * BP; u += blockDim.x) {
+      const int pl = u >> 1, pr = u & 1, p = c * BP + pl;
+      if (p < C.ncols) {
+        const float2* Z = pr ? ZB : ZA;
+        const int pm = (N - p) & (N - 1);
+        const float2 za = Z[fidx(p, L1, lg, rs)], zm = Z[fidx(pm, L1, lg, rs)];
+        // row y: (Z[p] + conj Z[-p]) / 2 ; row y+1: (Z[p] - conj Z[-p]) / (2 i)
+        t[pl * 4 + 2 * pr] = make_float2(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y));
+        t[pl * 4 + 2 * pr + 1] = make_float2(0.5f * (za.y + zm.y), -0.5f * (za.x - zm.x));
+      }
+    }
+    ac::fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ac::tma_store_3d(&tm, t, y0, c * BP, b);
+      ac::bulk_commit();
+    }
   }
+  if (threadIdx.x == 0) ac::bulk_wait_all();
 }
 
 // ================================================================== K2Ta: target sums
@@ -250,7 +270,7 @@ __global__ void __launch_bounds__(256) k2t_sum(DevPlan P) {
 // S~1[p][y] = sum_s X_s[y'] conj(W_N^{s y''}), the residue sum reduced through smem.
 template <int n>
 __global__ void __launch_bounds__(1024) k2t_adj(DevPlan P) {
-  extern __shared__ __align__(16) float2 sm[];
+  extern __shared__ __align__(128) float2 sm[];
   constexpr int rs = rstride(n);
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs;
@@ -312,8 +332,9 @@ __global__ void __launch_bounds__(1024) k2t_adj(DevPlan P) {
 // Two row pairs per CTA: Z[p] = C_y[p] + i C_{y+1}[p] (Hermitian completion of the half
 // spectra, C[0], C[N/2] = 2 Re), inverse residue FFTs, residue sum -> f~ rows.
 template <int n>
-__global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, float* __restrict__ fout) {
-  extern __shared__ __align__(16) float2 sm[];
+__global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, const __grid_constant__ CUtensorMap tm,
+                                                 float* __restrict__ fout) {
+  extern __shared__ __align__(128) float2 sm[];
   constexpr int rs = rstride(n);
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs, N = C.N;
@@ -326,23 +347,47 @@ __global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, float* __restrict__ f
   float2* ZA = sm;
   float2* ZB = sm + ln;
   float2* X = sm + 2 * ln;
-  const float4* in = reinterpret_cast<const float4*>(P.S1 + (size_t)b * C.ncols * n);
-  for (int p = threadIdx.x; p < C.ncols; p += blockDim.x) {
-    const float4* src = in + (((size_t)p * n + y0) >> 1);
-    const float4 v0 = __ldg(&src[0]), v1 = __ldg(&src[1]);   // rows y0, y0+1 | y0+2, y0+3
-    const int ip = fidx(p, L1, lg, rs);
-    if (p == 0 || p == N / 2) {
-      ZA[ip] = make_float2(2.f * v0.x, 2.f * v0.z);
-      ZB[ip] = make_float2(2.f * v1.x, 2.f * v1.z);
-    } else {
-      const int im = fidx(N - p, L1, lg, rs);
-      ZA[ip] = make_float2(v0.x - v0.w, v0.y + v0.z);
-      ZA[im] = make_float2(v0.x + v0.w, -v0.y + v0.z);
-      ZB[ip] = make_float2(v1.x - v1.w, v1.y + v1.z);
-      ZB[im] = make_float2(v1.x + v1.w, -v1.y + v1.z);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 3 * ln + 2 * n);
+  // input: S~1[p][y0..y0+3] as [256 p][4 y] tiles loaded by TMA into X (free before the FFTs)
+  const int BP = C.s1boxP, CH = BP * kS1BoxY;
+  const int nslot = (ln / CH) < 4 ? (ln / CH) : 4;
+  const int nch = (C.ncols + BP - 1) / BP;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < nslot; ++q) ac::mbar_init(&bar[q], 1);
+    ac::fence_mbar_init();
+    for (int c = 0; c < nch && c < nslot; ++c) {
+      ac::mbar_expect_tx(&bar[c], CH * 8);
+      ac::tma_load_3d(X + c * CH, &tm, y0, c * BP, b, &bar[c]);
     }
   }
   __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int slot = c % nslot;
+    ac::mbar_wait(&bar[slot], (c / nslot) & 1);
+    const float2* t = X + slot * CH;
+    for (int pl = threadIdx.x; pl < BP; pl += blockDim.x) {
+      const int p = c * BP + pl;
+      if (p >= C.ncols) break;
+      const float2 a0 = t[pl * 4], a1 = t[pl * 4 + 1], b0 = t[pl * 4 + 2], b1 = t[pl * 4 + 3];
+      const int ip = fidx(p, L1, lg, rs);
+      if (p == 0 || p == N / 2) {
+        ZA[ip] = make_float2(2.f * a0.x, 2.f * a1.x);
+        ZB[ip] = make_float2(2.f * b0.x, 2.f * b1.x);
+      } else {
+        const int im = fidx(N - p, L1, lg, rs);
+        ZA[ip] = make_float2(a0.x - a1.y, a0.y + a1.x);    // C_y + i C_{y+1}
+        ZA[im] = make_float2(a0.x + a1.y, -a0.y + a1.x);   // conj C_y + i conj C_{y+1}
+        ZB[ip] = make_float2(b0.x - b1.y, b0.y + b1.x);
+        ZB[im] = make_float2(b0.x + b1.y, -b0.y + b1.x);
+      }
+    }
+    __syncthreads();   // slot consumed
+    if (threadIdx.x == 0 && c + nslot < nch) {
+      ac::fence_proxy_async();
+      ac::mbar_expect_tx(&bar[slot], CH * 8);
+      ac::tma_load_3d(X + slot * CH, &tm, y0, (c + nslot) * BP, b, &bar[slot]);
+    }
+  }
 #pragma unroll 1
   for (int pr = 0; pr < 2; ++pr) {
     float2* Zs = pr ? ZB : ZA;
@@ -368,7 +413,7 @@ __global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, float* __restrict__ f
 // ================================================================== dispatch
 static size_t rstride_h(int n) { return (size_t)rstride(n); }
 size_t smem_fft4(const Consts& C) {
-  return (size_t)3 * C.Lres * rstride_h(C.n) * sizeof(float2) + 2 * C.n * sizeof(float2) + 16;
+  return (size_t)3 * C.Lres * rstride_h(C.n) * sizeof(float2) + 2 * C.n * sizeof(float2) + 64;
 }
 static size_t smem_k2t(const Consts& C) { return (size_t)2 * C.Lres * rstride_h(C.n) * sizeof(float2); }
 int fft_threads(const Consts& C) { return C.Lres * (C.n / 8); }
@@ -400,10 +445,30 @@ cudaError_t configure_fft_kernels(const Consts& C) {
   return cudaSuccess;
 }
 
-cudaError_t launch_k1(const DevPlan& P, const float* f, cudaStream_t s) {
+cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const Consts& C = P.C;
+  cuuint64_t dims[3] = {(cuuint64_t)C.n, (cuuint64_t)C.ncols, (cuuint64_t)C.batch};
+  cuuint64_t strides[2] = {(cuuint64_t)C.n * 8, (cuuint64_t)C.ncols * C.n * 8};
+  cuuint32_t box[3] = {kS1BoxY, (cuuint32_t)C.s1boxP, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, P.S1, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s) {
   const Consts& C = P.C;
   const dim3 grid(C.n / 4, C.batch);
-  TAT_DISPATCH_N(k1_fwd<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P, f));
+  TAT_DISPATCH_N(k1_fwd<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P, tm, f));
   return cudaGetLastError();
 }
 cudaError_t launch_k2(const DevPlan& P, cudaStream_t s) {
@@ -419,10 +484,10 @@ cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s) {
   TAT_DISPATCH_N(k2t_adj<NN><<<grid, fft_threads(C), smem_k2t(C), s>>>(P));
   return cudaGetLastError();
 }
-cudaError_t launch_k1t(const DevPlan& P, float* f, cudaStream_t s) {
+cudaError_t launch_k1t(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s) {
   const Consts& C = P.C;
   const dim3 grid(C.n / 4, C.batch);
-  TAT_DISPATCH_N(k1t_adj<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P, f));
+  TAT_DISPATCH_N(k1t_adj<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P, tm, f));
   return cudaGetLastError();
 }
 

@@ -94,6 +94,12 @@ std::string derive_consts(int n, int n_det, int n_t, double R, double c, double 
   C.half = n_ring / 2;
   C.ncols = C.N / 2 + 1;
   C.omega = C.dt * 2.0 * kPi * R / (n_ring * C.h * C.h);
+  {   // S1 TMA tile: largest power of two <= min(256, L * rstride(n) / 8)
+    const int pn = n + n / 16, rs = pn + ((18 - pn % 16) % 16);
+    const int lim = std::min(256, C.Lres * rs / 8);
+    C.s1boxP = 1;
+    while (C.s1boxP * 2 <= lim) C.s1boxP *= 2;
+  }
   code = 0;
   return "";
 }
@@ -232,8 +238,18 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
   H.node_perm.assign(nodes, 0);
   std::vector<int> sorted_pos(nodes);
   {
+    // within a column, nodes are ordered by q0 so that neighbouring Cartesian targets of the
+    // transposed bilinear read neighbouring node values (L1 locality in K2Ta)
+    std::vector<long> byq(nodes);
+    {
+      std::vector<int> cq(N + 2, 0);
+      for (long i = 0; i < nodes; ++i) cq[q0v[i] + N / 2 + 1]++;
+      for (int q = 0; q <= N; ++q) cq[q + 1] += cq[q];
+      for (long i = 0; i < nodes; ++i) byq[cq[q0v[i] + N / 2]++] = i;
+    }
     std::vector<int> pos(H.k2_colptr.begin(), H.k2_colptr.end() - 1);
-    for (long i = 0; i < nodes; ++i) {
+    for (long ii = 0; ii < nodes; ++ii) {
+      const long i = byq[ii];
       int4 e;
       e.x = (int)((i % NL) * half + i / NL);   // S2 slot, ring-major [j][l']
       e.y = q0v[i];

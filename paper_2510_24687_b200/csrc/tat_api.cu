@@ -12,6 +12,7 @@ using namespace tat;
 
 struct tat_plan {
   DevPlan P;
+  CUtensorMap tm_s1;
   std::vector<int> ring;
   std::vector<void*> allocs;
   size_t workspace_bytes = 0, table_bytes = 0;
@@ -170,6 +171,7 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     if ((e = alloc_ws(p, B * (size_t)P.C.ntargets * sizeof(float2), &d)) != cudaSuccess) break;
     P.Rc = (float2*)d;
     e = configure_kernels(P);
+    if (e == cudaSuccess) e = make_s1_tensor_map(P, &p->tm_s1);
   } while (false);
   p->table_bytes = tb;
   if (e != cudaSuccess) {
@@ -211,7 +213,7 @@ tat_status tat_forward(const tat_plan* plan, const float* f, float* g, cudaStrea
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
   tat_plan* p = const_cast<tat_plan*>(plan);
   cudaEvent_t* ev = prof_slot(p, true);
-  cudaError_t e = launch_forward(plan->P, f, g, stream, ev);
+  cudaError_t e = launch_forward(plan->P, plan->tm_s1, f, g, stream, ev);
   if (e != cudaSuccess) return cuda_fail(e, "tat_forward launch");
   return TAT_OK;
 }
@@ -220,7 +222,7 @@ tat_status tat_adjoint(const tat_plan* plan, const float* g, float* f, cudaStrea
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
   tat_plan* p = const_cast<tat_plan*>(plan);
   cudaEvent_t* ev = prof_slot(p, false);
-  cudaError_t e = launch_adjoint(plan->P, g, f, stream, ev);
+  cudaError_t e = launch_adjoint(plan->P, plan->tm_s1, g, f, stream, ev);
   if (e != cudaSuccess) return cuda_fail(e, "tat_adjoint launch");
   return TAT_OK;
 }

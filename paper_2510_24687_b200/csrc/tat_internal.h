@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <string>
 #include <vector>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace tat {
@@ -23,6 +24,7 @@ struct Consts {
   int n_ring = 0, K = 0, Kp = 0, half = 0;
   int ncols = 0;    // N/2 + 1 Cartesian columns kept (p in [0, N/2])
   int ntargets = 0; // K2T: distinct Cartesian targets (p, q) of the transposed bilinear
+  int s1boxP = 0;   // TMA box extent along p for S1 tiles (box = {4 y, s1boxP p, 1})
 };  // plain data: passed by value to kernels inside DevPlan
 
 // Host-side tables (float64 built, float32/int stored), uploaded by tat_plan_create.
@@ -77,18 +79,21 @@ struct DevPlan {
 };
 
 // Launchers (kernels.cu).  ev != nullptr: record ev[i] before stage i and ev[5] at the end.
-cudaError_t launch_forward(const DevPlan& P, const float* f, float* g, cudaStream_t s,
-                           cudaEvent_t* ev);
-cudaError_t launch_adjoint(const DevPlan& P, const float* g, float* f, cudaStream_t s,
-                           cudaEvent_t* ev);
+cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float* f, float* g,
+                           cudaStream_t s, cudaEvent_t* ev);
+cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float* g, float* f,
+                           cudaStream_t s, cudaEvent_t* ev);
 cudaError_t configure_kernels(const DevPlan& P);   // smem attributes
 // kernels_fft.cu: residue-FFT kernels K1, K2, K2T, K1T
 cudaError_t configure_fft_kernels(const Consts& C);
 size_t smem_fft4(const Consts& C);
-cudaError_t launch_k1(const DevPlan& P, const float* f, cudaStream_t s);
+// S1 viewed as a 3-D tensor {n (y), ncols (p), batch} of 8-byte elements; TMA box {4, 256, 1}
+constexpr int kS1BoxY = 4;
+cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out);
+cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
 cudaError_t launch_k2(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s);   // target sums + column IDFT
-cudaError_t launch_k1t(const DevPlan& P, float* f, cudaStream_t s);
+cudaError_t launch_k1t(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s);
 // kernels_ring.cu: K3, K3T, K5, K5T on n_phi-point register FFTs
 bool ring_fast_ok(const Consts& C);
 size_t smem_ring_fast(const Consts& C);
