@@ -100,11 +100,11 @@ __device__ float2* smem_fft(float2* A, float2* B, int len, int count,
 
 // ------------------------------------------------------------------ tile sizes
 __host__ __device__ inline int tile_ring(int n_ring) { int t = 4096 / n_ring; return t < 1 ? 1 : (t > 16 ? 16 : t); }
-constexpr int kK2Strip = 16;
 constexpr int kThreads = 256;
 
 size_t max_smem_needed(const Consts& C) {
   size_t s = smem_fft4(C);                                         // K1/K2/K2T/K1T
+  if (col_ok(C)) s = std::max(s, smem_k2c_fwd(C));                 // K2 two-stage
   if (dct_fast_r(C)) s = std::max(s, smem_dct_fast(C));            // K4 / K4T
   else s = std::max(s, (size_t)2 * 2 * C.M * sizeof(float2));
   if (ring_fast_ok(C)) s = std::max(s, smem_ring_fast(C));           // K3/K5
@@ -270,6 +270,7 @@ cudaError_t configure_kernels(const DevPlan& P) {
   if (e == cudaSuccess)                                                                      \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes));
   if (e == cudaSuccess) e = configure_fft_kernels(C);
+  if (e == cudaSuccess) e = configure_col_kernels(C);
   if (e == cudaSuccess) e = configure_ring_kernels(C);
   if (e == cudaSuccess) e = configure_dct_kernels(C);
   SETSM(k3_angular_mult, smem_ring(C));

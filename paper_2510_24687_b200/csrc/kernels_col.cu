@@ -1,0 +1,301 @@
+// Column stage of the oversampled 2-D DFT (Alg. 1 steps 2-3 and Alg. 2 steps 5-6, PAPER.md
+// L547-551, L684-687) as a two-stage split with R = 16 points per thread in registers:
+//
+//   F[q] = sum_{y<n} x[y] W_N^{q (y - n/2)},  N = L n,  y = j + J r  (J = n/R),
+//   q = q0 + Q0 q1  (Q0 = R L, q0 = s + L k1):
+//   F[q0 + Q0 q1] = sum_j W_J^{q1 j} * W_n^{k1 (j - n/2)} *
+//                   sum_r x[j + J r] W_N^{s (j + J r - n/2)} W_R^{k1 r}
+//
+//   stage A (thread (j, s)): pre-twiddle, R-point DFT over r, post-twiddle b^k1 (b = W_n^{j-n/2})
+//   stage B (thread q0)    : J-point DFT over j (pure, in place in shared memory)
+//
+// Each point crosses shared memory once between the stages (vs. P-1 exchanges of a radix-8
+// Stockham), and a thread reads its column samples once for all of its residues s.
+// The transposed kernel runs the conjugate stages in reverse order (exact adjoint).
+//
+//   k2c_fwd : S1 [B][ncols][n] -> S2 [B][nodes]   column DFT + bilinear gather (as k2_fwd)
+//   k2c_adj : Rc [B][targets]  -> S1              target values -> inverse column DFT
+//                                                 (targets per column ordered by (q0, q1))
+#include "async_copy.cuh"
+#include "col_engine.cuh"
+#include "tat_internal.h"
+
+namespace tat {
+
+namespace {
+
+constexpr int kStripC = 16;   // columns per CTA (k2c_fwd recomputes one halo column)
+
+template <int n>
+struct ColGeo {
+  static constexpr int L = 8, R = 16, J = n / R, Q0 = R * L, T = Q0;
+  static constexpr int NG = T / J;        // residue groups (threads sharing j)
+  static constexpr int NRES = J / R;      // residues per thread in stage A
+  static constexpr int LGQ0 = 7;          // log2 Q0
+  static_assert(J >= R && J <= 32, "n in {256, 512}");
+  // element (q0, c) of a column buffer [Q0][J]: XOR swizzle, conflict-free for both stages
+  __device__ static __forceinline__ int widx(int q0, int c) { return q0 * J + (c ^ (q0 & (J - 1))); }
+  __device__ static __forceinline__ int fq(int q) { return widx(q & (Q0 - 1), q >> LGQ0); }
+};
+
+}  // namespace
+
+using ce::cmul;
+using ce::cmulc;
+using ce::csub;
+
+// ================================================================== forward
+template <int n>
+__global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
+  using G = ColGeo<n>;
+  constexpr int R = G::R, J = G::J, L = G::L, NG = G::NG, NRES = G::NRES;
+  extern __shared__ __align__(128) float2 sm[];
+  const Consts& C = P.C;
+  const int N1 = C.N - 1;
+  const int t = threadIdx.x, j = t % J, sg = t / J;
+  const int b = blockIdx.y;
+  const int P0 = blockIdx.x * kStripC;
+  const int Pend = min(P0 + kStripC, C.ncols);
+  const int plast = min(Pend, C.ncols - 1);
+  float2* Fa = sm;
+  float2* Fb = sm + G::Q0 * J;
+  float2* xbuf = sm + 2 * G::Q0 * J;                          // 2 x n, TMA destination
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xbuf + 2 * n);
+  float2 A[NRES][R];
+#pragma unroll
+  for (int i = 0; i < NRES; ++i)
+#pragma unroll
+    for (int r = 0; r < R; ++r) A[i][r] = __ldg(&P.tw_col[(sg + NG * i) * n + j + J * r]);
+  float2 pw[R];
+  ce::pow_tree<R>(__ldg(&P.tw_n[(j - n / 2) & (n - 1)]), pw);
+  const float2* S1 = P.S1 + (size_t)b * C.ncols * n;
+  float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
+  if (t == 0) {
+    ac::mbar_init(&bar[0], 1);
+    ac::mbar_init(&bar[1], 1);
+    ac::fence_mbar_init();
+    ac::mbar_expect_tx(&bar[0], n * 8);
+    ac::bulk_g2s(xbuf, S1 + (size_t)P0 * n, n * 8, &bar[0]);
+  }
+  __syncthreads();
+  float2* Fprev = Fb;
+  float2* Fcur = Fa;
+  for (int p = P0; p <= plast; ++p) {
+    const int it = p - P0, slot = it & 1;
+    if (t == 0 && p < plast) {
+      ac::fence_proxy_async();
+      ac::mbar_expect_tx(&bar[slot ^ 1], n * 8);
+      ac::bulk_g2s(xbuf + (slot ^ 1) * n, S1 + (size_t)(p + 1) * n, n * 8, &bar[slot ^ 1]);
+    }
+    const int e0 = (p > P0) ? __ldg(&P.k2_colptr[p - 1]) : 0;
+    const int e1 = (p > P0) ? __ldg(&P.k2_colptr[p]) : 0;
+    int4 nd0 = make_int4(0, 0, 0, 0);
+    if (e0 + t < e1) nd0 = __ldg(&P.k2_nodes[e0 + t]);
+    ac::mbar_wait(&bar[slot], (it >> 1) & 1);
+    {   // stage A
+      const float2* xs = xbuf + slot * n;
+      float2 x[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = xs[j + J * r];
+#pragma unroll
+      for (int i = 0; i < NRES; ++i) {
+        const int s = sg + NG * i;
+        float2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = cmul(x[r], A[i][r]);
+        ce::dftr<R, -1>(v);
+#pragma unroll
+        for (int k1 = 1; k1 < R; ++k1) v[k1] = cmul(v[k1], pw[k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < R; ++k1) Fcur[G::widx(s + L * k1, j)] = v[k1];
+      }
+    }
+    __syncthreads();
+    {   // stage B (in place)
+      float2 u[J];
+#pragma unroll
+      for (int c = 0; c < J; ++c) u[c] = Fcur[G::widx(t, c)];
+      ce::dftr<J, -1>(u);
+#pragma unroll
+      for (int c = 0; c < J; ++c) Fcur[G::widx(t, c)] = u[c];
+    }
+    __syncthreads();
+    if (p > P0) {   // bilinear gather of the nodes with p0 = p - 1 (Alg. 1 step 3)
+      int e = e0 + t;
+      int4 nd = nd0;
+      while (e < e1) {
+        const float a = __int_as_float(nd.z), bb = __int_as_float(nd.w);
+        const int i00 = G::fq(nd.y & N1), i01 = G::fq((nd.y + 1) & N1);
+        const float2 f00 = Fprev[i00], f01 = Fprev[i01], f10 = Fcur[i00], f11 = Fcur[i01];
+        const float2 c0 = __ffma2_rn(make_float2(a, a), csub(f10, f00), f00);
+        const float2 c1 = __ffma2_rn(make_float2(a, a), csub(f11, f01), f01);
+        S2[nd.x] = __ffma2_rn(make_float2(bb, bb), csub(c1, c0), c0);
+        e += G::T;
+        if (e < e1) nd = __ldg(&P.k2_nodes[e]);
+      }
+    }
+    __syncthreads();
+    float2* tmp = Fprev;
+    Fprev = Fcur;
+    Fcur = tmp;
+  }
+  if (Pend == C.ncols) {   // p0 = N/2: alpha == 0, only F[N/2] is used
+    for (int e = P.k2_colptr[C.ncols - 1] + t; e < P.k2_colptr[C.ncols]; e += G::T) {
+      const int4 nd = __ldg(&P.k2_nodes[e]);
+      const float bb = __int_as_float(nd.w);
+      const float2 f00 = Fprev[G::fq(nd.y & N1)];
+      const float2 f01 = Fprev[G::fq((nd.y + 1) & N1)];
+      S2[nd.x] = __ffma2_rn(make_float2(bb, bb), csub(f01, f00), f00);
+    }
+  }
+}
+
+// ================================================================== adjoint (transpose)
+// Column p: the target values of column p (Rc, ordered by (q0, q1), moved by one bulk copy per
+// column into a double buffer) -> stage B^H (thread q0, only the present q1 are read) ->
+// stage A^H (thread (j, s)) -> residue-group partial sums -> S~1[b][p][y].
+template <int n>
+__global__ void __launch_bounds__(128, 3) k2c_adj(DevPlan P) {
+  using G = ColGeo<n>;
+  constexpr int R = G::R, J = G::J, L = G::L, NG = G::NG, NRES = G::NRES, Q0 = G::Q0;
+  extern __shared__ __align__(128) float2 sm[];
+  const Consts& C = P.C;
+  const int t = threadIdx.x, j = t % J, sg = t / J;
+  const int b = blockIdx.y;
+  const int P0 = blockIdx.x * kStripC;
+  const int Pend = min(P0 + kStripC, C.ncols);
+  const int RB = C.k2c_rbuf;                                  // entries per target buffer
+  float2* Wb = sm;
+  float2* rbuf = sm + Q0 * J;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(rbuf + 2 * RB);
+  float2 A[NRES][R];
+#pragma unroll
+  for (int i = 0; i < NRES; ++i)
+#pragma unroll
+    for (int r = 0; r < R; ++r) A[i][r] = __ldg(&P.tw_col[(sg + NG * i) * n + j + J * r]);
+  float2 pw[R];
+  ce::pow_tree<R>(__ldg(&P.tw_n[(j - n / 2) & (n - 1)]), pw);
+  const float2* Rc = P.Rc + (size_t)b * C.ntpad;
+  float2* out = P.S1 + (size_t)b * C.ncols * n;
+  auto issue = [&](int p, int slot) {   // thread 0: bulk copy of column p's targets
+    const int s0 = __ldg(&P.k2t_colptr[p]) & ~1;
+    const int s1 = (__ldg(&P.k2t_colptr[p + 1]) + 1) & ~1;
+    if (s1 > s0) {
+      ac::mbar_expect_tx(&bar[slot], (s1 - s0) * 8);
+      ac::bulk_g2s(rbuf + slot * RB, Rc + s0, (s1 - s0) * 8, &bar[slot]);
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ac::smem_u32(&bar[slot])) : "memory");
+    }
+  };
+  if (t == 0) {
+    ac::mbar_init(&bar[0], 1);
+    ac::mbar_init(&bar[1], 1);
+    ac::fence_mbar_init();
+    issue(P0, 0);
+  }
+  __syncthreads();
+  uint32_t m = __ldg(&P.k2c_mask[(size_t)P0 * Q0 + t]);
+  int base = __ldg(&P.k2c_base[(size_t)P0 * Q0 + t]) - (__ldg(&P.k2t_colptr[P0]) & ~1);
+  for (int p = P0; p < Pend; ++p) {
+    const int it = p - P0, slot = it & 1;
+    if (t == 0 && p + 1 < Pend) {
+      ac::fence_proxy_async();
+      issue(p + 1, slot ^ 1);
+    }
+    uint32_t m_next = 0;
+    int base_next = 0;
+    if (p + 1 < Pend) {
+      m_next = __ldg(&P.k2c_mask[(size_t)(p + 1) * Q0 + t]);
+      base_next = __ldg(&P.k2c_base[(size_t)(p + 1) * Q0 + t]) - (__ldg(&P.k2t_colptr[p + 1]) & ~1);
+    }
+    ac::mbar_wait(&bar[slot], (it >> 1) & 1);
+    {   // stage B^H: A~[q0][j] = sum_q1 W_J^{-q1 j} F~[q0 + Q0 q1]
+      const float2* rb = rbuf + slot * RB + base;
+      float2 u[J];
+#pragma unroll
+      for (int c = 0; c < J; ++c) {
+        const uint32_t below = m & ((1u << c) - 1u);
+        u[c] = ((m >> c) & 1u) ? rb[__popc(below)] : make_float2(0.f, 0.f);
+      }
+      ce::dftr<J, 1>(u);
+#pragma unroll
+      for (int c = 0; c < J; ++c) Wb[G::widx(t, c)] = u[c];
+    }
+    __syncthreads();
+    float2 acc[R];
+    {   // stage A^H
+#pragma unroll
+      for (int i = 0; i < NRES; ++i) {
+        const int s = sg + NG * i;
+        float2 v[R];
+#pragma unroll
+        for (int k1 = 0; k1 < R; ++k1) v[k1] = Wb[G::widx(s + L * k1, j)];
+#pragma unroll
+        for (int k1 = 1; k1 < R; ++k1) v[k1] = cmulc(v[k1], pw[k1]);
+        ce::dftr<R, 1>(v);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float2 w = cmulc(v[r], A[i][r]);
+          acc[r] = (i == 0) ? w : ce::cadd(acc[r], w);
+        }
+      }
+    }
+    __syncthreads();   // all stage-A^H reads of Wb done
+#pragma unroll
+    for (int r = 0; r < R; ++r) Wb[sg * n + j + J * r] = acc[r];
+    __syncthreads();
+    for (int y = t; y < n; y += G::T) {
+      float2 s = Wb[y];
+#pragma unroll
+      for (int g = 1; g < NG; ++g) s = ce::cadd(s, Wb[g * n + y]);
+      out[(size_t)p * n + y] = s;
+    }
+    __syncthreads();   // Wb free; rbuf[slot] consumed
+    m = m_next;
+    base = base_next;
+  }
+}
+
+// ================================================================== dispatch
+bool col_ok(const Consts& C) { return C.Lres == 8 && (C.n == 256 || C.n == 512); }
+
+size_t smem_k2c_fwd(const Consts& C) {
+  const int Q0 = 128, J = C.n / 16;
+  return (size_t)2 * Q0 * J * 8 + (size_t)2 * C.n * 8 + 64;
+}
+size_t smem_k2c_adj(const Consts& C) {
+  const int Q0 = 128, J = C.n / 16;
+  return (size_t)Q0 * J * 8 + (size_t)2 * C.k2c_rbuf * 8 + 64;
+}
+
+cudaError_t configure_col_kernels(const Consts& C) {
+  if (!col_ok(C)) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  const int lim = 227 * 1024;
+  if (C.n == 512) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2c_fwd<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2c_adj<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  } else {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2c_fwd<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2c_adj<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  }
+  return e;
+}
+
+cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
+  if (C.n == 512) k2c_fwd<512><<<grid, 128, smem_k2c_fwd(C), s>>>(P);
+  else k2c_fwd<256><<<grid, 128, smem_k2c_fwd(C), s>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
+  if (C.n == 512) k2c_adj<512><<<grid, 128, smem_k2c_adj(C), s>>>(P);
+  else k2c_adj<256><<<grid, 128, smem_k2c_adj(C), s>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace tat

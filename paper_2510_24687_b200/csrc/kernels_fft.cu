@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256) k2t_sum(DevPlan P) {
     const float w = __int_as_float(en.y);
     acc = __ffma2_rn(make_float2(w, w), __ldg(&S2[en.x]), acc);
   }
-  P.Rc[(size_t)b * C.ntargets + t] = acc;
+  P.Rc[(size_t)b * C.ntpad + t] = acc;
 }
 
 // ================================================================== K2Tb (transpose of K2)
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(1024) k2t_adj(DevPlan P) {
   float2 post[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) post[e] = __ldg(&P.tw_pre[g * n + last_pos<n>(j, e)]);
-  const float2* Rc = P.Rc + (size_t)b * C.ntargets;
+  const float2* Rc = P.Rc + (size_t)b * C.ntpad;
   float2* out = P.S1 + (size_t)b * C.ncols * n;
   float2* R = sm;        // scatter target, zero outside the targets
   float2* Xb = sm + ln;  // ping-pong, then residue-sum staging
@@ -473,6 +473,7 @@ cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, c
 }
 cudaError_t launch_k2(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
+  if (col_ok(C)) return launch_k2c_fwd(P, s);
   const dim3 grid((C.ncols + kStrip - 1) / kStrip, C.batch);
   TAT_DISPATCH_N(k2_fwd<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P));
   return cudaGetLastError();
@@ -480,6 +481,7 @@ cudaError_t launch_k2(const DevPlan& P, cudaStream_t s) {
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   k2t_sum<<<dim3((C.ntargets + 255) / 256, C.batch), 256, 0, s>>>(P);
+  if (col_ok(C)) return launch_k2c_adj(P, s);
   const dim3 grid((C.ncols + kStrip - 1) / kStrip, C.batch);
   TAT_DISPATCH_N(k2t_adj<NN><<<grid, fft_threads(C), smem_k2t(C), s>>>(P));
   return cudaGetLastError();

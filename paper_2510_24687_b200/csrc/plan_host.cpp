@@ -202,6 +202,9 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
     }
   H.tw_ring.resize(nphi);
   for (int k = 0; k < nphi; ++k) H.tw_ring[k] = root(k, nphi, -1);
+  H.tw_col.resize((size_t)L * n);
+  for (int s = 0; s < L; ++s)
+    for (int y = 0; y < n; ++y) H.tw_col[(size_t)s * n + y] = root((long)s * (y - n / 2), N, -1);
   H.tw_dct.resize(2 * (size_t)C.M);
   for (int k = 0; k < 2 * C.M; ++k) H.tw_dct[k] = root(k, 2L * C.M, -1);
   H.ring = ring;
@@ -278,13 +281,16 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
       ent.push_back({pp[c4], qm, sorted_pos[i], (float)w[c4]});
     }
   }
-  // two-pass stable counting sort: by q, then by p
+  // two-pass stable counting sort: by key(q), then by p.  key(q) = (q mod Q0, q / Q0) with
+  // Q0 = 16 L orders a column's targets by the (q0, q1) split of kernels_col.cu
+  const int Q0 = 16 * L;
+  auto qkey = [&](int q) { return (q % Q0) * (N / Q0) + q / Q0; };
   {
     std::vector<int> cnt(N + 1, 0);
-    for (auto& e : ent) cnt[e.q + 1]++;
+    for (auto& e : ent) cnt[qkey(e.q) + 1]++;
     for (int q = 0; q < N; ++q) cnt[q + 1] += cnt[q];
     std::vector<Ent> tmp(ent.size());
-    for (auto& e : ent) tmp[cnt[e.q]++] = e;
+    for (auto& e : ent) tmp[cnt[qkey(e.q)]++] = e;
     std::vector<int> cp(C.ncols + 1, 0);
     for (auto& e : tmp) cp[e.p + 1]++;
     for (int p = 0; p < C.ncols; ++p) cp[p + 1] += cp[p];
@@ -304,6 +310,18 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
   }
   H.k2t_tstart.push_back((int)ent.size());
   for (int p = 0; p < C.ncols; ++p) H.k2t_colptr[p + 1] += H.k2t_colptr[p];
+  // k2c_adj: per (p, q0) presence mask over q1 and first target index
+  if (col_ok(C)) {
+    H.k2c_mask.assign((size_t)C.ncols * Q0, 0u);
+    H.k2c_base.assign((size_t)C.ncols * Q0, 0);
+    for (int p = 0; p < C.ncols; ++p) {
+      for (int t = H.k2t_colptr[p + 1] - 1; t >= H.k2t_colptr[p]; --t) {
+        const int q = H.k2t_tq[t], q0 = q % Q0, q1 = q / Q0;
+        H.k2c_mask[(size_t)p * Q0 + q0] |= 1u << q1;
+        H.k2c_base[(size_t)p * Q0 + q0] = t;
+      }
+    }
+  }
 }
 
 }  // namespace tat

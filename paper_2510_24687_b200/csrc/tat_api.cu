@@ -2,6 +2,7 @@
 #include "tat.h"
 #include "tat_internal.h"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -157,6 +158,9 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     if ((e = upload(p, H.k2t_tstart, &P.k2t_tstart, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2t_ent, &P.k2t_ent, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.ring, &P.ring, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.tw_col, &P.tw_col, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2c_mask, &P.k2c_mask, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2c_base, &P.k2c_base, tb)) != cudaSuccess) break;
     const size_t B = (size_t)C.batch;
     void* d;
     if ((e = alloc_ws(p, B * C.ncols * C.n * sizeof(float2), &d)) != cudaSuccess) break;
@@ -168,7 +172,17 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     if ((e = alloc_ws(p, B * C.Kp * C.n_t * sizeof(float2), &d)) != cudaSuccess) break;
     P.S4 = (float2*)d;
     P.C.ntargets = (int)H.k2t_tq.size();
-    if ((e = alloc_ws(p, B * (size_t)P.C.ntargets * sizeof(float2), &d)) != cudaSuccess) break;
+    P.C.ntpad = (P.C.ntargets + 1) & ~1;
+    {
+      int mx = 0;
+      for (int q = 0; q < C.ncols; ++q) mx = std::max(mx, H.k2t_colptr[q + 1] - H.k2t_colptr[q]);
+      P.C.k2c_rbuf = (mx + 3) & ~1;   // even: 16-B aligned bulk-copy destinations
+    }
+    if (col_ok(P.C) && smem_k2c_adj(P.C) > 227 * 1024) {
+      e = cudaErrorInvalidConfiguration;
+      break;
+    }
+    if ((e = alloc_ws(p, B * (size_t)P.C.ntpad * sizeof(float2) + 16, &d)) != cudaSuccess) break;
     P.Rc = (float2*)d;
     e = configure_kernels(P);
     if (e == cudaSuccess) e = make_s1_tensor_map(P, &p->tm_s1);

@@ -25,6 +25,8 @@ struct Consts {
   int ncols = 0;    // N/2 + 1 Cartesian columns kept (p in [0, N/2])
   int ntargets = 0; // K2T: distinct Cartesian targets (p, q) of the transposed bilinear
   int s1boxP = 0;   // TMA box extent along p for S1 tiles (box = {4 y, s1boxP p, 1})
+  int ntpad = 0;    // per-image stride of Rc (ntargets rounded up to even: 16-B bulk copies)
+  int k2c_rbuf = 0; // k2c_adj: entries per column target buffer (max targets per column + 2)
 };  // plain data: passed by value to kernels inside DevPlan
 
 // Host-side tables (float64 built, float32/int stored), uploaded by tat_plan_create.
@@ -34,6 +36,7 @@ struct HostTables {
   std::vector<float2> tw_pre;       // [Lres][n]: exp(-2 pi i s y'' / N) at FFT slot y' = y'' mod n
   std::vector<float2> tw_ring;      // n_ring roots
   std::vector<float2> tw_dct;       // 2M roots
+  std::vector<float2> tw_col;       // [Lres][n]: exp(-2 pi i s (y - n/2) / N) (kernels_col.cu)
   // K2 forward gather: half-plane nodes sorted by p0
   std::vector<int> k2_colptr;       // [ncols + 1]
   std::vector<int4> k2_nodes;       // (l'*NL + j, q0, alpha bits, beta bits), sorted by p0
@@ -44,6 +47,10 @@ struct HostTables {
   std::vector<int> k2t_tstart;      // [T + 1] into entries
   std::vector<int2> k2t_ent;        // [E] (src sorted node position, weight bits)
   std::vector<int> ring;            // [n_det]
+  // k2c_adj: per (column p, q0 = q mod 16L): bit q1 set if target (p, q0 + 16L q1) exists,
+  // and the index of the first such target (targets of a column are ordered by (q0, q1))
+  std::vector<uint32_t> k2c_mask;   // [ncols][16L] (only when col_ok)
+  std::vector<int> k2c_base;        // [ncols][16L]
 };
 
 // returns "" on success, else an error message; code receives 1 (invalid) or 2 (unsupported)
@@ -62,6 +69,7 @@ struct DevPlan {
   const float2* tw_pre = nullptr;
   const float2* tw_ring = nullptr;
   const float2* tw_dct = nullptr;
+  const float2* tw_col = nullptr;
   const int* k2_colptr = nullptr;
   const int4* k2_nodes = nullptr;
   const int* node_perm = nullptr;
@@ -70,12 +78,14 @@ struct DevPlan {
   const int* k2t_tstart = nullptr;
   const int2* k2t_ent = nullptr;
   const int* ring = nullptr;
+  const uint32_t* k2c_mask = nullptr;
+  const int* k2c_base = nullptr;
   // workspace
   float2* S1 = nullptr;   // [B][ncols][n]
   float2* S2 = nullptr;   // [B][half * NL]: forward ring-major [j][l'], adjoint K2 node order
   float2* S3 = nullptr;   // [B][Kp][NL]
   float2* S4 = nullptr;   // [B][Kp][n_t]
-  float2* Rc = nullptr;   // [B][ntargets]: K2T target sums (transposed bilinear), column order
+  float2* Rc = nullptr;   // [B][ntpad]: K2T target sums (transposed bilinear), column order
 };
 
 // Launchers (kernels.cu).  ev != nullptr: record ev[i] before stage i and ev[5] at the end.
@@ -108,6 +118,13 @@ size_t smem_dct_fast(const Consts& C);
 cudaError_t configure_dct_kernels(const Consts& C);
 cudaError_t launch_k4_fast(const DevPlan& P, bool adj, cudaStream_t s);
 size_t max_smem_needed(const Consts& C);
+// kernels_col.cu: two-stage column transforms (L = 8, n in {256, 512})
+bool col_ok(const Consts& C);
+size_t smem_k2c_fwd(const Consts& C);
+size_t smem_k2c_adj(const Consts& C);
+cudaError_t configure_col_kernels(const Consts& C);
+cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s);
+cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s);
 
 constexpr int kLaunchesForward = 5;
 constexpr int kLaunchesAdjoint = 5;
