@@ -20,6 +20,8 @@
 #include "col_engine.cuh"
 #include "tat_internal.h"
 
+#include <cstdlib>
+
 namespace tat {
 
 namespace {
@@ -45,8 +47,8 @@ using ce::cmulc;
 using ce::csub;
 
 // ================================================================== forward
-template <int n>
-__global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
+template <int n, int MINB, bool HOIST, int SKIP = 0>
+__global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
   using G = ColGeo<n>;
   constexpr int R = G::R, J = G::J, L = G::L, NG = G::NG, NRES = G::NRES;
   extern __shared__ __align__(128) float2 sm[];
@@ -66,8 +68,9 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
   for (int i = 0; i < NRES; ++i)
 #pragma unroll
     for (int r = 0; r < R; ++r) A[i][r] = __ldg(&P.tw_col[(sg + NG * i) * n + j + J * r]);
+  const float2 bpw = __ldg(&P.tw_n[(j - n / 2) & (n - 1)]);
   float2 pw[R];
-  ce::pow_tree<R>(__ldg(&P.tw_n[(j - n / 2) & (n - 1)]), pw);
+  if constexpr (HOIST) ce::pow_tree<R>(bpw, pw);
   const float2* S1 = P.S1 + (size_t)b * C.ncols * n;
   float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
   if (t == 0) {
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
     int4 nd0 = make_int4(0, 0, 0, 0);
     if (e0 + t < e1) nd0 = __ldg(&P.k2_nodes[e0 + t]);
     ac::mbar_wait(&bar[slot], (it >> 1) & 1);
-    {   // stage A
+    if (!(SKIP & 1)) {   // stage A
       const float2* xs = xbuf + slot * n;
       float2 x[R];
 #pragma unroll
@@ -104,6 +107,7 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = cmul(x[r], A[i][r]);
         ce::dftr<R, -1>(v);
+        if constexpr (!HOIST) ce::pow_tree<R>(bpw, pw);
 #pragma unroll
         for (int k1 = 1; k1 < R; ++k1) v[k1] = cmul(v[k1], pw[k1]);
 #pragma unroll
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
       }
     }
     __syncthreads();
-    {   // stage B (in place)
+    if (!(SKIP & 2)) {   // stage B (in place)
       float2 u[J];
 #pragma unroll
       for (int c = 0; c < J; ++c) u[c] = Fcur[G::widx(t, c)];
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
       for (int c = 0; c < J; ++c) Fcur[G::widx(t, c)] = u[c];
     }
     __syncthreads();
-    if (p > P0) {   // bilinear gather of the nodes with p0 = p - 1 (Alg. 1 step 3)
+    if (!(SKIP & 4) && p > P0) {   // bilinear gather of the nodes with p0 = p - 1 (Alg. 1 step 3)
       int e = e0 + t;
       int4 nd = nd0;
       while (e < e1) {
@@ -154,8 +158,8 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
 // Column p: the target values of column p (Rc, ordered by (q0, q1), moved by one bulk copy per
 // column into a double buffer) -> stage B^H (thread q0, only the present q1 are read) ->
 // stage A^H (thread (j, s)) -> residue-group partial sums -> S~1[b][p][y].
-template <int n>
-__global__ void __launch_bounds__(128, 3) k2c_adj(DevPlan P) {
+template <int n, int MINB>
+__global__ void __launch_bounds__(128, MINB) k2c_adj(DevPlan P) {
   using G = ColGeo<n>;
   constexpr int R = G::R, J = G::J, L = G::L, NG = G::NG, NRES = G::NRES, Q0 = G::Q0;
   extern __shared__ __align__(128) float2 sm[];
@@ -268,33 +272,67 @@ size_t smem_k2c_adj(const Consts& C) {
   return (size_t)Q0 * J * 8 + (size_t)2 * C.k2c_rbuf * 8 + 64;
 }
 
-cudaError_t configure_col_kernels(const Consts& C) {
-  if (!col_ok(C)) return cudaSuccess;
+static int k2c_variant() {   // experiment selector (TAT_K2C_VAR), 0 = default
+  const char* v = getenv("TAT_K2C_VAR");
+  return v ? atoi(v) : 0;
+}
+
+template <int n>
+static cudaError_t cfg_col() {
   cudaError_t e = cudaSuccess;
   const int lim = 227 * 1024;
-  if (C.n == 512) {
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2c_fwd<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2c_adj<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  } else {
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2c_fwd<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k2c_adj<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  }
+#define SETC(k) if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  SETC((k2c_fwd<n, 3, true>));
+  SETC((k2c_fwd<n, 2, true>));
+  SETC((k2c_fwd<n, 3, false>));
+  SETC((k2c_fwd<n, 3, true, 1>));
+  SETC((k2c_fwd<n, 3, true, 2>));
+  SETC((k2c_fwd<n, 3, true, 4>));
+  SETC((k2c_fwd<n, 3, true, 7>));
+  SETC((k2c_adj<n, 3>));
+  SETC((k2c_adj<n, 2>));
+#undef SETC
   return e;
+}
+
+cudaError_t configure_col_kernels(const Consts& C) {
+  if (!col_ok(C)) return cudaSuccess;
+  return C.n == 512 ? cfg_col<512>() : cfg_col<256>();
+}
+
+template <int n>
+static void launch_fwd_n(const DevPlan& P, dim3 grid, size_t sm, cudaStream_t s) {
+  switch (k2c_variant()) {
+    case 1: k2c_fwd<n, 2, true><<<grid, 128, sm, s>>>(P); break;
+    case 2: k2c_fwd<n, 3, false><<<grid, 128, sm, s>>>(P); break;
+    case 11: k2c_fwd<n, 3, true, 1><<<grid, 128, sm, s>>>(P); break;
+    case 12: k2c_fwd<n, 3, true, 2><<<grid, 128, sm, s>>>(P); break;
+    case 14: k2c_fwd<n, 3, true, 4><<<grid, 128, sm, s>>>(P); break;
+    case 17: k2c_fwd<n, 3, true, 7><<<grid, 128, sm, s>>>(P); break;
+    default: k2c_fwd<n, 3, true><<<grid, 128, sm, s>>>(P); break;
+  }
+}
+template <int n>
+static void launch_adj_n(const DevPlan& P, dim3 grid, size_t sm, cudaStream_t s) {
+  switch (k2c_variant()) {
+    case 1: k2c_adj<n, 2><<<grid, 128, sm, s>>>(P); break;
+    default: k2c_adj<n, 3><<<grid, 128, sm, s>>>(P); break;
+  }
 }
 
 cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
-  if (C.n == 512) k2c_fwd<512><<<grid, 128, smem_k2c_fwd(C), s>>>(P);
-  else k2c_fwd<256><<<grid, 128, smem_k2c_fwd(C), s>>>(P);
+  if (C.n == 512) launch_fwd_n<512>(P, grid, smem_k2c_fwd(C), s);
+  else launch_fwd_n<256>(P, grid, smem_k2c_fwd(C), s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
-  if (C.n == 512) k2c_adj<512><<<grid, 128, smem_k2c_adj(C), s>>>(P);
-  else k2c_adj<256><<<grid, 128, smem_k2c_adj(C), s>>>(P);
+  if (C.n == 512) launch_adj_n<512>(P, grid, smem_k2c_adj(C), s);
+  else launch_adj_n<256>(P, grid, smem_k2c_adj(C), s);
   return cudaGetLastError();
 }
 

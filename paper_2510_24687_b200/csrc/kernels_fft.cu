@@ -248,19 +248,30 @@ __global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const __grid_constant_
 
 // ================================================================== K2Ta: target sums
 // Transposed bilinear (D2^T, reading G12): every Cartesian target (p, q) of the half plane
-// gets the fixed-order sum of its CSR entries w * P~[node]; written in column order.
+// gets the fixed-order sum of its entries w * P~[node] (deterministic, no atomics).  One
+// thread per (target, image); a target's first two entries sit in one 16-byte record.
 __global__ void __launch_bounds__(256) k2t_sum(DevPlan P) {
   const Consts& C = P.C;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= C.ntargets) return;
   const int b = blockIdx.y;
   const float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
-  const int e0 = __ldg(&P.k2t_tstart[t]), e1 = __ldg(&P.k2t_tstart[t + 1]);
-  float2 acc = make_float2(0.f, 0.f);
-  for (int e = e0; e < e1; ++e) {
-    const int2 en = __ldg(&P.k2t_ent[e]);
-    const float w = __int_as_float(en.y);
-    acc = __ffma2_rn(make_float2(w, w), __ldg(&S2[en.x]), acc);
+  const int4 rc = __ldg(&P.k2t_rec[t]);
+  const float w0 = __int_as_float(rc.y);
+  float2 acc;
+  if (rc.z >= 0) {
+    const float2 v0 = __ldg(&S2[rc.x]), v1 = __ldg(&S2[rc.z]);
+    const float w1 = __int_as_float(rc.w);
+    acc = __fmul2_rn(make_float2(w0, w0), v0);
+    acc = __ffma2_rn(make_float2(w1, w1), v1, acc);
+  } else {
+    const int k0 = -rc.z - 1, cnt = rc.w;
+    acc = __fmul2_rn(make_float2(w0, w0), __ldg(&S2[rc.x]));
+    for (int e = 0; e < cnt - 1; ++e) {
+      const int2 en = __ldg(&P.k2t_ov[k0 + e]);
+      const float w = __int_as_float(en.y);
+      acc = __ffma2_rn(make_float2(w, w), __ldg(&S2[en.x]), acc);
+    }
   }
   P.Rc[(size_t)b * C.ntpad + t] = acc;
 }

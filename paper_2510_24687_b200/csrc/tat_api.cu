@@ -155,8 +155,8 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     if ((e = upload(p, H.node_perm, &P.node_perm, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2t_colptr, &P.k2t_colptr, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2t_tq, &P.k2t_tq, tb)) != cudaSuccess) break;
-    if ((e = upload(p, H.k2t_tstart, &P.k2t_tstart, tb)) != cudaSuccess) break;
-    if ((e = upload(p, H.k2t_ent, &P.k2t_ent, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2t_rec, &P.k2t_rec, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k2t_ov, &P.k2t_ov, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.ring, &P.ring, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.tw_col, &P.tw_col, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2c_mask, &P.k2c_mask, tb)) != cudaSuccess) break;

@@ -44,8 +44,12 @@ struct HostTables {
   // K2T transposed gather: per column p, targets (q mod N) with entry ranges
   std::vector<int> k2t_colptr;      // [ncols + 1] into targets
   std::vector<int> k2t_tq;          // [T] q mod N
-  std::vector<int> k2t_tstart;      // [T + 1] into entries
-  std::vector<int2> k2t_ent;        // [E] (src sorted node position, weight bits)
+  std::vector<int> k2t_tstart;      // [T + 1] into entries (host only: builds k2t_rec)
+  std::vector<int2> k2t_ent;        // [E] (src sorted node position, weight bits) (host only)
+  // per target: (src0, w0 bits, src1, w1 bits); one entry: src1 = src0, w1 = 0; more than
+  // two: (src0, w0 bits, -(k+1), count) with entries 1..count-1 at k2t_ov[k ..]
+  std::vector<int4> k2t_rec;        // [T]
+  std::vector<int2> k2t_ov;         // overflow entries (src, w bits)
   std::vector<int> ring;            // [n_det]
   // k2c_adj: per (column p, q0 = q mod 16L): bit q1 set if target (p, q0 + 16L q1) exists,
   // and the index of the first such target (targets of a column are ordered by (q0, q1))
@@ -75,8 +79,8 @@ struct DevPlan {
   const int* node_perm = nullptr;
   const int* k2t_colptr = nullptr;
   const int* k2t_tq = nullptr;
-  const int* k2t_tstart = nullptr;
-  const int2* k2t_ent = nullptr;
+  const int4* k2t_rec = nullptr;
+  const int2* k2t_ov = nullptr;
   const int* ring = nullptr;
   const uint32_t* k2c_mask = nullptr;
   const int* k2c_base = nullptr;
