@@ -248,32 +248,58 @@ __global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const __grid_constant_
 
 // ================================================================== K2Ta: target sums
 // Transposed bilinear (D2^T, reading G12): every Cartesian target (p, q) of the half plane
-// gets the fixed-order sum of its entries w * P~[node] (deterministic, no atomics).  One
-// thread per (target, image); a target's first two entries sit in one 16-byte record.
-__global__ void __launch_bounds__(256) k2t_sum(DevPlan P) {
-  const Consts& C = P.C;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= C.ntargets) return;
-  const int b = blockIdx.y;
-  const float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
-  const int4 rc = __ldg(&P.k2t_rec[t]);
+// gets the fixed-order sum of its entries w * P~[node] (deterministic, no atomics).
+// One CTA per (column p, image): the targets of column p only reference nodes with
+// p0 in {p-1, p}, a contiguous range of the (p0-sorted) adjoint S2 that is staged in shared
+// memory (coalesced loads, issued together with the coalesced 16-byte target records).
+constexpr int kSumKT = 2;   // target records per thread loaded before the window barrier
+
+__device__ __forceinline__ float2 k2t_target(const int4 rc, const float2* w, const int2* __restrict__ ov) {
   const float w0 = __int_as_float(rc.y);
-  float2 acc;
+  float2 acc = __fmul2_rn(make_float2(w0, w0), w[rc.x]);
   if (rc.z >= 0) {
-    const float2 v0 = __ldg(&S2[rc.x]), v1 = __ldg(&S2[rc.z]);
     const float w1 = __int_as_float(rc.w);
-    acc = __fmul2_rn(make_float2(w0, w0), v0);
-    acc = __ffma2_rn(make_float2(w1, w1), v1, acc);
+    acc = __ffma2_rn(make_float2(w1, w1), w[rc.z], acc);
   } else {
     const int k0 = -rc.z - 1, cnt = rc.w;
-    acc = __fmul2_rn(make_float2(w0, w0), __ldg(&S2[rc.x]));
     for (int e = 0; e < cnt - 1; ++e) {
-      const int2 en = __ldg(&P.k2t_ov[k0 + e]);
-      const float w = __int_as_float(en.y);
-      acc = __ffma2_rn(make_float2(w, w), __ldg(&S2[en.x]), acc);
+      const int2 en = __ldg(&ov[k0 + e]);
+      const float ww = __int_as_float(en.y);
+      acc = __ffma2_rn(make_float2(ww, ww), w[en.x], acc);
     }
   }
-  P.Rc[(size_t)b * C.ntpad + t] = acc;
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k2t_sum(DevPlan P) {
+  extern __shared__ __align__(16) float2 win[];
+  const Consts& C = P.C;
+  const int p = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int n0 = __ldg(&P.k2_colptr[p > 0 ? p - 1 : 0]), nw = __ldg(&P.k2_colptr[p + 1]) - n0;
+  const int ta = __ldg(&P.k2t_colptr[p]), tb = __ldg(&P.k2t_colptr[p + 1]);
+  int4 rec[kSumKT];
+#pragma unroll
+  for (int k = 0; k < kSumKT; ++k) {
+    const int t = ta + tid + 256 * k;
+    rec[k] = (t < tb) ? __ldg(&P.k2t_rec[t]) : make_int4(0, 0, 0, 0);
+  }
+  const float2* S2 = P.S2 + (size_t)b * C.half * C.NL + n0;
+  for (int i = tid; i < nw; i += 256) win[i] = __ldg(&S2[i]);
+  __syncthreads();
+  float2* Rc = P.Rc + (size_t)b * C.ntpad;
+  const float2* w = win - n0;
+#pragma unroll
+  for (int k = 0; k < kSumKT; ++k) {
+    const int t = ta + tid + 256 * k;
+    if (t < tb) Rc[t] = k2t_target(rec[k], w, P.k2t_ov);
+  }
+  for (int t = ta + tid + 256 * kSumKT; t < tb; t += 256) Rc[t] = k2t_target(__ldg(&P.k2t_rec[t]), w, P.k2t_ov);
+}
+
+static cudaError_t launch_k2t_sum(const DevPlan& P, cudaStream_t s) {
+  const Consts& C = P.C;
+  k2t_sum<<<dim3(C.ncols, C.batch), 256, (size_t)C.k2t_win * sizeof(float2), s>>>(P);
+  return cudaGetLastError();
 }
 
 // ================================================================== K2Tb (transpose of K2)
@@ -437,6 +463,7 @@ static cudaError_t cfg_one() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k1_fwd<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k2t_adj<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k1t_adj<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k2t_sum, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   return e;
 }
 
@@ -491,7 +518,8 @@ cudaError_t launch_k2(const DevPlan& P, cudaStream_t s) {
 }
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
-  k2t_sum<<<dim3((C.ntargets + 255) / 256, C.batch), 256, 0, s>>>(P);
+  cudaError_t e = launch_k2t_sum(P, s);
+  if (e != cudaSuccess) return e;
   if (col_ok(C)) return launch_k2c_adj(P, s);
   const dim3 grid((C.ncols + kStrip - 1) / kStrip, C.batch);
   TAT_DISPATCH_N(k2t_adj<NN><<<grid, fft_threads(C), smem_k2t(C), s>>>(P));

@@ -177,6 +177,14 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
       int mx = 0;
       for (int q = 0; q < C.ncols; ++q) mx = std::max(mx, H.k2t_colptr[q + 1] - H.k2t_colptr[q]);
       P.C.k2c_rbuf = (mx + 3) & ~1;   // even: 16-B aligned bulk-copy destinations
+      int mw = 0;
+      for (int q = 0; q < C.ncols; ++q)
+        mw = std::max(mw, H.k2_colptr[q + 1] - H.k2_colptr[q > 0 ? q - 1 : 0]);
+      P.C.k2t_win = std::max(mw, 1);
+    }
+    if ((size_t)P.C.k2t_win * 8 > 227 * 1024) {
+      e = cudaErrorInvalidConfiguration;
+      break;
     }
     if (col_ok(P.C) && smem_k2c_adj(P.C) > 227 * 1024) {
       e = cudaErrorInvalidConfiguration;

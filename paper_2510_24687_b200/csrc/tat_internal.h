@@ -27,6 +27,7 @@ struct Consts {
   int s1boxP = 0;   // TMA box extent along p for S1 tiles (box = {4 y, s1boxP p, 1})
   int ntpad = 0;    // per-image stride of Rc (ntargets rounded up to even: 16-B bulk copies)
   int k2c_rbuf = 0; // k2c_adj: entries per column target buffer (max targets per column + 2)
+  int k2t_win = 0;  // k2t_sum: max nodes with p0 in {p-1, p} over columns p
 };  // plain data: passed by value to kernels inside DevPlan
 
 // Host-side tables (float64 built, float32/int stored), uploaded by tat_plan_create.
