@@ -46,6 +46,91 @@ using ce::cmul;
 using ce::cmulc;
 using ce::csub;
 
+// ------------------------------------------------------------------ shared stage code
+// Per-thread twiddles: A[i][r] = W_N^{s_i (j + J r - n/2)} (s_i = sg + NG i), pw[k] = b^k with
+// b = W_n^{j - n/2}.
+template <int n>
+__device__ __forceinline__ void col_twiddles(const DevPlan& P, int j, int sg,
+                                             float2 (&A)[ColGeo<n>::NRES][16], float2 (&pw)[16]) {
+  using G = ColGeo<n>;
+#pragma unroll
+  for (int i = 0; i < G::NRES; ++i)
+#pragma unroll
+    for (int r = 0; r < 16; ++r) A[i][r] = __ldg(&P.tw_col[(sg + G::NG * i) * n + j + G::J * r]);
+  ce::pow_tree<16>(__ldg(&P.tw_n[(j - n / 2) & (n - 1)]), pw);
+}
+
+// stage A: samples x[r] = x[j + J r] -> W[(s + L k1, j)] for the thread's residues s
+template <int n>
+__device__ __forceinline__ void stage_a_fwd(const float2 (&x)[16], const float2 (&A)[ColGeo<n>::NRES][16],
+                                            const float2 (&pw)[16], float2* W, int j, int sg) {
+  using G = ColGeo<n>;
+#pragma unroll
+  for (int i = 0; i < G::NRES; ++i) {
+    const int s = sg + G::NG * i;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = cmul(x[r], A[i][r]);
+    ce::dftr<16, -1>(v);
+#pragma unroll
+    for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], pw[k1]);
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) W[G::widx(s + G::L * k1, j)] = v[k1];
+  }
+}
+
+// stage B: J-point DFT (sign S) of row q0 of W, in place
+template <int n, int S>
+__device__ __forceinline__ void stage_b(float2* W, int q0) {
+  using G = ColGeo<n>;
+  float2 u[G::J];
+#pragma unroll
+  for (int c = 0; c < G::J; ++c) u[c] = W[G::widx(q0, c)];
+  ce::dftr<G::J, S>(u);
+#pragma unroll
+  for (int c = 0; c < G::J; ++c) W[G::widx(q0, c)] = u[c];
+}
+
+// stage A^H: W -> acc[r] = sum over the thread's residues of the conjugate chain at j + J r
+template <int n>
+__device__ __forceinline__ void stage_a_adj(const float2* W, const float2 (&A)[ColGeo<n>::NRES][16],
+                                            const float2 (&pw)[16], int j, int sg, float2 (&acc)[16]) {
+  using G = ColGeo<n>;
+#pragma unroll
+  for (int i = 0; i < G::NRES; ++i) {
+    const int s = sg + G::NG * i;
+    float2 v[16];
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) v[k1] = W[G::widx(s + G::L * k1, j)];
+#pragma unroll
+    for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmulc(v[k1], pw[k1]);
+    ce::dftr<16, 1>(v);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const float2 w = cmulc(v[r], A[i][r]);
+      acc[r] = (i == 0) ? w : ce::cadd(acc[r], w);
+    }
+  }
+}
+
+// residue-group partial sums -> W[0..n) (fixed order); starts with the barrier that ends the
+// stage-A^H reads of W, ends with a barrier (W[y] = sum, y in [0, n))
+template <int n>
+__device__ __forceinline__ void residue_reduce(float2* W, const float2 (&acc)[16], int j, int sg) {
+  using G = ColGeo<n>;
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) W[sg * n + j + G::J * r] = acc[r];
+  __syncthreads();
+}
+template <int n>
+__device__ __forceinline__ float2 residue_sum(const float2* W, int y) {
+  float2 s = W[y];
+#pragma unroll
+  for (int g = 1; g < ColGeo<n>::NG; ++g) s = ce::cadd(s, W[g * n + y]);
+  return s;
+}
+
 // ================================================================== forward
 template <int n, int MINB, bool HOIST, int SKIP = 0>
 __global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
@@ -260,6 +345,95 @@ __global__ void __launch_bounds__(128, MINB) k2c_adj(DevPlan P) {
   }
 }
 
+// ================================================================== K1 forward (row pairs)
+// z = f_y + i f_{y+1}; Z[p] = sum_x z[x] W_N^{p (x - n/2)} (Alg. 1 steps 1-2, the zero-extended
+// row DFT); S1[b][p][y] = (Z[p] + conj Z[-p]) / 2, S1[b][p][y+1] = (Z[p] - conj Z[-p]) / (2i)
+// for p in [0, N/2].  One CTA (128 threads) per two row pairs (rows y0..y0+3), so that every
+// p writes one full 32-byte sector of S1.
+template <int n>
+__global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const float* __restrict__ f) {
+  using G = ColGeo<n>;
+  extern __shared__ __align__(128) float2 sm[];
+  const Consts& C = P.C;
+  const int t = threadIdx.x, j = t % G::J, sg = t / G::J;
+  const int b = blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
+  float2* W0 = sm;
+  float2* W1 = sm + G::Q0 * G::J;
+  float2 A[G::NRES][16], pw[16];
+  col_twiddles<n>(P, j, sg, A, pw);
+  const float* r0 = f + ((size_t)b * n + y0) * n;
+#pragma unroll 1
+  for (int pr = 0; pr < 2; ++pr) {
+    float2 x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      x[r] = make_float2(__ldg(&r0[(2 * pr) * n + j + G::J * r]), __ldg(&r0[(2 * pr + 1) * n + j + G::J * r]));
+    stage_a_fwd<n>(x, A, pw, pr ? W1 : W0, j, sg);
+  }
+  __syncthreads();
+  stage_b<n, -1>(W0, t);
+  stage_b<n, -1>(W1, t);
+  __syncthreads();
+  float2* out = P.S1 + (size_t)b * C.ncols * n + y0;
+  for (int p = t; p < C.ncols; p += G::T) {
+    const int ia = G::fq(p), im = G::fq((N - p) & (N - 1));
+    const float2 za = W0[ia], zm = W0[im], zb = W1[ia], zn = W1[im];
+    float4* o = reinterpret_cast<float4*>(out + (size_t)p * n);
+    o[0] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y), 0.5f * (za.y + zm.y), -0.5f * (za.x - zm.x));
+    o[1] = make_float4(0.5f * (zb.x + zn.x), 0.5f * (zb.y - zn.y), 0.5f * (zb.y + zn.y), -0.5f * (zb.x - zn.x));
+  }
+}
+
+// ================================================================== K1T (transpose of K1)
+// Z[p] = C_y[p] + i C_{y+1}[p] and Z[-p] = conj C_y[p] + i conj C_{y+1}[p] (Hermitian
+// completion; C[0], C[N/2] -> 2 Re), conjugate transform, f~_y = Re z~, f~_{y+1} = Im z~.
+// Two row pairs per CTA (32-byte sectors of S~1 per p).
+template <int n>
+__global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, float* __restrict__ fout) {
+  using G = ColGeo<n>;
+  extern __shared__ __align__(128) float2 sm[];
+  const Consts& C = P.C;
+  const int t = threadIdx.x, j = t % G::J, sg = t / G::J;
+  const int b = blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
+  float2* W0 = sm;
+  float2* W1 = sm + G::Q0 * G::J;
+  float2 A[G::NRES][16], pw[16];
+  col_twiddles<n>(P, j, sg, A, pw);
+  const float2* in = P.S1 + (size_t)b * C.ncols * n + y0;
+  for (int p = t; p < C.ncols; p += G::T) {
+    const float4* ip = reinterpret_cast<const float4*>(in + (size_t)p * n);
+    const float4 a = __ldg(ip), c = __ldg(ip + 1);   // (C_y, C_{y+1}), (C_{y+2}, C_{y+3})
+    const int ia = G::fq(p);
+    if (p == 0 || p == N / 2) {
+      W0[ia] = make_float2(2.f * a.x, 2.f * a.z);
+      W1[ia] = make_float2(2.f * c.x, 2.f * c.z);
+    } else {
+      const int im = G::fq(N - p);
+      W0[ia] = make_float2(a.x - a.w, a.y + a.z);
+      W0[im] = make_float2(a.x + a.w, -a.y + a.z);
+      W1[ia] = make_float2(c.x - c.w, c.y + c.z);
+      W1[im] = make_float2(c.x + c.w, -c.y + c.z);
+    }
+  }
+  __syncthreads();
+  stage_b<n, 1>(W0, t);
+  stage_b<n, 1>(W1, t);
+  __syncthreads();
+#pragma unroll 1
+  for (int pr = 0; pr < 2; ++pr) {
+    float2* W = pr ? W1 : W0;
+    float2 acc[16];
+    stage_a_adj<n>(W, A, pw, j, sg, acc);
+    residue_reduce<n>(W, acc, j, sg);
+    float* o = fout + ((size_t)b * n + y0 + 2 * pr) * n;
+    for (int xx = t; xx < n; xx += G::T) {
+      const float2 z = residue_sum<n>(W, xx);
+      o[xx] = z.x;
+      o[n + xx] = z.y;
+    }
+  }
+}
+
 // ================================================================== dispatch
 bool col_ok(const Consts& C) { return C.Lres == 8 && (C.n == 256 || C.n == 512); }
 
@@ -271,6 +445,8 @@ size_t smem_k2c_adj(const Consts& C) {
   const int Q0 = 128, J = C.n / 16;
   return (size_t)Q0 * J * 8 + (size_t)2 * C.k2c_rbuf * 8 + 64;
 }
+
+size_t smem_k1c(const Consts& C) { return (size_t)2 * 128 * (C.n / 16) * 8; }
 
 static int k2c_variant() {   // experiment selector (TAT_K2C_VAR), 0 = default
   const char* v = getenv("TAT_K2C_VAR");
@@ -291,6 +467,8 @@ static cudaError_t cfg_col() {
   SETC((k2c_fwd<n, 3, true, 7>));
   SETC((k2c_adj<n, 3>));
   SETC((k2c_adj<n, 2>));
+  SETC((k1c_fwd<n>));
+  SETC((k1c_adj<n>));
 #undef SETC
   return e;
 }
@@ -333,6 +511,22 @@ cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
   if (C.n == 512) launch_adj_n<512>(P, grid, smem_k2c_adj(C), s);
   else launch_adj_n<256>(P, grid, smem_k2c_adj(C), s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k1c_fwd(const DevPlan& P, const float* f, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid(C.n / 4, C.batch);
+  if (C.n == 512) k1c_fwd<512><<<grid, 128, smem_k1c(C), s>>>(P, f);
+  else k1c_fwd<256><<<grid, 128, smem_k1c(C), s>>>(P, f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k1c_adj(const DevPlan& P, float* f, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid(C.n / 4, C.batch);
+  if (C.n == 512) k1c_adj<512><<<grid, 128, smem_k1c(C), s>>>(P, f);
+  else k1c_adj<256><<<grid, 128, smem_k1c(C), s>>>(P, f);
   return cudaGetLastError();
 }
 
