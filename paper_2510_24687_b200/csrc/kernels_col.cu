@@ -348,10 +348,13 @@ __global__ void __launch_bounds__(128, MINB) k2c_adj(DevPlan P) {
 // ================================================================== K1 forward (row pairs)
 // z = f_y + i f_{y+1}; Z[p] = sum_x z[x] W_N^{p (x - n/2)} (Alg. 1 steps 1-2, the zero-extended
 // row DFT); S1[b][p][y] = (Z[p] + conj Z[-p]) / 2, S1[b][p][y+1] = (Z[p] - conj Z[-p]) / (2i)
-// for p in [0, N/2].  One CTA (128 threads) per two row pairs (rows y0..y0+3), so that every
-// p writes one full 32-byte sector of S1.
+// for p in [0, N/2].  One CTA (128 threads) per two row pairs (rows y0..y0+3); the [p][4 y]
+// output tiles are transposed into S1 by TMA tensor stores (32-byte rows per p).
+constexpr int kK1BoxP = 128;   // p extent of one S1 tile (= C.s1boxP on this path)
+
 template <int n>
-__global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const float* __restrict__ f) {
+__global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_constant__ CUtensorMap tm,
+                                                  const float* __restrict__ f) {
   using G = ColGeo<n>;
   extern __shared__ __align__(128) float2 sm[];
   const Consts& C = P.C;
@@ -359,6 +362,7 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const float* __rest
   const int b = blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
   float2* W0 = sm;
   float2* W1 = sm + G::Q0 * G::J;
+  float2* stg = sm + 2 * G::Q0 * G::J;   // 2 tiles [kK1BoxP][4]
   float2 A[G::NRES][16], pw[16];
   col_twiddles<n>(P, j, sg, A, pw);
   const float* r0 = f + ((size_t)b * n + y0) * n;
@@ -374,22 +378,39 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const float* __rest
   stage_b<n, -1>(W0, t);
   stage_b<n, -1>(W1, t);
   __syncthreads();
-  float2* out = P.S1 + (size_t)b * C.ncols * n + y0;
-  for (int p = t; p < C.ncols; p += G::T) {
-    const int ia = G::fq(p), im = G::fq((N - p) & (N - 1));
-    const float2 za = W0[ia], zm = W0[im], zb = W1[ia], zn = W1[im];
-    float4* o = reinterpret_cast<float4*>(out + (size_t)p * n);
-    o[0] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y), 0.5f * (za.y + zm.y), -0.5f * (za.x - zm.x));
-    o[1] = make_float4(0.5f * (zb.x + zn.x), 0.5f * (zb.y - zn.y), 0.5f * (zb.y + zn.y), -0.5f * (zb.x - zn.x));
+  const int nch = (C.ncols + kK1BoxP - 1) / kK1BoxP;
+  for (int c = 0; c < nch; ++c) {
+    float4* tile = reinterpret_cast<float4*>(stg + (c & 1) * kK1BoxP * 4);
+    if (c >= 2) {   // the store issued from this slot two chunks ago has read its tile
+      if (t == 0) ac::bulk_wait_read<1>();
+      __syncthreads();
+    }
+    const int p = c * kK1BoxP + t;
+    if (p < C.ncols) {
+      const int ia = G::fq(p), im = G::fq((N - p) & (N - 1));
+      const float2 za = W0[ia], zm = W0[im], zb = W1[ia], zn = W1[im];
+      tile[2 * t] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y), 0.5f * (za.y + zm.y),
+                                -0.5f * (za.x - zm.x));
+      tile[2 * t + 1] = make_float4(0.5f * (zb.x + zn.x), 0.5f * (zb.y - zn.y), 0.5f * (zb.y + zn.y),
+                                    -0.5f * (zb.x - zn.x));
+    }
+    ac::fence_proxy_async();
+    __syncthreads();
+    if (t == 0) {
+      ac::tma_store_3d(&tm, tile, y0, c * kK1BoxP, b);
+      ac::bulk_commit();
+    }
   }
+  if (t == 0) ac::bulk_wait_all();
 }
 
 // ================================================================== K1T (transpose of K1)
 // Z[p] = C_y[p] + i C_{y+1}[p] and Z[-p] = conj C_y[p] + i conj C_{y+1}[p] (Hermitian
 // completion; C[0], C[N/2] -> 2 Re), conjugate transform, f~_y = Re z~, f~_{y+1} = Im z~.
-// Two row pairs per CTA (32-byte sectors of S~1 per p).
+// Two row pairs per CTA; the [p][4 y] tiles of S~1 arrive by TMA tensor loads.
 template <int n>
-__global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, float* __restrict__ fout) {
+__global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_constant__ CUtensorMap tm,
+                                                  float* __restrict__ fout) {
   using G = ColGeo<n>;
   extern __shared__ __align__(128) float2 sm[];
   const Consts& C = P.C;
@@ -397,25 +418,47 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, float* __restrict__
   const int b = blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
   float2* W0 = sm;
   float2* W1 = sm + G::Q0 * G::J;
-  float2 A[G::NRES][16], pw[16];
-  col_twiddles<n>(P, j, sg, A, pw);
-  const float2* in = P.S1 + (size_t)b * C.ncols * n + y0;
-  for (int p = t; p < C.ncols; p += G::T) {
-    const float4* ip = reinterpret_cast<const float4*>(in + (size_t)p * n);
-    const float4 a = __ldg(ip), c = __ldg(ip + 1);   // (C_y, C_{y+1}), (C_{y+2}, C_{y+3})
-    const int ia = G::fq(p);
-    if (p == 0 || p == N / 2) {
-      W0[ia] = make_float2(2.f * a.x, 2.f * a.z);
-      W1[ia] = make_float2(2.f * c.x, 2.f * c.z);
-    } else {
-      const int im = G::fq(N - p);
-      W0[ia] = make_float2(a.x - a.w, a.y + a.z);
-      W0[im] = make_float2(a.x + a.w, -a.y + a.z);
-      W1[ia] = make_float2(c.x - c.w, c.y + c.z);
-      W1[im] = make_float2(c.x + c.w, -c.y + c.z);
+  float2* stg = sm + 2 * G::Q0 * G::J;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 2 * kK1BoxP * 4);
+  const int nch = (C.ncols + kK1BoxP - 1) / kK1BoxP;
+  if (t == 0) {
+    ac::mbar_init(&bar[0], 1);
+    ac::mbar_init(&bar[1], 1);
+    ac::fence_mbar_init();
+    for (int c = 0; c < 2 && c < nch; ++c) {
+      ac::mbar_expect_tx(&bar[c], kK1BoxP * 32);
+      ac::tma_load_3d(stg + c * kK1BoxP * 4, &tm, y0, c * kK1BoxP, b, &bar[c]);
     }
   }
+  float2 A[G::NRES][16], pw[16];
+  col_twiddles<n>(P, j, sg, A, pw);
   __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int slot = c & 1;
+    ac::mbar_wait(&bar[slot], (c >> 1) & 1);
+    const float4* tile = reinterpret_cast<const float4*>(stg + slot * kK1BoxP * 4);
+    const int p = c * kK1BoxP + t;
+    if (p < C.ncols) {
+      const float4 a = tile[2 * t], cc = tile[2 * t + 1];   // (C_y, C_{y+1}), (C_{y+2}, C_{y+3})
+      const int ia = G::fq(p);
+      if (p == 0 || p == N / 2) {
+        W0[ia] = make_float2(2.f * a.x, 2.f * a.z);
+        W1[ia] = make_float2(2.f * cc.x, 2.f * cc.z);
+      } else {
+        const int im = G::fq(N - p);
+        W0[ia] = make_float2(a.x - a.w, a.y + a.z);
+        W0[im] = make_float2(a.x + a.w, -a.y + a.z);
+        W1[ia] = make_float2(cc.x - cc.w, cc.y + cc.z);
+        W1[im] = make_float2(cc.x + cc.w, -cc.y + cc.z);
+      }
+    }
+    __syncthreads();   // tile consumed
+    if (t == 0 && c + 2 < nch) {
+      ac::fence_proxy_async();
+      ac::mbar_expect_tx(&bar[slot], kK1BoxP * 32);
+      ac::tma_load_3d(stg + slot * kK1BoxP * 4, &tm, y0, (c + 2) * kK1BoxP, b, &bar[slot]);
+    }
+  }
   stage_b<n, 1>(W0, t);
   stage_b<n, 1>(W1, t);
   __syncthreads();
@@ -446,7 +489,7 @@ size_t smem_k2c_adj(const Consts& C) {
   return (size_t)Q0 * J * 8 + (size_t)2 * C.k2c_rbuf * 8 + 64;
 }
 
-size_t smem_k1c(const Consts& C) { return (size_t)2 * 128 * (C.n / 16) * 8; }
+size_t smem_k1c(const Consts& C) { return (size_t)2 * 128 * (C.n / 16) * 8 + 2 * kK1BoxP * 32 + 64; }
 
 static int k2c_variant() {   // experiment selector (TAT_K2C_VAR), 0 = default
   const char* v = getenv("TAT_K2C_VAR");
@@ -514,19 +557,19 @@ cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_k1c_fwd(const DevPlan& P, const float* f, cudaStream_t s) {
+cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s) {
   const Consts& C = P.C;
   const dim3 grid(C.n / 4, C.batch);
-  if (C.n == 512) k1c_fwd<512><<<grid, 128, smem_k1c(C), s>>>(P, f);
-  else k1c_fwd<256><<<grid, 128, smem_k1c(C), s>>>(P, f);
+  if (C.n == 512) k1c_fwd<512><<<grid, 128, smem_k1c(C), s>>>(P, tm, f);
+  else k1c_fwd<256><<<grid, 128, smem_k1c(C), s>>>(P, tm, f);
   return cudaGetLastError();
 }
 
-cudaError_t launch_k1c_adj(const DevPlan& P, float* f, cudaStream_t s) {
+cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s) {
   const Consts& C = P.C;
   const dim3 grid(C.n / 4, C.batch);
-  if (C.n == 512) k1c_adj<512><<<grid, 128, smem_k1c(C), s>>>(P, f);
-  else k1c_adj<256><<<grid, 128, smem_k1c(C), s>>>(P, f);
+  if (C.n == 512) k1c_adj<512><<<grid, 128, smem_k1c(C), s>>>(P, tm, f);
+  else k1c_adj<256><<<grid, 128, smem_k1c(C), s>>>(P, tm, f);
   return cudaGetLastError();
 }
 

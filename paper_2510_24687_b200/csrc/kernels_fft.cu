@@ -505,7 +505,7 @@ cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out) {
 
 cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s) {
   const Consts& C = P.C;
-  if (col_ok(C)) return launch_k1c_fwd(P, f, s);
+  if (col_ok(C)) return launch_k1c_fwd(P, tm, f, s);
   const dim3 grid(C.n / 4, C.batch);
   TAT_DISPATCH_N(k1_fwd<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P, tm, f));
   return cudaGetLastError();
@@ -528,7 +528,7 @@ cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s) {
 }
 cudaError_t launch_k1t(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s) {
   const Consts& C = P.C;
-  if (col_ok(C)) return launch_k1c_adj(P, f, s);
+  if (col_ok(C)) return launch_k1c_adj(P, tm, f, s);
   const dim3 grid(C.n / 4, C.batch);
   TAT_DISPATCH_N(k1t_adj<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P, tm, f));
   return cudaGetLastError();

@@ -99,6 +99,7 @@ std::string derive_consts(int n, int n_det, int n_t, double R, double c, double 
     const int lim = std::min(256, C.Lres * rs / 8);
     C.s1boxP = 1;
     while (C.s1boxP * 2 <= lim) C.s1boxP *= 2;
+    if (col_ok(C)) C.s1boxP = 128;   // kernels_col.cu K1/K1T tiles
   }
   code = 0;
   return "";

@@ -130,8 +130,8 @@ size_t smem_k2c_adj(const Consts& C);
 cudaError_t configure_col_kernels(const Consts& C);
 cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s);
-cudaError_t launch_k1c_fwd(const DevPlan& P, const float* f, cudaStream_t s);
-cudaError_t launch_k1c_adj(const DevPlan& P, float* f, cudaStream_t s);
+cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
+cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s);
 
 constexpr int kLaunchesForward = 5;
 constexpr int kLaunchesAdjoint = 5;
