@@ -105,6 +105,7 @@ constexpr int kThreads = 256;
 size_t max_smem_needed(const Consts& C) {
   size_t s = smem_fft4(C);                                         // K1/K2/K2T/K1T
   if (col_ok(C)) s = std::max(s, smem_k2c_fwd(C));                 // K2 two-stage
+  if (dct4_ok(C)) s = std::max(s, smem_k4c(C));
   if (dct_fast_r(C)) s = std::max(s, smem_dct_fast(C));            // K4 / K4T
   else s = std::max(s, (size_t)2 * 2 * C.M * sizeof(float2));
   if (ring_fast_ok(C)) s = std::max(s, smem_ring_fast(C));           // K3/K5
@@ -300,7 +301,8 @@ cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float*
   else k3_angular_mult<<<dim3((C.NL + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[3], s);
-  if (dct_fast_r(C)) e = launch_k4_fast(P, false, s);
+  if (dct4_ok(C)) e = launch_k4c(P, false, s);
+  else if (dct_fast_r(C)) e = launch_k4_fast(P, false, s);
   else k4_dct<<<dim3(C.Kp, B), kThreads, smem_dct(C), s>>>(P);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[4], s);
@@ -322,7 +324,8 @@ cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float*
   else k5t_analysis<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
-  if (dct_fast_r(C)) e = launch_k4_fast(P, true, s);
+  if (dct4_ok(C)) e = launch_k4c(P, true, s);
+  else if (dct_fast_r(C)) e = launch_k4_fast(P, true, s);
   else k4t_dct<<<dim3(C.Kp, B), kThreads, smem_dct(C), s>>>(P);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[2], s);

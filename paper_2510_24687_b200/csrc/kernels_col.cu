@@ -28,13 +28,13 @@ namespace {
 
 constexpr int kStripC = 16;   // columns per CTA (k2c_fwd recomputes one halo column)
 
-template <int n>
+template <int n_, int L_ = 8>
 struct ColGeo {
-  static constexpr int L = 8, R = 16, J = n / R, Q0 = R * L, T = Q0;
+  static constexpr int n = n_, L = L_, R = 16, J = n / R, Q0 = R * L, T = Q0;
   static constexpr int NG = T / J;        // residue groups (threads sharing j)
-  static constexpr int NRES = J / R;      // residues per thread in stage A
-  static constexpr int LGQ0 = 7;          // log2 Q0
-  static_assert(J >= R && J <= 32, "n in {256, 512}");
+  static constexpr int NRES = J * L / T;  // residues per thread in stage A
+  static constexpr int LGQ0 = (L == 8) ? 7 : 6;   // log2 Q0
+  static_assert(J >= R && J <= 32 && (L == 8 || L == 4), "n in {256, 512}, L in {4, 8}");
   // element (q0, c) of a column buffer [Q0][J]: XOR swizzle, conflict-free for both stages
   __device__ static __forceinline__ int widx(int q0, int c) { return q0 * J + (c ^ (q0 & (J - 1))); }
   __device__ static __forceinline__ int fq(int q) { return widx(q & (Q0 - 1), q >> LGQ0); }
@@ -47,24 +47,24 @@ using ce::cmulc;
 using ce::csub;
 
 // ------------------------------------------------------------------ shared stage code
-// Per-thread twiddles: A[i][r] = W_N^{s_i (j + J r - n/2)} (s_i = sg + NG i), pw[k] = b^k with
-// b = W_n^{j - n/2}.
-template <int n>
-__device__ __forceinline__ void col_twiddles(const DevPlan& P, int j, int sg,
-                                             float2 (&A)[ColGeo<n>::NRES][16], float2 (&pw)[16]) {
-  using G = ColGeo<n>;
+// Per-thread twiddles: A[i][r] = tab[s_i][j + J r] (s_i = sg + NG i; for the column transform
+// tab = tw_col, W_N^{s (y - n/2)}), pw[k] = b^k with b = W_n^{j - shift}.
+template <class G>
+__device__ __forceinline__ void col_twiddles(const float2* __restrict__ tab, const float2* __restrict__ tw_n,
+                                             int shift, int j, int sg, float2 (&A)[G::NRES][16],
+                                             float2 (&pw)[16]) {
+  constexpr int n = G::n;
 #pragma unroll
   for (int i = 0; i < G::NRES; ++i)
 #pragma unroll
-    for (int r = 0; r < 16; ++r) A[i][r] = __ldg(&P.tw_col[(sg + G::NG * i) * n + j + G::J * r]);
-  ce::pow_tree<16>(__ldg(&P.tw_n[(j - n / 2) & (n - 1)]), pw);
+    for (int r = 0; r < 16; ++r) A[i][r] = __ldg(&tab[(sg + G::NG * i) * n + j + G::J * r]);
+  ce::pow_tree<16>(__ldg(&tw_n[(j - shift) & (n - 1)]), pw);
 }
 
 // stage A: samples x[r] = x[j + J r] -> W[(s + L k1, j)] for the thread's residues s
-template <int n>
-__device__ __forceinline__ void stage_a_fwd(const float2 (&x)[16], const float2 (&A)[ColGeo<n>::NRES][16],
+template <class G>
+__device__ __forceinline__ void stage_a_fwd(const float2 (&x)[16], const float2 (&A)[G::NRES][16],
                                             const float2 (&pw)[16], float2* W, int j, int sg) {
-  using G = ColGeo<n>;
 #pragma unroll
   for (int i = 0; i < G::NRES; ++i) {
     const int s = sg + G::NG * i;
@@ -80,9 +80,8 @@ __device__ __forceinline__ void stage_a_fwd(const float2 (&x)[16], const float2 
 }
 
 // stage B: J-point DFT (sign S) of row q0 of W, in place
-template <int n, int S>
+template <class G, int S>
 __device__ __forceinline__ void stage_b(float2* W, int q0) {
-  using G = ColGeo<n>;
   float2 u[G::J];
 #pragma unroll
   for (int c = 0; c < G::J; ++c) u[c] = W[G::widx(q0, c)];
@@ -92,10 +91,9 @@ __device__ __forceinline__ void stage_b(float2* W, int q0) {
 }
 
 // stage A^H: W -> acc[r] = sum over the thread's residues of the conjugate chain at j + J r
-template <int n>
-__device__ __forceinline__ void stage_a_adj(const float2* W, const float2 (&A)[ColGeo<n>::NRES][16],
+template <class G>
+__device__ __forceinline__ void stage_a_adj(const float2* W, const float2 (&A)[G::NRES][16],
                                             const float2 (&pw)[16], int j, int sg, float2 (&acc)[16]) {
-  using G = ColGeo<n>;
 #pragma unroll
   for (int i = 0; i < G::NRES; ++i) {
     const int s = sg + G::NG * i;
@@ -115,19 +113,19 @@ __device__ __forceinline__ void stage_a_adj(const float2* W, const float2 (&A)[C
 
 // residue-group partial sums -> W[0..n) (fixed order); starts with the barrier that ends the
 // stage-A^H reads of W, ends with a barrier (W[y] = sum, y in [0, n))
-template <int n>
+template <class G>
 __device__ __forceinline__ void residue_reduce(float2* W, const float2 (&acc)[16], int j, int sg) {
-  using G = ColGeo<n>;
+  constexpr int n = G::n;
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < 16; ++r) W[sg * n + j + G::J * r] = acc[r];
   __syncthreads();
 }
-template <int n>
+template <class G>
 __device__ __forceinline__ float2 residue_sum(const float2* W, int y) {
   float2 s = W[y];
 #pragma unroll
-  for (int g = 1; g < ColGeo<n>::NG; ++g) s = ce::cadd(s, W[g * n + y]);
+  for (int g = 1; g < G::NG; ++g) s = ce::cadd(s, W[g * G::n + y]);
   return s;
 }
 
@@ -364,7 +362,7 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
   float2* W1 = sm + G::Q0 * G::J;
   float2* stg = sm + 2 * G::Q0 * G::J;   // 2 tiles [kK1BoxP][4]
   float2 A[G::NRES][16], pw[16];
-  col_twiddles<n>(P, j, sg, A, pw);
+  col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float* r0 = f + ((size_t)b * n + y0) * n;
 #pragma unroll 1
   for (int pr = 0; pr < 2; ++pr) {
@@ -372,11 +370,11 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
 #pragma unroll
     for (int r = 0; r < 16; ++r)
       x[r] = make_float2(__ldg(&r0[(2 * pr) * n + j + G::J * r]), __ldg(&r0[(2 * pr + 1) * n + j + G::J * r]));
-    stage_a_fwd<n>(x, A, pw, pr ? W1 : W0, j, sg);
+    stage_a_fwd<G>(x, A, pw, pr ? W1 : W0, j, sg);
   }
   __syncthreads();
-  stage_b<n, -1>(W0, t);
-  stage_b<n, -1>(W1, t);
+  stage_b<G, -1>(W0, t);
+  stage_b<G, -1>(W1, t);
   __syncthreads();
   const int nch = (C.ncols + kK1BoxP - 1) / kK1BoxP;
   for (int c = 0; c < nch; ++c) {
@@ -431,7 +429,7 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
     }
   }
   float2 A[G::NRES][16], pw[16];
-  col_twiddles<n>(P, j, sg, A, pw);
+  col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   __syncthreads();
   for (int c = 0; c < nch; ++c) {
     const int slot = c & 1;
@@ -459,25 +457,112 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
       ac::tma_load_3d(stg + slot * kK1BoxP * 4, &tm, y0, (c + 2) * kK1BoxP, b, &bar[slot]);
     }
   }
-  stage_b<n, 1>(W0, t);
-  stage_b<n, 1>(W1, t);
+  stage_b<G, 1>(W0, t);
+  stage_b<G, 1>(W1, t);
   __syncthreads();
 #pragma unroll 1
   for (int pr = 0; pr < 2; ++pr) {
     float2* W = pr ? W1 : W0;
     float2 acc[16];
-    stage_a_adj<n>(W, A, pw, j, sg, acc);
-    residue_reduce<n>(W, acc, j, sg);
+    stage_a_adj<G>(W, A, pw, j, sg, acc);
+    residue_reduce<G>(W, acc, j, sg);
     float* o = fout + ((size_t)b * n + y0 + 2 * pr) * n;
     for (int xx = t; xx < n; xx += G::T) {
-      const float2 z = residue_sum<n>(W, xx);
+      const float2 z = residue_sum<G>(W, xx);
       o[xx] = z.x;
       o[n + xx] = z.y;
     }
   }
 }
 
+// ================================================================== K4 / K4T (DCT-I)
+// lambda <-> t cosine transforms (Alg. 1 step 5, E:inverse_cos_tr P:L475-478; Alg. 2 step 3):
+//   out[u] = (X(u) + X(-u)) / 2,  X(u) = sum_i c_i W_2M^{i u},  2M = 12 n,
+// with the inputs decimated by 3 (i = 3 i' + e, i' < n): X(u) = sum_e W_2M^{e u} Y_e(u mod 4n),
+// Y_e = the 4n-point DFT of c_{3 i' + e} -- three two-stage transforms (L = 4) per row, one
+// per 64-thread group.  The single input i = 3n (j = J, forward only) adds h_J cos(pi u / 2).
+//   K4  (ADJ = false): c_j = H[k][j] (S3 row, j <= J), out for u = m + 1, m < n_t -> S4 row
+//   K4T (ADJ = true) : c_i = G~[k][i - 1] (S4 row, 1 <= i <= n_t), out for u = j <= J, then
+//                      x (-i)^k omega m'[k][j] -> S3 row
+template <int n, bool ADJ>
+__global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
+  using G = ColGeo<n, 4>;
+  constexpr int N4 = 4 * n;
+  extern __shared__ __align__(128) float2 sm[];
+  const Consts& C = P.C;
+  const int t = threadIdx.x, e = t / G::T, tl = t % G::T, j = tl % G::J, sg = tl / G::J;
+  const int b = blockIdx.y, k = blockIdx.x;
+  const int M2 = 2 * C.M, NL = C.NL, n_t = C.n_t;
+  const float2* in = ADJ ? P.S4 + ((size_t)b * C.Kp + k) * n_t : P.S3 + ((size_t)b * C.Kp + k) * NL;
+  const int cnt = ADJ ? n_t : NL;
+  float2 x[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int i = 3 * (j + G::J * r) + e, src = ADJ ? i - 1 : i;
+    x[r] = (src >= 0 && src < cnt) ? __ldg(&in[src]) : make_float2(0.f, 0.f);
+  }
+  float2 A[G::NRES][16], pw[16];
+  col_twiddles<G>(P.tw_dct4, P.tw_n, 0, j, sg, A, pw);
+  float2* W = sm + e * N4;
+  stage_a_fwd<G>(x, A, pw, W, j, sg);
+  __syncthreads();
+  stage_b<G, -1>(W, tl);
+  __syncthreads();
+  auto X = [&](int u) -> float2 {   // u in (-4n, 4n)
+    const int v = u & (N4 - 1);
+    const int u1 = ((u % M2) + M2) % M2, u2 = ((2 * u) % M2 + M2) % M2;
+    const float2 y0 = sm[G::fq(v)], y1 = sm[N4 + G::fq(v)], y2 = sm[2 * N4 + G::fq(v)];
+    return ce::cadd(y0, ce::cadd(cmul(y1, __ldg(&P.tw_dct[u1])), cmul(y2, __ldg(&P.tw_dct[u2]))));
+  };
+  if (!ADJ) {
+    const float2 hJ = (NL == 3 * n + 1) ? __ldg(&in[3 * n]) : make_float2(0.f, 0.f);
+    float2* out = P.S4 + ((size_t)b * C.Kp + k) * n_t;
+    for (int m = t; m < n_t; m += blockDim.x) {
+      const int u = m + 1;
+      float2 g = fe::cscale(ce::cadd(X(u), X(-u)), 0.5f);
+      if ((u & 3) == 0) g = ce::cadd(g, hJ);
+      else if ((u & 3) == 2) g = csub(g, hJ);
+      out[m] = g;
+    }
+  } else {
+    float2* out = P.S3 + ((size_t)b * C.Kp + k) * NL;
+    const float om = (float)C.omega;
+    for (int jj = t; jj < NL; jj += blockDim.x) {
+      const float2 y = fe::cscale(ce::cadd(X(jj), X(-jj)), 0.5f);
+      const float2 z = fe::cscale(y, om * __ldg(&P.mult[(size_t)k * NL + jj]));
+      float2 o;
+      switch ((-k) & 3) {   // (-i)^k
+        case 0: o = z; break;
+        case 1: o = make_float2(-z.y, z.x); break;
+        case 2: o = make_float2(-z.x, -z.y); break;
+        default: o = make_float2(z.y, -z.x); break;
+      }
+      out[jj] = o;
+    }
+  }
+}
+
 // ================================================================== dispatch
+bool dct4_ok(const Consts& C) {
+  return (C.n == 256 || C.n == 512) && 2L * C.M == 12L * C.n && C.J <= 3 * C.n &&
+         C.n_t <= 3 * C.n - 1;
+}
+size_t smem_k4c(const Consts& C) { return (size_t)3 * 4 * C.n * 8; }
+
+cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid(C.Kp, C.batch);
+  const size_t sm = smem_k4c(C);
+  if (C.n == 512) {
+    if (adj) k4c_dct<512, true><<<grid, 192, sm, s>>>(P);
+    else k4c_dct<512, false><<<grid, 192, sm, s>>>(P);
+  } else {
+    if (adj) k4c_dct<256, true><<<grid, 192, sm, s>>>(P);
+    else k4c_dct<256, false><<<grid, 192, sm, s>>>(P);
+  }
+  return cudaGetLastError();
+}
+
 bool col_ok(const Consts& C) { return C.Lres == 8 && (C.n == 256 || C.n == 512); }
 
 size_t smem_k2c_fwd(const Consts& C) {
@@ -512,12 +597,14 @@ static cudaError_t cfg_col() {
   SETC((k2c_adj<n, 2>));
   SETC((k1c_fwd<n>));
   SETC((k1c_adj<n>));
+  SETC((k4c_dct<n, false>));
+  SETC((k4c_dct<n, true>));
 #undef SETC
   return e;
 }
 
 cudaError_t configure_col_kernels(const Consts& C) {
-  if (!col_ok(C)) return cudaSuccess;
+  if (!col_ok(C) && !dct4_ok(C)) return cudaSuccess;
   return C.n == 512 ? cfg_col<512>() : cfg_col<256>();
 }
 

@@ -206,6 +206,9 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
   H.tw_col.resize((size_t)L * n);
   for (int s = 0; s < L; ++s)
     for (int y = 0; y < n; ++y) H.tw_col[(size_t)s * n + y] = root((long)s * (y - n / 2), N, -1);
+  H.tw_dct4.resize((size_t)4 * n);
+  for (int s = 0; s < 4; ++s)
+    for (int i = 0; i < n; ++i) H.tw_dct4[(size_t)s * n + i] = root((long)s * i, 4L * n, -1);
   H.tw_dct.resize(2 * (size_t)C.M);
   for (int k = 0; k < 2 * C.M; ++k) H.tw_dct[k] = root(k, 2L * C.M, -1);
   H.ring = ring;

@@ -159,6 +159,7 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     if ((e = upload(p, H.k2t_ov, &P.k2t_ov, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.ring, &P.ring, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.tw_col, &P.tw_col, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.tw_dct4, &P.tw_dct4, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2c_mask, &P.k2c_mask, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2c_base, &P.k2c_base, tb)) != cudaSuccess) break;
     const size_t B = (size_t)C.batch;

@@ -38,6 +38,7 @@ struct HostTables {
   std::vector<float2> tw_ring;      // n_ring roots
   std::vector<float2> tw_dct;       // 2M roots
   std::vector<float2> tw_col;       // [Lres][n]: exp(-2 pi i s (y - n/2) / N) (kernels_col.cu)
+  std::vector<float2> tw_dct4;      // [4][n]: exp(-2 pi i s i' / 4n) (kernels_col.cu K4/K4T)
   // K2 forward gather: half-plane nodes sorted by p0
   std::vector<int> k2_colptr;       // [ncols + 1]
   std::vector<int4> k2_nodes;       // (l'*NL + j, q0, alpha bits, beta bits), sorted by p0
@@ -75,6 +76,7 @@ struct DevPlan {
   const float2* tw_ring = nullptr;
   const float2* tw_dct = nullptr;
   const float2* tw_col = nullptr;
+  const float2* tw_dct4 = nullptr;
   const int* k2_colptr = nullptr;
   const int4* k2_nodes = nullptr;
   const int* node_perm = nullptr;
@@ -130,6 +132,9 @@ size_t smem_k2c_adj(const Consts& C);
 cudaError_t configure_col_kernels(const Consts& C);
 cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s);
+bool dct4_ok(const Consts& C);
+size_t smem_k4c(const Consts& C);
+cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s);
 cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
 cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s);
 
