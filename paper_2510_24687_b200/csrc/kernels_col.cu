@@ -508,9 +508,11 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
   __syncthreads();
   stage_b<G, -1>(W, tl);
   __syncthreads();
-  auto X = [&](int u) -> float2 {   // u in (-4n, 4n)
+  auto X = [&](int u) -> float2 {   // u in (-4n, 4n) (|2u| < 2M = 12n: one wrap at most)
     const int v = u & (N4 - 1);
-    const int u1 = ((u % M2) + M2) % M2, u2 = ((2 * u) % M2 + M2) % M2;
+    const int u1 = u < 0 ? u + M2 : u;
+    int u2 = 2 * u;
+    u2 = u2 < 0 ? u2 + M2 : (u2 >= M2 ? u2 - M2 : u2);
     const float2 y0 = sm[G::fq(v)], y1 = sm[N4 + G::fq(v)], y2 = sm[2 * N4 + G::fq(v)];
     return ce::cadd(y0, ce::cadd(cmul(y1, __ldg(&P.tw_dct[u1])), cmul(y2, __ldg(&P.tw_dct[u2]))));
   };
