@@ -90,8 +90,18 @@ def model(info: dict) -> dict:
     return {"bytes": by, "flops": fl, "pair_bytes": pair_bytes}
 
 
-BOUND = {"K1": "hbm", "K2": "alu", "K3": "hbm", "K4": "hbm", "K5": "hbm",
-         "K5T": "hbm", "K4T": "hbm", "K3T": "hbm", "K2T": "alu", "K1T": "hbm"}
+BOUND = {"K1": "hbm", "K2": "alu", "K3": "hbm", "K4": "alu", "K5": "hbm",
+         "K5T": "hbm", "K4T": "alu", "K3T": "hbm", "K2T": "alu", "K1T": "hbm"}
+
+
+def measured_traffic(name: str, stage: str):
+    """DRAM bytes per launch of `stage` from the committed ncu --set full capture
+    (profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return t[name][stage]
+    except Exception:
+        return None
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -304,14 +314,14 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     if BOUND[dom] == "alu":
         ach = mdl["flops"][dom] / dur_s / 1e12
         roof = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
-                "frac": ach / alu_peak, "traffic": None,
+                "frac": ach / alu_peak, "traffic": measured_traffic(name, dom),
                 "kernel": dom, "algorithmic_flops": mdl["flops"][dom],
                 "hbm_achieved_gbs": mdl["bytes"][dom] / dur_s / 1e9,
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md)"}
     else:
         ach = mdl["bytes"][dom] / dur_s / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / pk["hbm_gbs"], "traffic": None, "kernel": dom,
+                "frac": ach / pk["hbm_gbs"], "traffic": measured_traffic(name, dom), "kernel": dom,
                 "algorithmic_bytes": mdl["bytes"][dom], "peak_source": pk_kind}
     eff_hbm = mdl["pair_bytes"] / (ms_per_step * 1e-3) / 1e9     # GB/s, whole batch
     cpu = None
