@@ -20,6 +20,7 @@
 #include "col_engine.cuh"
 #include "tat_internal.h"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace tat {
@@ -46,25 +47,57 @@ using ce::cmul;
 using ce::cmulc;
 using ce::csub;
 
+// ------------------------------------------------------------------ post-twiddle powers b^k
+// FULL: b^1..b^15 in registers (binary splitting).  FACT: b^k = b^(k mod 4) (b^4)^(k div 4) from
+// six registers (one extra multiply for 9 of the 15 k; lower register pressure).
+template <bool FACT>
+struct Pow16 {
+  float2 p[16];
+  __device__ __forceinline__ void init(float2 b) { ce::pow_tree<16>(b, p); }
+  __device__ __forceinline__ float2 mul(float2 v, int k) const { return cmul(v, p[k]); }
+  __device__ __forceinline__ float2 mulc(float2 v, int k) const { return cmulc(v, p[k]); }
+};
+template <>
+struct Pow16<true> {
+  float2 lo[4], hi[4];
+  __device__ __forceinline__ void init(float2 b) {
+    lo[1] = b;
+    lo[2] = cmul(b, b);
+    lo[3] = cmul(lo[2], b);
+    hi[1] = cmul(lo[2], lo[2]);
+    hi[2] = cmul(hi[1], hi[1]);
+    hi[3] = cmul(hi[2], hi[1]);
+  }
+  __device__ __forceinline__ float2 mul(float2 v, int k) const {
+    if (k & 3) v = cmul(v, lo[k & 3]);
+    if (k >> 2) v = cmul(v, hi[k >> 2]);
+    return v;
+  }
+  __device__ __forceinline__ float2 mulc(float2 v, int k) const {
+    if (k & 3) v = cmulc(v, lo[k & 3]);
+    if (k >> 2) v = cmulc(v, hi[k >> 2]);
+    return v;
+  }
+};
+
 // ------------------------------------------------------------------ shared stage code
 // Per-thread twiddles: A[i][r] = tab[s_i][j + J r] (s_i = sg + NG i; for the column transform
 // tab = tw_col, W_N^{s (y - n/2)}), pw[k] = b^k with b = W_n^{j - shift}.
-template <class G>
+template <class G, class PW>
 __device__ __forceinline__ void col_twiddles(const float2* __restrict__ tab, const float2* __restrict__ tw_n,
-                                             int shift, int j, int sg, float2 (&A)[G::NRES][16],
-                                             float2 (&pw)[16]) {
+                                             int shift, int j, int sg, float2 (&A)[G::NRES][16], PW& pw) {
   constexpr int n = G::n;
 #pragma unroll
   for (int i = 0; i < G::NRES; ++i)
 #pragma unroll
     for (int r = 0; r < 16; ++r) A[i][r] = __ldg(&tab[(sg + G::NG * i) * n + j + G::J * r]);
-  ce::pow_tree<16>(__ldg(&tw_n[(j - shift) & (n - 1)]), pw);
+  pw.init(__ldg(&tw_n[(j - shift) & (n - 1)]));
 }
 
 // stage A: samples x[r] = x[j + J r] -> W[(s + L k1, j)] for the thread's residues s
-template <class G>
+template <class G, class PW>
 __device__ __forceinline__ void stage_a_fwd(const float2 (&x)[16], const float2 (&A)[G::NRES][16],
-                                            const float2 (&pw)[16], float2* W, int j, int sg) {
+                                            const PW& pw, float2* W, int j, int sg) {
 #pragma unroll
   for (int i = 0; i < G::NRES; ++i) {
     const int s = sg + G::NG * i;
@@ -73,7 +106,7 @@ __device__ __forceinline__ void stage_a_fwd(const float2 (&x)[16], const float2 
     for (int r = 0; r < 16; ++r) v[r] = cmul(x[r], A[i][r]);
     ce::dftr<16, -1>(v);
 #pragma unroll
-    for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], pw[k1]);
+    for (int k1 = 1; k1 < 16; ++k1) v[k1] = pw.mul(v[k1], k1);
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) W[G::widx(s + G::L * k1, j)] = v[k1];
   }
@@ -91,9 +124,9 @@ __device__ __forceinline__ void stage_b(float2* W, int q0) {
 }
 
 // stage A^H: W -> acc[r] = sum over the thread's residues of the conjugate chain at j + J r
-template <class G>
+template <class G, class PW>
 __device__ __forceinline__ void stage_a_adj(const float2* W, const float2 (&A)[G::NRES][16],
-                                            const float2 (&pw)[16], int j, int sg, float2 (&acc)[16]) {
+                                            const PW& pw, int j, int sg, float2 (&acc)[16]) {
 #pragma unroll
   for (int i = 0; i < G::NRES; ++i) {
     const int s = sg + G::NG * i;
@@ -101,7 +134,7 @@ __device__ __forceinline__ void stage_a_adj(const float2* W, const float2 (&A)[G
 #pragma unroll
     for (int k1 = 0; k1 < 16; ++k1) v[k1] = W[G::widx(s + G::L * k1, j)];
 #pragma unroll
-    for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmulc(v[k1], pw[k1]);
+    for (int k1 = 1; k1 < 16; ++k1) v[k1] = pw.mulc(v[k1], k1);
     ce::dftr<16, 1>(v);
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
@@ -130,7 +163,7 @@ __device__ __forceinline__ float2 residue_sum(const float2* W, int y) {
 }
 
 // ================================================================== forward
-template <int n, int MINB, bool HOIST, int SKIP = 0>
+template <int n, int MINB, bool FACT, int SKIP = 0>
 __global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
   using G = ColGeo<n>;
   constexpr int R = G::R, J = G::J, L = G::L, NG = G::NG, NRES = G::NRES;
@@ -147,13 +180,8 @@ __global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
   float2* xbuf = sm + 2 * G::Q0 * J;                          // 2 x n, TMA destination
   uint64_t* bar = reinterpret_cast<uint64_t*>(xbuf + 2 * n);
   float2 A[NRES][R];
-#pragma unroll
-  for (int i = 0; i < NRES; ++i)
-#pragma unroll
-    for (int r = 0; r < R; ++r) A[i][r] = __ldg(&P.tw_col[(sg + NG * i) * n + j + J * r]);
-  const float2 bpw = __ldg(&P.tw_n[(j - n / 2) & (n - 1)]);
-  float2 pw[R];
-  if constexpr (HOIST) ce::pow_tree<R>(bpw, pw);
+  Pow16<FACT> pw;
+  col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float2* S1 = P.S1 + (size_t)b * C.ncols * n;
   float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
   if (t == 0) {
@@ -183,29 +211,10 @@ __global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
       float2 x[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r] = xs[j + J * r];
-#pragma unroll
-      for (int i = 0; i < NRES; ++i) {
-        const int s = sg + NG * i;
-        float2 v[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = cmul(x[r], A[i][r]);
-        ce::dftr<R, -1>(v);
-        if constexpr (!HOIST) ce::pow_tree<R>(bpw, pw);
-#pragma unroll
-        for (int k1 = 1; k1 < R; ++k1) v[k1] = cmul(v[k1], pw[k1]);
-#pragma unroll
-        for (int k1 = 0; k1 < R; ++k1) Fcur[G::widx(s + L * k1, j)] = v[k1];
-      }
+      stage_a_fwd<G>(x, A, pw, Fcur, j, sg);
     }
     __syncthreads();
-    if (!(SKIP & 2)) {   // stage B (in place)
-      float2 u[J];
-#pragma unroll
-      for (int c = 0; c < J; ++c) u[c] = Fcur[G::widx(t, c)];
-      ce::dftr<J, -1>(u);
-#pragma unroll
-      for (int c = 0; c < J; ++c) Fcur[G::widx(t, c)] = u[c];
-    }
+    if (!(SKIP & 2)) stage_b<G, -1>(Fcur, t);   // stage B (in place)
     __syncthreads();
     if (!(SKIP & 4) && p > P0) {   // bilinear gather of the nodes with p0 = p - 1 (Alg. 1 step 3)
       int e = e0 + t;
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
 // Column p: the target values of column p (Rc, ordered by (q0, q1), moved by one bulk copy per
 // column into a double buffer) -> stage B^H (thread q0, only the present q1 are read) ->
 // stage A^H (thread (j, s)) -> residue-group partial sums -> S~1[b][p][y].
-template <int n, int MINB>
+template <int n, int MINB, bool FACT>
 __global__ void __launch_bounds__(128, MINB) k2c_adj(DevPlan P) {
   using G = ColGeo<n>;
   constexpr int R = G::R, J = G::J, L = G::L, NG = G::NG, NRES = G::NRES, Q0 = G::Q0;
@@ -256,12 +265,8 @@ __global__ void __launch_bounds__(128, MINB) k2c_adj(DevPlan P) {
   float2* rbuf = sm + Q0 * J;
   uint64_t* bar = reinterpret_cast<uint64_t*>(rbuf + 2 * RB);
   float2 A[NRES][R];
-#pragma unroll
-  for (int i = 0; i < NRES; ++i)
-#pragma unroll
-    for (int r = 0; r < R; ++r) A[i][r] = __ldg(&P.tw_col[(sg + NG * i) * n + j + J * r]);
-  float2 pw[R];
-  ce::pow_tree<R>(__ldg(&P.tw_n[(j - n / 2) & (n - 1)]), pw);
+  Pow16<FACT> pw;
+  col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float2* Rc = P.Rc + (size_t)b * C.ntpad;
   float2* out = P.S1 + (size_t)b * C.ncols * n;
   auto issue = [&](int p, int slot) {   // thread 0: bulk copy of column p's targets
@@ -310,33 +315,9 @@ __global__ void __launch_bounds__(128, MINB) k2c_adj(DevPlan P) {
     }
     __syncthreads();
     float2 acc[R];
-    {   // stage A^H
-#pragma unroll
-      for (int i = 0; i < NRES; ++i) {
-        const int s = sg + NG * i;
-        float2 v[R];
-#pragma unroll
-        for (int k1 = 0; k1 < R; ++k1) v[k1] = Wb[G::widx(s + L * k1, j)];
-#pragma unroll
-        for (int k1 = 1; k1 < R; ++k1) v[k1] = cmulc(v[k1], pw[k1]);
-        ce::dftr<R, 1>(v);
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const float2 w = cmulc(v[r], A[i][r]);
-          acc[r] = (i == 0) ? w : ce::cadd(acc[r], w);
-        }
-      }
-    }
-    __syncthreads();   // all stage-A^H reads of Wb done
-#pragma unroll
-    for (int r = 0; r < R; ++r) Wb[sg * n + j + J * r] = acc[r];
-    __syncthreads();
-    for (int y = t; y < n; y += G::T) {
-      float2 s = Wb[y];
-#pragma unroll
-      for (int g = 1; g < NG; ++g) s = ce::cadd(s, Wb[g * n + y]);
-      out[(size_t)p * n + y] = s;
-    }
+    stage_a_adj<G>(Wb, A, pw, j, sg, acc);
+    residue_reduce<G>(Wb, acc, j, sg);
+    for (int y = t; y < n; y += G::T) out[(size_t)p * n + y] = residue_sum<G>(Wb, y);
     __syncthreads();   // Wb free; rbuf[slot] consumed
     m = m_next;
     base = base_next;
@@ -361,7 +342,8 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
   float2* W0 = sm;
   float2* W1 = sm + G::Q0 * G::J;
   float2* stg = sm + 2 * G::Q0 * G::J;   // 2 tiles [kK1BoxP][4]
-  float2 A[G::NRES][16], pw[16];
+  float2 A[G::NRES][16];
+  Pow16<false> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float* r0 = f + ((size_t)b * n + y0) * n;
 #pragma unroll 1
@@ -428,7 +410,8 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
       ac::tma_load_3d(stg + c * kK1BoxP * 4, &tm, y0, c * kK1BoxP, b, &bar[c]);
     }
   }
-  float2 A[G::NRES][16], pw[16];
+  float2 A[G::NRES][16];
+  Pow16<false> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   __syncthreads();
   for (int c = 0; c < nch; ++c) {
@@ -484,6 +467,8 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
 //   K4  (ADJ = false): c_j = H[k][j] (S3 row, j <= J), out for u = m + 1, m < n_t -> S4 row
 //   K4T (ADJ = true) : c_i = G~[k][i - 1] (S4 row, 1 <= i <= n_t), out for u = j <= J, then
 //                      x (-i)^k omega m'[k][j] -> S3 row
+// Persistent CTAs loop over the rows (b, k); the next row is prefetched into shared memory by a
+// 1-D bulk copy while the current one is transformed, and the per-thread twiddles are loaded once.
 template <int n, bool ADJ>
 __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
   using G = ColGeo<n, 4>;
@@ -491,56 +476,101 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
   extern __shared__ __align__(128) float2 sm[];
   const Consts& C = P.C;
   const int t = threadIdx.x, e = t / G::T, tl = t % G::T, j = tl % G::J, sg = tl / G::J;
-  const int b = blockIdx.y, k = blockIdx.x;
   const int M2 = 2 * C.M, NL = C.NL, n_t = C.n_t;
-  const float2* in = ADJ ? P.S4 + ((size_t)b * C.Kp + k) * n_t : P.S3 + ((size_t)b * C.Kp + k) * NL;
-  const int cnt = ADJ ? n_t : NL;
-  float2 x[16];
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const int i = 3 * (j + G::J * r) + e, src = ADJ ? i - 1 : i;
-    x[r] = (src >= 0 && src < cnt) ? __ldg(&in[src]) : make_float2(0.f, 0.f);
-  }
-  float2 A[G::NRES][16], pw[16];
-  col_twiddles<G>(P.tw_dct4, P.tw_n, 0, j, sg, A, pw);
+  const int cnt = ADJ ? n_t : NL;                 // input entries per row
+  const int IB = (cnt + 3) & ~1;                  // slot size (entries; alignment slack)
+  const int rows = C.Kp * C.batch;
+  const float2* in_all = ADJ ? P.S4 : P.S3;
   float2* W = sm + e * N4;
-  stage_a_fwd<G>(x, A, pw, W, j, sg);
-  __syncthreads();
-  stage_b<G, -1>(W, tl);
-  __syncthreads();
-  auto X = [&](int u) -> float2 {   // u in (-4n, 4n) (|2u| < 2M = 12n: one wrap at most)
-    const int v = u & (N4 - 1);
-    const int u1 = u < 0 ? u + M2 : u;
-    int u2 = 2 * u;
-    u2 = u2 < 0 ? u2 + M2 : (u2 >= M2 ? u2 - M2 : u2);
-    const float2 y0 = sm[G::fq(v)], y1 = sm[N4 + G::fq(v)], y2 = sm[2 * N4 + G::fq(v)];
-    return ce::cadd(y0, ce::cadd(cmul(y1, __ldg(&P.tw_dct[u1])), cmul(y2, __ldg(&P.tw_dct[u2]))));
+  float2* ibuf = sm + 3 * N4;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ibuf + 2 * IB);
+  auto issue = [&](int r, int slot) {   // thread 0: row r -> ibuf[slot] (16-B aligned range)
+    const long s0 = ((long)r * cnt) & ~1L, s1 = ((long)r * cnt + cnt + 1) & ~1L;
+    ac::mbar_expect_tx(&bar[slot], (uint32_t)(s1 - s0) * 8);
+    ac::bulk_g2s(ibuf + slot * IB, in_all + s0, (uint32_t)(s1 - s0) * 8, &bar[slot]);
   };
-  if (!ADJ) {
-    const float2 hJ = (NL == 3 * n + 1) ? __ldg(&in[3 * n]) : make_float2(0.f, 0.f);
-    float2* out = P.S4 + ((size_t)b * C.Kp + k) * n_t;
-    for (int m = t; m < n_t; m += blockDim.x) {
-      const int u = m + 1;
-      float2 g = fe::cscale(ce::cadd(X(u), X(-u)), 0.5f);
-      if ((u & 3) == 0) g = ce::cadd(g, hJ);
-      else if ((u & 3) == 2) g = csub(g, hJ);
-      out[m] = g;
+  if (t == 0) {
+    ac::mbar_init(&bar[0], 1);
+    ac::mbar_init(&bar[1], 1);
+    ac::fence_mbar_init();
+    if ((int)blockIdx.x < rows) issue(blockIdx.x, 0);
+  }
+  float2 A[G::NRES][16];
+  Pow16<false> pw;
+  col_twiddles<G>(P.tw_dct4, P.tw_n, 0, j, sg, A, pw);
+  __syncthreads();
+  int it = 0;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x, ++it) {
+    const int slot = it & 1;
+    if (t == 0 && row + (int)gridDim.x < rows) {
+      ac::fence_proxy_async();
+      issue(row + gridDim.x, slot ^ 1);
     }
-  } else {
-    float2* out = P.S3 + ((size_t)b * C.Kp + k) * NL;
+    const int b = row / C.Kp, k = row - b * C.Kp;
+    ac::mbar_wait(&bar[slot], (it >> 1) & 1);
+    const float2* in = ibuf + slot * IB + (int)(((long)row * cnt) & 1L);
+    float2 x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int i = 3 * (j + G::J * r) + e, src = ADJ ? i - 1 : i;
+      x[r] = (src >= 0 && src < cnt) ? in[src] : make_float2(0.f, 0.f);
+    }
+    stage_a_fwd<G>(x, A, pw, W, j, sg);
+    __syncthreads();
+    stage_b<G, -1>(W, tl);
+    __syncthreads();
+    // S(u) = X(u) + X(-u) = sum_e [W^{eu} Y_e(u) + conj(W^{eu}) Y_e(-u)], W = W_2M, 0 <= u < 4n;
+    // outputs in groups of 4 per thread with all twiddle loads issued first
+    auto Ssum = [&](int u, float2 w1, float2 w2) -> float2 {
+      const int vp = G::fq(u & (N4 - 1)), vm = G::fq((N4 - u) & (N4 - 1));
+      const float2 a = ce::cadd(sm[vp], sm[vm]);
+      const float2 c1 = ce::cadd(cmul(sm[N4 + vp], w1), cmulc(sm[N4 + vm], w1));
+      const float2 c2 = ce::cadd(cmul(sm[2 * N4 + vp], w2), cmulc(sm[2 * N4 + vm], w2));
+      return ce::cadd(a, ce::cadd(c1, c2));
+    };
+    constexpr int U = 4;
+    const int nout = ADJ ? NL : n_t;
+    const float2 hJ = (!ADJ && NL == 3 * n + 1) ? in[3 * n] : make_float2(0.f, 0.f);
     const float om = (float)C.omega;
-    for (int jj = t; jj < NL; jj += blockDim.x) {
-      const float2 y = fe::cscale(ce::cadd(X(jj), X(-jj)), 0.5f);
-      const float2 z = fe::cscale(y, om * __ldg(&P.mult[(size_t)k * NL + jj]));
-      float2 o;
-      switch ((-k) & 3) {   // (-i)^k
-        case 0: o = z; break;
-        case 1: o = make_float2(-z.y, z.x); break;
-        case 2: o = make_float2(-z.x, -z.y); break;
-        default: o = make_float2(z.y, -z.x); break;
+    float2* out = ADJ ? P.S3 + (size_t)row * NL : P.S4 + (size_t)row * n_t;
+    for (int o0 = t; o0 < nout; o0 += U * (int)blockDim.x) {
+      float2 w1[U], w2[U];
+      float ml[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int o = o0 + q * blockDim.x;
+        const int u = ADJ ? o : o + 1;
+        const int u2 = 2 * u >= M2 ? 2 * u - M2 : 2 * u;
+        w1[q] = o < nout ? __ldg(&P.tw_dct[u]) : make_float2(0.f, 0.f);
+        w2[q] = o < nout ? __ldg(&P.tw_dct[u2]) : make_float2(0.f, 0.f);
+        ml[q] = (ADJ && o < nout) ? __ldg(&P.mult[(size_t)k * NL + o]) : 0.f;
       }
-      out[jj] = o;
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int o = o0 + q * blockDim.x;
+        if (o >= nout) break;
+        const int u = ADJ ? o : o + 1;
+        const float2 y = fe::cscale(Ssum(u, w1[q], w2[q]), 0.5f);
+        if (!ADJ) {
+          float2 g = y;
+          if ((u & 3) == 0) g = ce::cadd(g, hJ);
+          else if ((u & 3) == 2) g = csub(g, hJ);
+          out[o] = g;
+        } else {
+          const float2 z = fe::cscale(y, om * ml[q]);
+          float2 r;
+          switch ((-k) & 3) {   // (-i)^k
+            case 0: r = z; break;
+            case 1: r = make_float2(-z.y, z.x); break;
+            case 2: r = make_float2(-z.x, -z.y); break;
+            default: r = make_float2(z.y, -z.x); break;
+          }
+          out[o] = r;
+        }
+      }
     }
+    (void)b;
+    __syncthreads();   // W and ibuf[slot] free
   }
 }
 
@@ -549,11 +579,15 @@ bool dct4_ok(const Consts& C) {
   return (C.n == 256 || C.n == 512) && 2L * C.M == 12L * C.n && C.J <= 3 * C.n &&
          C.n_t <= 3 * C.n - 1;
 }
-size_t smem_k4c(const Consts& C) { return (size_t)3 * 4 * C.n * 8; }
+size_t smem_k4c(const Consts& C) {
+  const int cnt = std::max(C.NL, C.n_t);
+  return (size_t)3 * 4 * C.n * 8 + (size_t)2 * ((cnt + 3) & ~1) * 8 + 64;
+}
 
 cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s) {
   const Consts& C = P.C;
-  const dim3 grid(C.Kp, C.batch);
+  const int rows = C.Kp * C.batch;
+  const dim3 grid(std::min(rows, 2 * 148));
   const size_t sm = smem_k4c(C);
   if (C.n == 512) {
     if (adj) k4c_dct<512, true><<<grid, 192, sm, s>>>(P);
@@ -588,15 +622,11 @@ static cudaError_t cfg_col() {
   cudaError_t e = cudaSuccess;
   const int lim = 227 * 1024;
 #define SETC(k) if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  SETC((k2c_fwd<n, 3, true>));
-  SETC((k2c_fwd<n, 2, true>));
   SETC((k2c_fwd<n, 3, false>));
-  SETC((k2c_fwd<n, 3, true, 1>));
-  SETC((k2c_fwd<n, 3, true, 2>));
-  SETC((k2c_fwd<n, 3, true, 4>));
-  SETC((k2c_fwd<n, 3, true, 7>));
-  SETC((k2c_adj<n, 3>));
-  SETC((k2c_adj<n, 2>));
+  SETC((k2c_fwd<n, 3, true>));
+  SETC((k2c_fwd<n, 2, false>));
+  SETC((k2c_adj<n, 3, false>));
+  SETC((k2c_adj<n, 3, true>));
   SETC((k1c_fwd<n>));
   SETC((k1c_adj<n>));
   SETC((k4c_dct<n, false>));
@@ -613,20 +643,16 @@ cudaError_t configure_col_kernels(const Consts& C) {
 template <int n>
 static void launch_fwd_n(const DevPlan& P, dim3 grid, size_t sm, cudaStream_t s) {
   switch (k2c_variant()) {
-    case 1: k2c_fwd<n, 2, true><<<grid, 128, sm, s>>>(P); break;
-    case 2: k2c_fwd<n, 3, false><<<grid, 128, sm, s>>>(P); break;
-    case 11: k2c_fwd<n, 3, true, 1><<<grid, 128, sm, s>>>(P); break;
-    case 12: k2c_fwd<n, 3, true, 2><<<grid, 128, sm, s>>>(P); break;
-    case 14: k2c_fwd<n, 3, true, 4><<<grid, 128, sm, s>>>(P); break;
-    case 17: k2c_fwd<n, 3, true, 7><<<grid, 128, sm, s>>>(P); break;
+    case 1: k2c_fwd<n, 3, false><<<grid, 128, sm, s>>>(P); break;
+    case 2: k2c_fwd<n, 2, false><<<grid, 128, sm, s>>>(P); break;
     default: k2c_fwd<n, 3, true><<<grid, 128, sm, s>>>(P); break;
   }
 }
 template <int n>
 static void launch_adj_n(const DevPlan& P, dim3 grid, size_t sm, cudaStream_t s) {
   switch (k2c_variant()) {
-    case 1: k2c_adj<n, 2><<<grid, 128, sm, s>>>(P); break;
-    default: k2c_adj<n, 3><<<grid, 128, sm, s>>>(P); break;
+    case 1: k2c_adj<n, 3, true><<<grid, 128, sm, s>>>(P); break;
+    default: k2c_adj<n, 3, false><<<grid, 128, sm, s>>>(P); break;
   }
 }
 

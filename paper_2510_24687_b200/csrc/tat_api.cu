@@ -168,9 +168,9 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     P.S1 = (float2*)d;
     if ((e = alloc_ws(p, B * C.half * C.NL * sizeof(float2), &d)) != cudaSuccess) break;
     P.S2 = (float2*)d;
-    if ((e = alloc_ws(p, B * C.Kp * C.NL * sizeof(float2), &d)) != cudaSuccess) break;
+    if ((e = alloc_ws(p, B * C.Kp * C.NL * sizeof(float2) + 16, &d)) != cudaSuccess) break;
     P.S3 = (float2*)d;
-    if ((e = alloc_ws(p, B * C.Kp * C.n_t * sizeof(float2), &d)) != cudaSuccess) break;
+    if ((e = alloc_ws(p, B * C.Kp * C.n_t * sizeof(float2) + 16, &d)) != cudaSuccess) break;
     P.S4 = (float2*)d;
     P.C.ntargets = (int)H.k2t_tq.size();
     P.C.ntpad = (P.C.ntargets + 1) & ~1;
