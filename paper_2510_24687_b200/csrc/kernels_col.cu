@@ -21,13 +21,16 @@
 #include "tat_internal.h"
 
 #include <algorithm>
-#include <cstdlib>
 
 namespace tat {
 
 namespace {
 
 constexpr int kStripC = 16;   // columns per CTA (k2c_fwd recomputes one halo column)
+#ifndef TAT_FACT_POW
+#define TAT_FACT_POW 1
+#endif
+constexpr bool kFactPow = TAT_FACT_POW;   // K1/K1T/K4/K4T post-twiddle powers (Pow16)
 
 template <int n_, int L_ = 8>
 struct ColGeo {
@@ -163,10 +166,10 @@ __device__ __forceinline__ float2 residue_sum(const float2* W, int y) {
 }
 
 // ================================================================== forward
-template <int n, int MINB, bool FACT, int SKIP = 0>
-__global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
+template <int n>
+__global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
   using G = ColGeo<n>;
-  constexpr int R = G::R, J = G::J, L = G::L, NG = G::NG, NRES = G::NRES;
+  constexpr int R = G::R, J = G::J, NRES = G::NRES;
   extern __shared__ __align__(128) float2 sm[];
   const Consts& C = P.C;
   const int N1 = C.N - 1;
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
   float2* xbuf = sm + 2 * G::Q0 * J;                          // 2 x n, TMA destination
   uint64_t* bar = reinterpret_cast<uint64_t*>(xbuf + 2 * n);
   float2 A[NRES][R];
-  Pow16<FACT> pw;
+  Pow16<kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float2* S1 = P.S1 + (size_t)b * C.ncols * n;
   float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
     int4 nd0 = make_int4(0, 0, 0, 0);
     if (e0 + t < e1) nd0 = __ldg(&P.k2_nodes[e0 + t]);
     ac::mbar_wait(&bar[slot], (it >> 1) & 1);
-    if (!(SKIP & 1)) {   // stage A
+    {   // stage A
       const float2* xs = xbuf + slot * n;
       float2 x[R];
 #pragma unroll
@@ -214,9 +217,9 @@ __global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
       stage_a_fwd<G>(x, A, pw, Fcur, j, sg);
     }
     __syncthreads();
-    if (!(SKIP & 2)) stage_b<G, -1>(Fcur, t);   // stage B (in place)
+    stage_b<G, -1>(Fcur, t);   // stage B (in place)
     __syncthreads();
-    if (!(SKIP & 4) && p > P0) {   // bilinear gather of the nodes with p0 = p - 1 (Alg. 1 step 3)
+    if (p > P0) {   // bilinear gather of the nodes with p0 = p - 1 (Alg. 1 step 3)
       int e = e0 + t;
       int4 nd = nd0;
       while (e < e1) {
@@ -250,10 +253,10 @@ __global__ void __launch_bounds__(128, MINB) k2c_fwd(DevPlan P) {
 // Column p: the target values of column p (Rc, ordered by (q0, q1), moved by one bulk copy per
 // column into a double buffer) -> stage B^H (thread q0, only the present q1 are read) ->
 // stage A^H (thread (j, s)) -> residue-group partial sums -> S~1[b][p][y].
-template <int n, int MINB, bool FACT>
-__global__ void __launch_bounds__(128, MINB) k2c_adj(DevPlan P) {
+template <int n>
+__global__ void __launch_bounds__(128, 3) k2c_adj(DevPlan P) {
   using G = ColGeo<n>;
-  constexpr int R = G::R, J = G::J, L = G::L, NG = G::NG, NRES = G::NRES, Q0 = G::Q0;
+  constexpr int R = G::R, J = G::J, NRES = G::NRES, Q0 = G::Q0;
   extern __shared__ __align__(128) float2 sm[];
   const Consts& C = P.C;
   const int t = threadIdx.x, j = t % J, sg = t / J;
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(128, MINB) k2c_adj(DevPlan P) {
   float2* rbuf = sm + Q0 * J;
   uint64_t* bar = reinterpret_cast<uint64_t*>(rbuf + 2 * RB);
   float2 A[NRES][R];
-  Pow16<FACT> pw;
+  Pow16<kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float2* Rc = P.Rc + (size_t)b * C.ntpad;
   float2* out = P.S1 + (size_t)b * C.ncols * n;
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
   float2* W1 = sm + G::Q0 * G::J;
   float2* stg = sm + 2 * G::Q0 * G::J;   // 2 tiles [kK1BoxP][4]
   float2 A[G::NRES][16];
-  Pow16<false> pw;
+  Pow16<kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float* r0 = f + ((size_t)b * n + y0) * n;
 #pragma unroll 1
@@ -411,7 +414,7 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
     }
   }
   float2 A[G::NRES][16];
-  Pow16<false> pw;
+  Pow16<kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   __syncthreads();
   for (int c = 0; c < nch; ++c) {
@@ -496,7 +499,7 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
     if ((int)blockIdx.x < rows) issue(blockIdx.x, 0);
   }
   float2 A[G::NRES][16];
-  Pow16<false> pw;
+  Pow16<kFactPow> pw;
   col_twiddles<G>(P.tw_dct4, P.tw_n, 0, j, sg, A, pw);
   __syncthreads();
   int it = 0;
@@ -612,21 +615,13 @@ size_t smem_k2c_adj(const Consts& C) {
 
 size_t smem_k1c(const Consts& C) { return (size_t)2 * 128 * (C.n / 16) * 8 + 2 * kK1BoxP * 32 + 64; }
 
-static int k2c_variant() {   // experiment selector (TAT_K2C_VAR), 0 = default
-  const char* v = getenv("TAT_K2C_VAR");
-  return v ? atoi(v) : 0;
-}
-
 template <int n>
 static cudaError_t cfg_col() {
   cudaError_t e = cudaSuccess;
   const int lim = 227 * 1024;
 #define SETC(k) if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  SETC((k2c_fwd<n, 3, false>));
-  SETC((k2c_fwd<n, 3, true>));
-  SETC((k2c_fwd<n, 2, false>));
-  SETC((k2c_adj<n, 3, false>));
-  SETC((k2c_adj<n, 3, true>));
+  SETC((k2c_fwd<n>));
+  SETC((k2c_adj<n>));
   SETC((k1c_fwd<n>));
   SETC((k1c_adj<n>));
   SETC((k4c_dct<n, false>));
@@ -640,35 +635,19 @@ cudaError_t configure_col_kernels(const Consts& C) {
   return C.n == 512 ? cfg_col<512>() : cfg_col<256>();
 }
 
-template <int n>
-static void launch_fwd_n(const DevPlan& P, dim3 grid, size_t sm, cudaStream_t s) {
-  switch (k2c_variant()) {
-    case 1: k2c_fwd<n, 3, false><<<grid, 128, sm, s>>>(P); break;
-    case 2: k2c_fwd<n, 2, false><<<grid, 128, sm, s>>>(P); break;
-    default: k2c_fwd<n, 3, true><<<grid, 128, sm, s>>>(P); break;
-  }
-}
-template <int n>
-static void launch_adj_n(const DevPlan& P, dim3 grid, size_t sm, cudaStream_t s) {
-  switch (k2c_variant()) {
-    case 1: k2c_adj<n, 3, true><<<grid, 128, sm, s>>>(P); break;
-    default: k2c_adj<n, 3, false><<<grid, 128, sm, s>>>(P); break;
-  }
-}
-
 cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
-  if (C.n == 512) launch_fwd_n<512>(P, grid, smem_k2c_fwd(C), s);
-  else launch_fwd_n<256>(P, grid, smem_k2c_fwd(C), s);
+  if (C.n == 512) k2c_fwd<512><<<grid, 128, smem_k2c_fwd(C), s>>>(P);
+  else k2c_fwd<256><<<grid, 128, smem_k2c_fwd(C), s>>>(P);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
-  if (C.n == 512) launch_adj_n<512>(P, grid, smem_k2c_adj(C), s);
-  else launch_adj_n<256>(P, grid, smem_k2c_adj(C), s);
+  if (C.n == 512) k2c_adj<512><<<grid, 128, smem_k2c_adj(C), s>>>(P);
+  else k2c_adj<256><<<grid, 128, smem_k2c_adj(C), s>>>(P);
   return cudaGetLastError();
 }
 
