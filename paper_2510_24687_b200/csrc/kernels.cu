@@ -119,7 +119,7 @@ __global__ void k3_angular_mult(DevPlan P) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
   const int nphi = C.n_ring, half = C.half, NL = C.NL, JT = tile_ring(nphi);
-  const int b = blockIdx.y, j0 = blockIdx.x * JT;
+  const int b = C.b0 + blockIdx.y, j0 = blockIdx.x * JT;
   const int jt = min(JT, NL - j0);
   float2* A = sm;
   float2* Bf = sm + (size_t)JT * nphi;
@@ -148,7 +148,7 @@ __global__ void k4_dct(DevPlan P) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
   const int M2 = 2 * C.M, NL = C.NL;
-  const int b = blockIdx.y, k = blockIdx.x;
+  const int b = C.b0 + blockIdx.y, k = blockIdx.x;
   float2* A = sm;
   float2* Bf = sm + M2;
   const float2* H = P.S3 + ((size_t)b * C.Kp + k) * NL;
@@ -165,7 +165,7 @@ __global__ void k5_synth_restrict(DevPlan P, float* __restrict__ g) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
   const int nphi = C.n_ring, K = C.K, TT = tile_ring(nphi);
-  const int b = blockIdx.y, t0 = blockIdx.x * TT, tt_n = min(TT, C.n_t - t0);
+  const int b = C.b0 + blockIdx.y, t0 = blockIdx.x * TT, tt_n = min(TT, C.n_t - t0);
   float2* A = sm;
   float2* Bf = sm + (size_t)TT * nphi;
   const float2* S4 = P.S4 + (size_t)b * C.Kp * C.n_t;
@@ -189,7 +189,7 @@ __global__ void k5t_analysis(DevPlan P, const float* __restrict__ g) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
   const int nphi = C.n_ring, TT = tile_ring(nphi);
-  const int b = blockIdx.y, t0 = blockIdx.x * TT, tt_n = min(TT, C.n_t - t0);
+  const int b = C.b0 + blockIdx.y, t0 = blockIdx.x * TT, tt_n = min(TT, C.n_t - t0);
   float2* A = sm;
   float2* Bf = sm + (size_t)TT * nphi;
   for (int idx = threadIdx.x; idx < TT * nphi; idx += blockDim.x) A[idx] = make_float2(0.f, 0.f);
@@ -212,7 +212,7 @@ __global__ void k4t_dct(DevPlan P) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
   const int M2 = 2 * C.M, NL = C.NL;
-  const int b = blockIdx.y, k = blockIdx.x;
+  const int b = C.b0 + blockIdx.y, k = blockIdx.x;
   float2* A = sm;
   float2* Bf = sm + M2;
   const float2* G = P.S4 + ((size_t)b * C.Kp + k) * C.n_t;
@@ -235,7 +235,7 @@ __global__ void k3t_angular(DevPlan P) {
   extern __shared__ float2 sm[];
   const Consts& C = P.C;
   const int nphi = C.n_ring, half = C.half, NL = C.NL, K = C.K, JT = tile_ring(nphi);
-  const int b = blockIdx.y, j0 = blockIdx.x * JT, jt = min(JT, NL - j0);
+  const int b = C.b0 + blockIdx.y, j0 = blockIdx.x * JT, jt = min(JT, NL - j0);
   float2* A = sm;
   float2* Bf = sm + (size_t)JT * nphi;
   const float2* S3 = P.S3 + (size_t)b * C.Kp * NL;

@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
   const Consts& C = P.C;
   const int N1 = C.N - 1;
   const int t = threadIdx.x, j = t % J, sg = t / J;
-  const int b = blockIdx.y;
+  const int b = C.b0 + blockIdx.y;
   const int P0 = blockIdx.x * kStripC;
   const int Pend = min(P0 + kStripC, C.ncols);
   const int plast = min(Pend, C.ncols - 1);
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(128, 3) k2c_adj(DevPlan P) {
   extern __shared__ __align__(128) float2 sm[];
   const Consts& C = P.C;
   const int t = threadIdx.x, j = t % J, sg = t / J;
-  const int b = blockIdx.y;
+  const int b = C.b0 + blockIdx.y;
   const int P0 = blockIdx.x * kStripC;
   const int Pend = min(P0 + kStripC, C.ncols);
   const int RB = C.k2c_rbuf;                                  // entries per target buffer
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
   extern __shared__ __align__(128) float2 sm[];
   const Consts& C = P.C;
   const int t = threadIdx.x, j = t % G::J, sg = t / G::J;
-  const int b = blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
+  const int b = C.b0 + blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
   float2* W0 = sm;
   float2* W1 = sm + G::Q0 * G::J;
   float2* stg = sm + 2 * G::Q0 * G::J;   // 2 tiles [kK1BoxP][4]
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
   extern __shared__ __align__(128) float2 sm[];
   const Consts& C = P.C;
   const int t = threadIdx.x, j = t % G::J, sg = t / G::J;
-  const int b = blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
+  const int b = C.b0 + blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
   float2* W0 = sm;
   float2* W1 = sm + G::Q0 * G::J;
   float2* stg = sm + 2 * G::Q0 * G::J;
@@ -487,8 +487,9 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
   float2* W = sm + e * N4;
   float2* ibuf = sm + 3 * N4;
   uint64_t* bar = reinterpret_cast<uint64_t*>(ibuf + 2 * IB);
+  const long rbase = (long)C.b0 * C.Kp;   // global row of local row 0
   auto issue = [&](int r, int slot) {   // thread 0: row r -> ibuf[slot] (16-B aligned range)
-    const long s0 = ((long)r * cnt) & ~1L, s1 = ((long)r * cnt + cnt + 1) & ~1L;
+    const long s0 = ((rbase + r) * cnt) & ~1L, s1 = ((rbase + r) * cnt + cnt + 1) & ~1L;
     ac::mbar_expect_tx(&bar[slot], (uint32_t)(s1 - s0) * 8);
     ac::bulk_g2s(ibuf + slot * IB, in_all + s0, (uint32_t)(s1 - s0) * 8, &bar[slot]);
   };
@@ -509,9 +510,9 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
       ac::fence_proxy_async();
       issue(row + gridDim.x, slot ^ 1);
     }
-    const int b = row / C.Kp, k = row - b * C.Kp;
+    const int k = row % C.Kp;
     ac::mbar_wait(&bar[slot], (it >> 1) & 1);
-    const float2* in = ibuf + slot * IB + (int)(((long)row * cnt) & 1L);
+    const float2* in = ibuf + slot * IB + (int)(((rbase + row) * cnt) & 1L);
     float2 x[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
@@ -535,7 +536,7 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
     const int nout = ADJ ? NL : n_t;
     const float2 hJ = (!ADJ && NL == 3 * n + 1) ? in[3 * n] : make_float2(0.f, 0.f);
     const float om = (float)C.omega;
-    float2* out = ADJ ? P.S3 + (size_t)row * NL : P.S4 + (size_t)row * n_t;
+    float2* out = ADJ ? P.S3 + (size_t)(rbase + row) * NL : P.S4 + (size_t)(rbase + row) * n_t;
     for (int o0 = t; o0 < nout; o0 += U * (int)blockDim.x) {
       float2 w1[U], w2[U];
       float ml[U];
@@ -572,7 +573,6 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
         }
       }
     }
-    (void)b;
     __syncthreads();   // W and ibuf[slot] free
   }
 }

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(512) k4_dct_fast(DevPlan P, int r) {
   constexpr int PP = Plan<nf>::P;
   const Consts& C = P.C;
   const int M2 = 2 * C.M, NL = C.NL, n_t = C.n_t;
-  const int b = blockIdx.y, k = blockIdx.x;
+  const int b = C.b0 + blockIdx.y, k = blockIdx.x;
   const int j = threadIdx.x;                 // butterfly index, blockDim.x == nf / 8
   const float2* in = ADJ ? P.S4 + ((size_t)b * C.Kp + k) * n_t : P.S3 + ((size_t)b * C.Kp + k) * NL;
   const int lo = ADJ ? 1 : 0;                // input index of in[0]

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(1024) k2_fwd(DevPlan P) {
   constexpr int rs = rstride(n);
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs, N1 = C.N - 1;
-  const int b = blockIdx.y;
+  const int b = C.b0 + blockIdx.y;
   const int P0 = blockIdx.x * kStrip;
   const int Pend = min(P0 + kStrip, C.ncols);
   const int plast = min(Pend, C.ncols - 1);
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const __grid_constant_
   constexpr int rs = rstride(n);
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs, N = C.N;
-  const int b = blockIdx.y, y0 = 4 * blockIdx.x;
+  const int b = C.b0 + blockIdx.y, y0 = 4 * blockIdx.x;
   const int g = threadIdx.x / (n / 8), j = threadIdx.x & (n / 8 - 1);
   const int so = g * rs;
   float2 pre[8];
@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const __grid_constant_
 // One CTA per (column p, image): the targets of column p only reference nodes with
 // p0 in {p-1, p}, a contiguous range of the (p0-sorted) adjoint S2 that is staged in shared
 // memory (coalesced loads, issued together with the coalesced 16-byte target records).
-constexpr int kSumKT = 2;   // target records per thread loaded before the window barrier
+constexpr int kSumKT = 4;   // target records per thread loaded before the window barrier
+constexpr int kSumThreads = 128;
 
 __device__ __forceinline__ float2 k2t_target(const int4 rc, const float2* w, const int2* __restrict__ ov) {
   const float w0 = __int_as_float(rc.y);
@@ -271,34 +272,34 @@ __device__ __forceinline__ float2 k2t_target(const int4 rc, const float2* w, con
   return acc;
 }
 
-__global__ void __launch_bounds__(256) k2t_sum(DevPlan P) {
+__global__ void __launch_bounds__(kSumThreads) k2t_sum(DevPlan P) {
   extern __shared__ __align__(16) float2 win[];
   const Consts& C = P.C;
-  const int p = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int p = blockIdx.x, b = C.b0 + blockIdx.y, tid = threadIdx.x;
   const int n0 = __ldg(&P.k2_colptr[p > 0 ? p - 1 : 0]), nw = __ldg(&P.k2_colptr[p + 1]) - n0;
   const int ta = __ldg(&P.k2t_colptr[p]), tb = __ldg(&P.k2t_colptr[p + 1]);
   int4 rec[kSumKT];
 #pragma unroll
   for (int k = 0; k < kSumKT; ++k) {
-    const int t = ta + tid + 256 * k;
+    const int t = ta + tid + kSumThreads * k;
     rec[k] = (t < tb) ? __ldg(&P.k2t_rec[t]) : make_int4(0, 0, 0, 0);
   }
   const float2* S2 = P.S2 + (size_t)b * C.half * C.NL + n0;
-  for (int i = tid; i < nw; i += 256) win[i] = __ldg(&S2[i]);
+  for (int i = tid; i < nw; i += kSumThreads) win[i] = __ldg(&S2[i]);
   __syncthreads();
   float2* Rc = P.Rc + (size_t)b * C.ntpad;
   const float2* w = win - n0;
 #pragma unroll
   for (int k = 0; k < kSumKT; ++k) {
-    const int t = ta + tid + 256 * k;
+    const int t = ta + tid + kSumThreads * k;
     if (t < tb) Rc[t] = k2t_target(rec[k], w, P.k2t_ov);
   }
-  for (int t = ta + tid + 256 * kSumKT; t < tb; t += 256) Rc[t] = k2t_target(__ldg(&P.k2t_rec[t]), w, P.k2t_ov);
+  for (int t = ta + tid + kSumThreads * kSumKT; t < tb; t += kSumThreads) Rc[t] = k2t_target(__ldg(&P.k2t_rec[t]), w, P.k2t_ov);
 }
 
 static cudaError_t launch_k2t_sum(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
-  k2t_sum<<<dim3(C.ncols, C.batch), 256, (size_t)C.k2t_win * sizeof(float2), s>>>(P);
+  k2t_sum<<<dim3(C.ncols, C.batch), kSumThreads, (size_t)C.k2t_win * sizeof(float2), s>>>(P);
   return cudaGetLastError();
 }
 
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(1024) k2t_adj(DevPlan P) {
   constexpr int rs = rstride(n);
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs;
-  const int b = blockIdx.y;
+  const int b = C.b0 + blockIdx.y;
   const int P0 = blockIdx.x * kStrip;
   const int Pend = min(P0 + kStrip, C.ncols);
   const int g = threadIdx.x / (n / 8), j = threadIdx.x & (n / 8 - 1);
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, const __grid_constant
   constexpr int rs = rstride(n);
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs, N = C.N;
-  const int b = blockIdx.y, y0 = 4 * blockIdx.x;
+  const int b = C.b0 + blockIdx.y, y0 = 4 * blockIdx.x;
   const int g = threadIdx.x / (n / 8), j = threadIdx.x & (n / 8 - 1);
   const int so = g * rs;
   float2 post[8];

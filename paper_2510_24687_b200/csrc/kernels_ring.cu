@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
   constexpr int NOUT = (Kp * 2 * G + T - 1) / T;         // <= 9
   const Consts& C = P.C;
   const int NL = C.NL;
-  const int b = blockIdx.y, j0 = blockIdx.x * (2 * G);
+  const int b = C.b0 + blockIdx.y, j0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S2 = P.S2 + (size_t)b * half * NL;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
   constexpr int NOUT = half * 2 * G / T;      // = 8
   const Consts& C = P.C;
   const int NL = C.NL;
-  const int b = blockIdx.y, j0 = blockIdx.x * (2 * G);
+  const int b = C.b0 + blockIdx.y, j0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
   constexpr int NIN = (Kp * G + T - 1) / T;   // <= 5
   const Consts& C = P.C;
   const int n_t = C.n_t, n_det = C.n_det;
-  const int b = blockIdx.y, t0 = blockIdx.x * (2 * G);
+  const int b = C.b0 + blockIdx.y, t0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restri
   constexpr int NOUT = (Kp * G + T - 1) / T;  // <= 5
   const Consts& C = P.C;
   const int n_t = C.n_t, n_det = C.n_det;
-  const int b = blockIdx.y, t0 = blockIdx.x * (2 * G);
+  const int b = C.b0 + blockIdx.y, t0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const int tt_n = min(2 * G, n_t - t0);

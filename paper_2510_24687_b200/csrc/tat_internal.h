@@ -13,6 +13,7 @@ namespace tat {
 // Derived constants of the discretisation (D0).
 struct Consts {
   int n = 0, n_det = 0, n_t = 0, batch = 0;
+  int b0 = 0;       // first image of a launch (sub-batch pipelining); batch = images in it
   double R = 1, c = 1, T = 1;
   double h = 0, T_new0 = 0, T_new = 0, Lbox = 0, dxi = 0, dt = 0, dlam = 0, lam_max = 0;
   double wJ = 1, omega = 0;
