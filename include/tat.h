@@ -83,6 +83,33 @@ tat_status tat_forward_host(const tat_plan* plan, const float* f_host, float* g_
 tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_host,
                             cudaStream_t stream);
 
+/* ---- Iterative reconstruction driver.  NNLS as projected gradient descent,
+ * PAPER.md §4.2 "Reconstruction methods" L838-850 (E:operators L164-167):
+ *     f^(k+1/2) = f^(k) - lambda A*(A f^(k) - g),   f^(k+1) = Pi_Omega0 max(0, f^(k+1/2))
+ * (eq:NNLS-projstep, eqn:projectionHalfCircle).  The residual and the update are fused into
+ * the epilogues of the last forward / adjoint kernels (no extra elementwise passes).
+ *
+ * tat_residual:     r = A f - g_obs.  f device [batch][n][n]; g_obs, r device
+ *                   [batch][n_t][n_det] (r may not alias g_obs).  Enqueued on `stream`.
+ * tat_adjoint_step: f <- P(f - lambda A* r) in place, P = max(0, .) if nonneg != 0, then times
+ *                   roi[iy][ix] (device [n][n] float32 mask, shared by the batch) if roi != NULL.
+ *                   TAT_ERR_INVALID_ARGUMENT if lambda is not finite.
+ * tat_nnls:         `iters` iterations of the two calls above (r_work: device data-sized
+ *                   scratch).  f holds the start value (the paper starts from 0) and receives
+ *                   the iterate.  Enqueue-only: capturable in a CUDA graph.
+ * tat_power_norm:   lambda_max = the largest eigenvalue of A*A (Rayleigh quotients of `iters`
+ *                   power iterations from a seeded counter-based random start over the whole
+ *                   batch); the step lambda of eq. NNLS must satisfy 0 < lambda < 2 / lambda_max.
+ *                   SYNCHRONOUS (setup): synchronises `stream`; uses plan-owned buffers. */
+tat_status tat_residual(const tat_plan* plan, const float* f, const float* g_obs, float* r,
+                        cudaStream_t stream);
+tat_status tat_adjoint_step(const tat_plan* plan, const float* r, float* f, float lambda,
+                            int nonneg, const float* roi, cudaStream_t stream);
+tat_status tat_nnls(const tat_plan* plan, const float* g_obs, float* f, float* r_work,
+                    float lambda, int iters, int nonneg, const float* roi, cudaStream_t stream);
+tat_status tat_power_norm(const tat_plan* plan, int iters, unsigned long long seed,
+                          double* lambda_max, cudaStream_t stream);
+
 /* NULL-safe.  The caller must ensure no work using the plan is in flight. */
 void tat_plan_destroy(tat_plan* plan);
 

@@ -372,3 +372,38 @@ def forward(f: np.ndarray, C: Constants) -> np.ndarray:
 def adjoint(g: np.ndarray, C: Constants) -> np.ndarray:
     """A* g for [n_t, n_det] or [B, n_t, n_det]; returns [.., n, n] float64."""
     return _batched(lambda x, c: adjoint_stages(x, c)["f"], g, C)
+
+
+# ---------------------------------------------------------------------------------------------
+# Iterative reconstruction (SURVEY §8(f) f2): NNLS as projected gradient descent,
+# PAPER.md §4.2 "Reconstruction methods" L838-850, with the gradient of the data fidelity
+# E:operators (L164-167): grad ||A f - g||^2 = 2 A*(A f - g).
+#     f^(k+1/2) = f^(k) - lambda A*(A f^(k) - g)             (L841-843)
+#     f^(k+1)   = Pi_Omega0 max(0, f^(k+1/2))                (eq:NNLS-projstep L845,
+#                                                             eqn:projectionHalfCircle L848-850)
+# Pi_Omega0 is a 0/1 mask over the pixels (None: the whole image).  f^(0) = 0 in the paper.
+
+def nnls(g_obs: np.ndarray, f0: np.ndarray, C: Constants, lam: float, iters: int,
+         nonneg: bool = True, roi: np.ndarray | None = None) -> np.ndarray:
+    f = np.array(f0, dtype=np.float64)
+    for _ in range(iters):
+        f = f - lam * adjoint(forward(f, C) - g_obs, C)              # L841-843
+        if nonneg:
+            f = np.maximum(f, 0.0)                                     # L845
+        if roi is not None:
+            f = f * roi                                                # L848-850
+    return f
+
+
+def power_norm(C: Constants, v0: np.ndarray, iters: int) -> float:
+    """Largest eigenvalue of A*A (self-adjoint in X; eqn:innerProducts P:L217-222) by power
+    iteration from v0: the last Rayleigh quotient <v, A*A v> / <v, v>.  The NNLS step must
+    satisfy 0 < lambda < 2 / lambda_max for the projected gradient to be a descent method."""
+    v = np.array(v0, dtype=np.float64)
+    lam = 0.0
+    for _ in range(iters):
+        v = v / np.linalg.norm(v)
+        u = adjoint(forward(v, C), C)
+        lam = float(np.sum(v * u))
+        v = u
+    return lam

@@ -179,7 +179,8 @@ __global__ void k5_synth_restrict(DevPlan P, float* __restrict__ g) {
   float2* X = smem_fft<1>(A, Bf, nphi, TT, P.tw_ring);
   for (int idx = threadIdx.x; idx < tt_n * C.n_det; idx += blockDim.x) {
     int tt = idx / C.n_det, d = idx - tt * C.n_det;
-    g[((size_t)b * C.n_t + t0 + tt) * C.n_det + d] = X[tt * nphi + __ldg(&P.ring[d])].x;
+    const size_t i = ((size_t)b * C.n_t + t0 + tt) * C.n_det + d;
+    g[i] = epi_fwd(P, i, X[tt * nphi + __ldg(&P.ring[d])].x);
   }
 }
 

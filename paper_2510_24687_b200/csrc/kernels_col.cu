@@ -452,11 +452,12 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
     float2 acc[16];
     stage_a_adj<G>(W, A, pw, j, sg, acc);
     residue_reduce<G>(W, acc, j, sg);
-    float* o = fout + ((size_t)b * n + y0 + 2 * pr) * n;
+    const size_t o = ((size_t)b * n + y0 + 2 * pr) * n;
+    const int oxy = (y0 + 2 * pr) * n;
     for (int xx = t; xx < n; xx += G::T) {
       const float2 z = residue_sum<G>(W, xx);
-      o[xx] = z.x;
-      o[n + xx] = z.y;
+      epi_adj_store(P, fout, o + xx, oxy + xx, z.x);
+      epi_adj_store(P, fout, o + n + xx, oxy + n + xx, z.y);
     }
   }
 }

@@ -436,13 +436,14 @@ __global__ void __launch_bounds__(1024) k1t_adj(DevPlan P, const __grid_constant
 #pragma unroll
     for (int e = 0; e < 8; ++e) red[so + last_pos<n>(j, e)] = cmulc(v[e], post[e]);
     __syncthreads();
-    float* o = fout + ((size_t)b * n + y0 + 2 * pr) * n;
+    const size_t o = ((size_t)b * n + y0 + 2 * pr) * n;
+    const int oxy = (y0 + 2 * pr) * n;
     for (int xp = threadIdx.x; xp < n; xp += blockDim.x) {
       float2 acc = red[xp];
       for (int gg = 1; gg < L; ++gg) acc = cadd(acc, red[gg * rs + xp]);
       const int x = (xp + n / 2) & (n - 1);
-      o[x] = acc.x;
-      o[n + x] = acc.y;
+      epi_adj_store(P, fout, o + x, oxy + x, acc.x);
+      epi_adj_store(P, fout, o + n + x, oxy + n + x, acc.y);
     }
     __syncthreads();
   }

@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
   for (int idx = threadIdx.x; idx < tt_n * n_det; idx += blockDim.x) {
     const int tt = idx / n_det, d = idx - tt * n_det;
     const float2 z = X[(tt >> 1) * rs + phys(__ldg(&P.ring[d]))];
-    gout[((size_t)b * n_t + t0 + tt) * n_det + d] = (tt & 1) ? z.y : z.x;
+    const size_t i = ((size_t)b * n_t + t0 + tt) * n_det + d;
+    gout[i] = epi_fwd(P, i, (tt & 1) ? z.y : z.x);
   }
 }
 

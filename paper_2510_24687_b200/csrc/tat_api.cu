@@ -3,10 +3,12 @@
 #include "tat_internal.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 using namespace tat;
@@ -19,6 +21,8 @@ struct tat_plan {
   size_t workspace_bytes = 0, table_bytes = 0;
   float* stage_in = nullptr;    // host-variant staging: [B][n][n]
   float* stage_out = nullptr;   // [B][n_t][n_det]
+  float* pw_img = nullptr;      // power iteration: second image buffer [B][n][n]
+  float* pw_part = nullptr;     // kUtilBlocks partial dot products
   // profiling
   int prof_max = 0, prof_fwd = 0, prof_adj = 0;
   std::vector<cudaEvent_t> prof_ev;   // (prof_max) sets of 6 events
@@ -300,6 +304,102 @@ tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_
   if (st != TAT_OK) return st;
   e = cudaMemcpyAsync(f_host, p->stage_in, nimg, cudaMemcpyDeviceToHost, stream);
   if (e != cudaSuccess) return cuda_fail(e, "D2H");
+  return TAT_OK;
+}
+
+// ------------------------------------------------------------------ iterative driver
+// NNLS / projected Landweber (§4.2): r = A f - g (fused into the last forward
+// stage), f <- Pi max(0, f - lambda A* r) (fused into the last adjoint stage).
+tat_status tat_residual(const tat_plan* plan, const float* f, const float* g_obs, float* r,
+                        cudaStream_t stream) {
+  if (!plan || !f || !g_obs || !r) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  DevPlan Q = plan->P;
+  Q.epi_sub = g_obs;
+  cudaError_t e = launch_forward(Q, plan->tm_s1, f, r, stream, nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_residual launch");
+  return TAT_OK;
+}
+
+tat_status tat_adjoint_step(const tat_plan* plan, const float* r, float* f, float lambda,
+                            int nonneg, const float* roi, cudaStream_t stream) {
+  if (!plan || !f || !r) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  if (!std::isfinite(lambda)) return fail(TAT_ERR_INVALID_ARGUMENT, "lambda is not finite");
+  DevPlan Q = plan->P;
+  Q.epi_update = nonneg ? 2 : 1;
+  Q.epi_tau = lambda;
+  Q.epi_roi = roi;
+  cudaError_t e = launch_adjoint(Q, plan->tm_s1, r, f, stream, nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_adjoint_step launch");
+  return TAT_OK;
+}
+
+tat_status tat_nnls(const tat_plan* plan, const float* g_obs, float* f, float* r_work,
+                    float lambda, int iters, int nonneg, const float* roi, cudaStream_t stream) {
+  if (!plan || !g_obs || !f || !r_work) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  if (iters < 0) return fail(TAT_ERR_INVALID_ARGUMENT, "iters < 0");
+  if (!std::isfinite(lambda)) return fail(TAT_ERR_INVALID_ARGUMENT, "lambda is not finite");
+  for (int k = 0; k < iters; ++k) {
+    tat_status st = tat_residual(plan, f, g_obs, r_work, stream);
+    if (st != TAT_OK) return st;
+    st = tat_adjoint_step(plan, r_work, f, lambda, nonneg, roi, stream);
+    if (st != TAT_OK) return st;
+  }
+  return TAT_OK;
+}
+
+static cudaError_t dot_host(tat_plan* p, const float* a, const float* b, size_t count,
+                            cudaStream_t s, double* out) {
+  cudaError_t e = launch_dot_partial(a, b, count, p->pw_part, s);
+  float part[kUtilBlocks];
+  if (e == cudaSuccess) e = cudaMemcpyAsync(part, p->pw_part, sizeof part, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  double acc = 0.0;
+  for (int i = 0; i < kUtilBlocks; ++i) acc += part[i];   // fixed order
+  *out = acc;
+  return e;
+}
+
+tat_status tat_power_norm(const tat_plan* plan, int iters, unsigned long long seed,
+                          double* lambda_max, cudaStream_t stream) {
+  if (!plan || !lambda_max || iters < 1) return fail(TAT_ERR_INVALID_ARGUMENT, "bad arguments");
+  tat_plan* p = const_cast<tat_plan*>(plan);
+  tat_status st = ensure_staging(p);
+  if (st != TAT_OK) return st;
+  const Consts& C = p->P.C;
+  const size_t nimg = (size_t)C.batch * C.n * C.n;
+  cudaError_t e = cudaSuccess;
+  if (!p->pw_img) {
+    void* a = nullptr;
+    void* b = nullptr;
+    e = cudaMalloc(&a, nimg * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&b, kUtilBlocks * sizeof(float));
+    if (e != cudaSuccess) {
+      if (a) cudaFree(a);
+      return cuda_fail(e, "power-iteration buffers");
+    }
+    p->allocs.push_back(a);
+    p->allocs.push_back(b);
+    p->pw_img = (float*)a;
+    p->pw_part = (float*)b;
+  }
+  float* v = p->stage_in;    // current vector
+  float* u = p->pw_img;      // A* A v
+  float* w = p->stage_out;   // A v
+  e = launch_fill_random(v, nimg, seed, stream);
+  double lam = 0.0;
+  for (int it = 0; it < iters && e == cudaSuccess; ++it) {
+    double vv = 0.0;
+    e = dot_host(p, v, v, nimg, stream, &vv);
+    if (e != cudaSuccess) break;
+    if (!(vv > 0.0)) return fail(TAT_ERR_CUDA, "power iteration collapsed to zero");
+    e = launch_scale(v, nimg, (float)(1.0 / std::sqrt(vv)), stream);
+    if (e == cudaSuccess) e = launch_forward(p->P, p->tm_s1, v, w, stream, nullptr);
+    if (e == cudaSuccess) e = launch_adjoint(p->P, p->tm_s1, w, u, stream, nullptr);
+    if (e == cudaSuccess) e = dot_host(p, v, u, nimg, stream, &lam);   // Rayleigh quotient
+    std::swap(v, u);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "tat_power_norm");
+  *lambda_max = lam;
   return TAT_OK;
 }
 

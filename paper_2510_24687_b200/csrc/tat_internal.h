@@ -94,7 +94,33 @@ struct DevPlan {
   float2* S3 = nullptr;   // [B][Kp][NL]
   float2* S4 = nullptr;   // [B][Kp][n_t]
   float2* Rc = nullptr;   // [B][ntpad]: K2T target sums (transposed bilinear), column order
+  // epilogue of the last stage of a launch (fused iterative-driver steps, tat_residual /
+  // tat_adjoint_step): forward stores A f - epi_sub when epi_sub != nullptr; adjoint with
+  // epi_update != 0 stores f <- f - epi_tau (A* g) in place, then max(0, .) if epi_update == 2,
+  // then times epi_roi[iy][ix] if epi_roi != nullptr.
+  const float* epi_sub = nullptr;
+  const float* epi_roi = nullptr;
+  float epi_tau = 0.f;
+  int epi_update = 0;
 };
+
+#ifdef __CUDACC__
+// forward epilogue: value at flat output index i of g
+__device__ __forceinline__ float epi_fwd(const DevPlan& P, size_t i, float v) {
+  return P.epi_sub ? v - __ldg(&P.epi_sub[i]) : v;
+}
+// adjoint epilogue: store value v of A* g at flat index i of f (pixel ixy = i mod n^2)
+__device__ __forceinline__ void epi_adj_store(const DevPlan& P, float* f, size_t i, int ixy, float v) {
+  if (P.epi_update) {
+    float o = f[i] - P.epi_tau * v;
+    if (P.epi_update == 2) o = fmaxf(o, 0.f);
+    if (P.epi_roi) o *= __ldg(&P.epi_roi[ixy]);
+    f[i] = o;
+  } else {
+    f[i] = v;
+  }
+}
+#endif
 
 // Launchers (kernels.cu).  ev != nullptr: record ev[i] before stage i and ev[5] at the end.
 cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float* f, float* g,
@@ -138,6 +164,12 @@ size_t smem_k4c(const Consts& C);
 cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s);
 cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
 cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s);
+
+// kernels_util.cu: setup vector kernels (power iteration)
+constexpr int kUtilBlocks = 296;
+cudaError_t launch_fill_random(float* v, size_t count, unsigned long long seed, cudaStream_t s);
+cudaError_t launch_scale(float* v, size_t count, float f, cudaStream_t s);
+cudaError_t launch_dot_partial(const float* a, const float* b, size_t count, float* partial, cudaStream_t s);
 
 constexpr int kLaunchesForward = 5;
 constexpr int kLaunchesAdjoint = 5;

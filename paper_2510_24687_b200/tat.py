@@ -24,6 +24,7 @@ STATUS = {0: "TAT_OK", 1: "TAT_ERR_INVALID_ARGUMENT", 2: "TAT_ERR_UNSUPPORTED_GE
 EXPORTS = ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
            "tat_adjoint_host", "tat_plan_destroy", "tat_plan_info", "tat_plan_derive",
            "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
+           "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm",
            "tat_status_string", "tat_last_error")
 
 
@@ -75,13 +76,19 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.tat_plan_host_multiplier.argtypes = [i, i, i, d, d, d, dp, ctypes.POINTER(ctypes.c_float), sz]
     lib.tat_profile_begin.argtypes = [vp, i]
     lib.tat_profile_end.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ip, ip]
+    f32 = ctypes.c_float
+    lib.tat_residual.argtypes = [vp, vp, vp, vp, vp]
+    lib.tat_adjoint_step.argtypes = [vp, vp, vp, f32, i, vp, vp]
+    lib.tat_nnls.argtypes = [vp, vp, vp, vp, f32, i, i, vp, vp]
+    lib.tat_power_norm.argtypes = [vp, i, ctypes.c_ulonglong, dp, vp]
     lib.tat_status_string.argtypes = [i]
     lib.tat_status_string.restype = ctypes.c_char_p
     lib.tat_last_error.argtypes = []
     lib.tat_last_error.restype = ctypes.c_char_p
     for name in ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
                  "tat_adjoint_host", "tat_plan_info", "tat_plan_derive",
-                 "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end"):
+                 "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
+                 "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -187,6 +194,55 @@ class Plan:
         _check(self._lib.tat_adjoint(self._h, ctypes.c_void_p(g.data_ptr()),
                                      ctypes.c_void_p(f.data_ptr()), self._stream(stream)))
         return f
+
+    # ---- iterative driver (NNLS / projected Landweber, §4.2)
+    def residual(self, f, g_obs, out=None, stream=None):
+        """r = A f - g_obs (fused into the last forward kernel)."""
+        import torch
+        self._chk(f, (self.batch, self.n, self.n), "f")
+        self._chk(g_obs, (self.batch, self.n_t, self.n_det), "g_obs")
+        r = out if out is not None else torch.empty_like(g_obs)
+        self._chk(r, (self.batch, self.n_t, self.n_det), "r")
+        _check(self._lib.tat_residual(self._h, ctypes.c_void_p(f.data_ptr()),
+                                      ctypes.c_void_p(g_obs.data_ptr()),
+                                      ctypes.c_void_p(r.data_ptr()), self._stream(stream)))
+        return r
+
+    def _roi(self, roi):
+        if roi is None:
+            return ctypes.c_void_p(None)
+        self._chk(roi, (self.n, self.n), "roi")
+        return ctypes.c_void_p(roi.data_ptr())
+
+    def adjoint_step(self, r, f, lam: float, nonneg: bool = True, roi=None, stream=None):
+        """f <- Pi max(0, f - lam A* r) in place (fused into the last adjoint kernel)."""
+        self._chk(r, (self.batch, self.n_t, self.n_det), "r")
+        self._chk(f, (self.batch, self.n, self.n), "f")
+        _check(self._lib.tat_adjoint_step(self._h, ctypes.c_void_p(r.data_ptr()),
+                                          ctypes.c_void_p(f.data_ptr()), float(lam), int(nonneg),
+                                          self._roi(roi), self._stream(stream)))
+        return f
+
+    def nnls(self, g_obs, f, lam: float, iters: int, nonneg: bool = True, roi=None, r_work=None,
+             stream=None):
+        """`iters` NNLS iterations in place on f (start value in f); enqueue-only."""
+        import torch
+        self._chk(g_obs, (self.batch, self.n_t, self.n_det), "g_obs")
+        self._chk(f, (self.batch, self.n, self.n), "f")
+        r = r_work if r_work is not None else torch.empty_like(g_obs)
+        self._chk(r, (self.batch, self.n_t, self.n_det), "r_work")
+        _check(self._lib.tat_nnls(self._h, ctypes.c_void_p(g_obs.data_ptr()),
+                                  ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(r.data_ptr()),
+                                  float(lam), int(iters), int(nonneg), self._roi(roi),
+                                  self._stream(stream)))
+        return f
+
+    def power_norm(self, iters: int = 20, seed: int = 0, stream=None) -> float:
+        """Largest eigenvalue of A*A by power iteration (synchronous setup call)."""
+        out = ctypes.c_double()
+        _check(self._lib.tat_power_norm(self._h, int(iters), ctypes.c_ulonglong(seed),
+                                        ctypes.byref(out), self._stream(stream)))
+        return out.value
 
     def forward_host(self, f_host: np.ndarray, g_host: np.ndarray, stream=None):
         """Host-buffer variant (H2D + A + D2H on the stream); caller synchronises."""
