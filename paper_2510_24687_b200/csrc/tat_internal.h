@@ -172,6 +172,6 @@ cudaError_t launch_scale(float* v, size_t count, float f, cudaStream_t s);
 cudaError_t launch_dot_partial(const float* a, const float* b, size_t count, float* partial, cudaStream_t s);
 
 constexpr int kLaunchesForward = 5;
-constexpr int kLaunchesAdjoint = 5;
+constexpr int kLaunchesAdjoint = 6;   // K5T K4T K3T K2Ta K2Tb K1T
 
 }  // namespace tat
