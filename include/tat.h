@@ -83,6 +83,16 @@ tat_status tat_forward_host(const tat_plan* plan, const float* f_host, float* g_
 tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_host,
                             cudaStream_t stream);
 
+/* ---- Euclidean transposes for reverse-mode autodiff.  A* is the L2
+ * adjoint omega A^T (reading G20); a framework's backward pass needs the Euclidean transpose:
+ *   d/df <A f, w>  = A^T w      -> tat_transpose(g = w, f = out):  out = A^T w = A* w / omega
+ *   d/dg <A* g, v> = omega A v  -> tat_forward_scaled(f = v, g = out, alpha = omega)
+ * tat_forward_scaled: g = alpha * A f (alpha applied in the last forward kernel).
+ * Shapes, streams and errors as tat_forward / tat_adjoint; alpha must be finite. */
+tat_status tat_transpose(const tat_plan* plan, const float* g, float* f, cudaStream_t stream);
+tat_status tat_forward_scaled(const tat_plan* plan, const float* f, float* g, float alpha,
+                              cudaStream_t stream);
+
 /* ---- Iterative reconstruction driver.  NNLS as projected gradient descent,
  * PAPER.md §4.2 "Reconstruction methods" L838-850 (E:operators L164-167):
  *     f^(k+1/2) = f^(k) - lambda A*(A f^(k) - g),   f^(k+1) = Pi_Omega0 max(0, f^(k+1/2))

@@ -307,6 +307,27 @@ tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_
   return TAT_OK;
 }
 
+// ------------------------------------------------------------------ autograd support
+tat_status tat_transpose(const tat_plan* plan, const float* g, float* f, cudaStream_t stream) {
+  if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  DevPlan Q = plan->P;
+  Q.C.omega = 1.0;   // omega enters only through the K4T multiplier: A^T = A* / omega
+  cudaError_t e = launch_adjoint(Q, plan->tm_s1, g, f, stream, nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_transpose launch");
+  return TAT_OK;
+}
+
+tat_status tat_forward_scaled(const tat_plan* plan, const float* f, float* g, float alpha,
+                              cudaStream_t stream) {
+  if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  if (!std::isfinite(alpha)) return fail(TAT_ERR_INVALID_ARGUMENT, "alpha is not finite");
+  DevPlan Q = plan->P;
+  Q.epi_scale = alpha;
+  cudaError_t e = launch_forward(Q, plan->tm_s1, f, g, stream, nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_forward_scaled launch");
+  return TAT_OK;
+}
+
 // ------------------------------------------------------------------ iterative driver
 // NNLS / projected Landweber (§4.2): r = A f - g (fused into the last forward
 // stage), f <- Pi max(0, f - lambda A* r) (fused into the last adjoint stage).

@@ -100,6 +100,7 @@ struct DevPlan {
   // then times epi_roi[iy][ix] if epi_roi != nullptr.
   const float* epi_sub = nullptr;
   const float* epi_roi = nullptr;
+  float epi_scale = 1.f;   // forward: stores epi_scale * (A f) (- epi_sub)
   float epi_tau = 0.f;
   int epi_update = 0;
 };
@@ -107,6 +108,7 @@ struct DevPlan {
 #ifdef __CUDACC__
 // forward epilogue: value at flat output index i of g
 __device__ __forceinline__ float epi_fwd(const DevPlan& P, size_t i, float v) {
+  v *= P.epi_scale;
   return P.epi_sub ? v - __ldg(&P.epi_sub[i]) : v;
 }
 // adjoint epilogue: store value v of A* g at flat index i of f (pixel ixy = i mod n^2)

@@ -24,6 +24,7 @@ STATUS = {0: "TAT_OK", 1: "TAT_ERR_INVALID_ARGUMENT", 2: "TAT_ERR_UNSUPPORTED_GE
 EXPORTS = ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
            "tat_adjoint_host", "tat_plan_destroy", "tat_plan_info", "tat_plan_derive",
            "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
+           "tat_transpose", "tat_forward_scaled",
            "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm",
            "tat_status_string", "tat_last_error")
 
@@ -77,6 +78,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.tat_profile_begin.argtypes = [vp, i]
     lib.tat_profile_end.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ip, ip]
     f32 = ctypes.c_float
+    lib.tat_transpose.argtypes = [vp, vp, vp, vp]
+    lib.tat_forward_scaled.argtypes = [vp, vp, vp, f32, vp]
     lib.tat_residual.argtypes = [vp, vp, vp, vp, vp]
     lib.tat_adjoint_step.argtypes = [vp, vp, vp, f32, i, vp, vp]
     lib.tat_nnls.argtypes = [vp, vp, vp, vp, f32, i, i, vp, vp]
@@ -88,6 +91,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
                  "tat_adjoint_host", "tat_plan_info", "tat_plan_derive",
                  "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
+                 "tat_transpose", "tat_forward_scaled",
                  "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -195,6 +199,37 @@ class Plan:
                                      ctypes.c_void_p(f.data_ptr()), self._stream(stream)))
         return f
 
+    def transpose(self, g, out=None, stream=None):
+        """f = A^T g (Euclidean transpose, = A* g / omega): the backward of A."""
+        import torch
+        self._chk(g, (self.batch, self.n_t, self.n_det), "g")
+        f = out if out is not None else torch.empty((self.batch, self.n, self.n),
+                                                    device=g.device, dtype=torch.float32)
+        self._chk(f, (self.batch, self.n, self.n), "f")
+        _check(self._lib.tat_transpose(self._h, ctypes.c_void_p(g.data_ptr()),
+                                       ctypes.c_void_p(f.data_ptr()), self._stream(stream)))
+        return f
+
+    def forward_scaled(self, f, alpha: float, out=None, stream=None):
+        """g = alpha A f (alpha = omega: the backward of A*)."""
+        import torch
+        self._chk(f, (self.batch, self.n, self.n), "f")
+        g = out if out is not None else torch.empty((self.batch, self.n_t, self.n_det),
+                                                    device=f.device, dtype=torch.float32)
+        self._chk(g, (self.batch, self.n_t, self.n_det), "g")
+        _check(self._lib.tat_forward_scaled(self._h, ctypes.c_void_p(f.data_ptr()),
+                                            ctypes.c_void_p(g.data_ptr()), float(alpha),
+                                            self._stream(stream)))
+        return g
+
+    def A(self, f):
+        """Differentiable A (torch.autograd): backward = A^T."""
+        return _ForwardFn.apply(f, self)
+
+    def Astar(self, g):
+        """Differentiable A* (torch.autograd): backward = omega A."""
+        return _AdjointFn.apply(g, self)
+
     # ---- iterative driver (NNLS / projected Landweber, PAPER.md §4.2 L838-850)
     def residual(self, f, g_obs, out=None, stream=None):
         """r = A f - g_obs (fused into the last forward kernel)."""
@@ -277,3 +312,46 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+# ---- torch.autograd wrappers: every pass runs in libtat's kernels
+def _autograd_fns():
+    import torch
+
+    class ForwardFn(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, f, plan):
+            ctx.plan = plan
+            return plan.forward(f.contiguous())
+
+        @staticmethod
+        def backward(ctx, grad_g):
+            return ctx.plan.transpose(grad_g.contiguous()), None
+
+    class AdjointFn(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, g, plan):
+            ctx.plan = plan
+            return plan.adjoint(g.contiguous())
+
+        @staticmethod
+        def backward(ctx, grad_f):
+            return ctx.plan.forward_scaled(grad_f.contiguous(), ctx.plan.omega), None
+
+    return ForwardFn, AdjointFn
+
+
+class _Lazy:
+    def __init__(self, idx):
+        self.idx = idx
+
+    def apply(self, *args):
+        global _FNS
+        if _FNS is None:
+            _FNS = _autograd_fns()
+        return _FNS[self.idx].apply(*args)
+
+
+_FNS = None
+_ForwardFn = _Lazy(0)
+_AdjointFn = _Lazy(1)
