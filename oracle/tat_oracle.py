@@ -407,3 +407,109 @@ def power_norm(C: Constants, v0: np.ndarray, iters: int) -> float:
         lam = float(np.sum(v * u))
         v = u
     return lam
+
+
+# ---------------------------------------------------------------------------------------------
+# Inverse A^{-1}: PAPER.md §3.3 "Inverse operator" L703-784, Algorithm 3,
+# E:approx_UBP (L721-726), E:Four_ser_v / E:Four_coef_v (L733-739), E:silly_integral (L747-749);
+# derivation in the Appendix (L1174-1249) for R = c = 1.
+#
+# Reading G21: E:Four_coef_v's prefactor -4 pi inherits the 2 pi of E:Fourier_Green
+# (reading G5: under the paper's F_2D convention P:L256-260, G = F^{-1}_2D(sin|xi|t / (2 pi |xi|)));
+# with the consistent Green's function the coefficient is
+#     vhat_k(lambda) = -2 (-i)^|k| J'_|k|(lambda) int_0^T g_k(t) sin(lambda t) dt.
+# The scale is pinned by A^{-1} A f ~ f (tests/test_oracle_inverse.py); -4 pi gives 2 pi f.
+#
+# Discretisation (the forward's grids, Alg. 3 "same sizes of grids ... as for A*" L743-745):
+#   1-2  g_k(t_m) = (1/n_phi) sum_l ghat(t_m, phi_l) e^{-i k phi_l}, ghat zero off the detectors
+#   3    vhat_k(lambda_j) = -2 (-i)^|k| J'_|k|(lambda_j) dt sum_m g_k(t_m) sin(lambda_j t_m)
+#        (rectangle rule on t_m = (m+1) dt, reading G18), J'_0 = -J_1,
+#        J'_m = (J_{m-1} - J_{m+1}) / 2 (the identities quoted in the Appendix)
+#   4    vhat(lambda_j, phi_l) = sum_{k=-K}^{K-1} vhat_k(lambda_j) e^{i k phi_l}
+#   5    bilinear interpolation in (lambda, phi) to the Cartesian nodes xi_pq = dxi (p, q) with
+#        |xi| < lambda_max (zero elsewhere; reading G22)
+#   6    v(x) = (dxi^2 / 2 pi) Re sum_{p,q} vhat(xi_pq) e^{i xi_pq . x} at the image nodes
+#   7    C = -mean of v over the image nodes with r0 < |x| < R (Omega \ Omega_0, open at the
+#        detector circle; reading G23)
+#   8    A^{-1} g = (v + C) on |x| <= r0, 0 elsewhere (Pi_Omega0)
+
+def inverse_multiplier_table(C: Constants) -> np.ndarray:
+    """mi[|k|, j] = -2 J'_|k|(lambda_j), |k| = 0..K (step 3 without dt and the phase)."""
+    lam = np.arange(C.J + 1) * C.dlam
+    Jv = special.jv(np.arange(C.K + 2)[:, None], lam[None, :])
+    Jp = np.empty((C.K + 1, C.J + 1))
+    Jp[0] = -Jv[1]
+    Jp[1:] = 0.5 * (Jv[0:C.K] - Jv[2:C.K + 2])
+    return -2.0 * Jp
+
+
+def _sin_matrix(C: Constants) -> np.ndarray:
+    """sinm[m, j] = sin(c lambda_j t_m) = sin(pi j (m+1) / M), argument reduced mod 2M."""
+    m1 = np.arange(1, C.n_t + 1, dtype=np.int64)
+    j = np.arange(C.J + 1, dtype=np.int64)
+    r = np.mod(np.outer(m1, j), 2 * C.M)
+    table = np.sin(np.pi * np.arange(2 * C.M) / C.M)
+    return table[r]
+
+
+def cartesian_polar_cells(C: Constants):
+    """Step 5 cells: for every Cartesian node (p, q) (centred indices, [N, N]) the polar cell
+    (j0, l0) and bilinear fractions (a, b) of rho = |xi| / dlam and theta / (2 pi / n_phi),
+    plus the mask rho < J."""
+    N = C.N
+    p = np.arange(N) - N // 2
+    Pg, Qg = np.meshgrid(p, p, indexing="ij")
+    rho = np.hypot(Pg.astype(np.float64), Qg.astype(np.float64)) * (C.dxi / C.dlam)
+    th = np.mod(np.arctan2(Qg.astype(np.float64), Pg.astype(np.float64)), 2 * np.pi) * (C.n_phi / (2 * np.pi))
+    inside = rho < C.J - 1e-9        # open disk: the grid holds only one side of each
+                                     # axis point |xi| = lambda_max (reading G22)
+    j0 = np.minimum(np.floor(rho), C.J - 1).astype(np.int64)
+    a = np.where(inside, rho - j0, 0.0)
+    l0f = np.floor(th)
+    b = th - l0f
+    l0 = np.mod(l0f.astype(np.int64), C.n_phi)
+    return j0, l0, a, b, inside
+
+
+def polar_to_cartesian(vpol: np.ndarray, C: Constants) -> np.ndarray:
+    """Step 5 (Alg. 3): V[p + N/2, q + N/2] from vpol[j, l]."""
+    j0, l0, a, b, inside = cartesian_polar_cells(C)
+    j0c = np.where(inside, j0, 0)
+    l1 = np.mod(l0 + 1, C.n_phi)
+    V = ((1 - a) * (1 - b) * vpol[j0c, l0] + a * (1 - b) * vpol[j0c + 1, l0]
+         + (1 - a) * b * vpol[j0c, l1] + a * b * vpol[j0c + 1, l1])
+    return np.where(inside, V, 0.0)
+
+
+def inverse(g: np.ndarray, C: Constants, r0: float) -> np.ndarray:
+    """A^{-1} g for one data set [n_t, n_det] (Algorithm 3, steps 1-8 above); [n, n] float64."""
+    if C.R != 1.0 or C.c != 1.0:
+        raise NotImplementedError("the paper derives A^{-1} for R = c = 1 (Appendix)")
+    if not (0.0 < r0 < C.R):
+        raise ValueError("r0 must lie in (0, R)")
+    gfull = restrict_adjoint(np.asarray(g, np.float64), C)                 # step 1
+    gk = synthesis_adjoint(gfull, C) / C.n_phi                              # step 2 [m, k]
+    sk = C.dt * (_sin_matrix(C).T @ gk)                                     # step 3 [j, k]
+    k = _harmonics(C)
+    mi = inverse_multiplier_table(C)[np.abs(k), :].T                        # [j, k]
+    vk = mi * np.conj(_i_pow(k))[None, :] * sk                              # (-i)^|k|
+    vpol = synthesis(vk, C)                                                 # step 4 [j, l]
+    V = polar_to_cartesian(vpol, C)                                         # step 5
+    n, N = C.n, C.N
+    pos = np.arange(n) - n // 2
+    E = _dft_matrix(_freqs(N), pos, N)
+    v = (C.dxi ** 2 / (2 * np.pi)) * (E.conj().T @ V @ E.conj())           # step 6 [ix, iy]
+    v = v.T.real
+    x = pos * C.h
+    X, Y = np.meshgrid(x, x)
+    r = np.hypot(X, Y)
+    ann = (r > r0) & (r < C.R)
+    Cc = -v[ann].mean() if ann.any() else 0.0                               # step 7
+    return np.where(r <= r0, v + Cc, 0.0)                                   # step 8
+
+
+def inverse_batch(g: np.ndarray, C: Constants, r0: float) -> np.ndarray:
+    g = np.asarray(g)
+    if g.ndim == 2:
+        return inverse(g, C, r0)
+    return np.stack([inverse(gi, C, r0) for gi in g])
