@@ -83,6 +83,20 @@ tat_status tat_forward_host(const tat_plan* plan, const float* f_host, float* g_
 tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_host,
                             cudaStream_t stream);
 
+/* ---- Inverse: A^{-1} g by the approximate universal backprojection of
+ * PAPER.md §3.3 Algorithm 3 (L703-784): analysis of g on the ring, the sine transform and the
+ * multiplier -2 (-i)^|k| J'_|k|(lambda) (E:Four_coef_v with the 2 pi of reading G21 removed),
+ * angular synthesis, bilinear interpolation in (lambda, phi) to the Cartesian nodes inside
+ * |xi| < lambda_max, the inverse 2-D DFT, the constant C of E:silly_integral over the annulus
+ * r0 < |x| < R, and Pi_Omega0 = restriction to |x| <= r0 (readings G22, G23).
+ *   g  device [batch][n_t][n_det];  f  device [batch][n][n] (output);  0 < r0 < R.
+ * The paper derives A^{-1} for R = c = 1: other R, c return TAT_ERR_UNSUPPORTED_GEOMETRY.
+ * The first call builds the interpolation tables (synchronous, ~32 bytes per Cartesian node of
+ * the half spectrum); a call with a new r0 uploads a pixel mask (synchronous); otherwise
+ * enqueue-only on `stream`. */
+tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0,
+                       cudaStream_t stream);
+
 /* ---- Euclidean transposes for reverse-mode autodiff.  A* is the L2
  * adjoint omega A^T (reading G20); a framework's backward pass needs the Euclidean transpose:
  *   d/df <A f, w>  = A^T w      -> tat_transpose(g = w, f = out):  out = A^T w = A* w / omega

@@ -343,4 +343,32 @@ cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float*
   return cudaGetLastError();
 }
 
+// Algorithm 3 through step 6: the adjoint chain with the sine transform and the
+// J' multiplier (P has dct_sine = 1, omega = 1, the inverse tables), the polar -> Cartesian
+// interpolation in place of K2Ta.  Steps 7-8 (constant, projection) are launched by the caller.
+cudaError_t launch_inverse(const DevPlan& P, const CUtensorMap& tm, const float* g, float* f,
+                           cudaStream_t s) {
+  const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
+  if (ring_fast_ok(C)) e = launch_k5t(P, g, s);
+  else k5t_analysis<<<dim3((C.n_t + tile_ring(C.n_ring) - 1) / tile_ring(C.n_ring), C.batch), kThreads,
+                      smem_ring(C), s>>>(P, g);
+  if (e != cudaSuccess) return e;
+  if (dct4_ok(C)) e = launch_k4c(P, true, s);
+  else if (dct_fast_r(C)) e = launch_k4_fast(P, true, s);
+  else return cudaErrorNotSupported;
+  if (e != cudaSuccess) return e;
+  if (ring_fast_ok(C)) e = launch_k3t(P, s);
+  else k3t_angular<<<dim3((C.NL + tile_ring(C.n_ring) - 1) / tile_ring(C.n_ring), C.batch), kThreads,
+                     smem_ring(C), s>>>(P);
+  if (e != cudaSuccess) return e;
+  e = launch_k2i_interp(P, s);
+  if (e != cudaSuccess) return e;
+  e = launch_k2tb(P, s);
+  if (e != cudaSuccess) return e;
+  e = launch_k1t(P, tm, f, s);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 }  // namespace tat

@@ -526,8 +526,18 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
     __syncthreads();
     // S(u) = X(u) + X(-u) = sum_e [W^{eu} Y_e(u) + conj(W^{eu}) Y_e(-u)], W = W_2M, 0 <= u < 4n;
     // outputs in groups of 4 per thread with all twiddle loads issued first
+    // D(u) = X(u) - X(-u) for the sine transform of the inverse (C.dct_sine, ADJ only):
+    // sum_i c_i sin(theta i u) = i D(u) / 2
+    const bool sine = ADJ && C.dct_sine;
     auto Ssum = [&](int u, float2 w1, float2 w2) -> float2 {
       const int vp = G::fq(u & (N4 - 1)), vm = G::fq((N4 - u) & (N4 - 1));
+      if (sine) {
+        const float2 a = csub(sm[vp], sm[vm]);
+        const float2 c1 = csub(cmul(sm[N4 + vp], w1), cmulc(sm[N4 + vm], w1));
+        const float2 c2 = csub(cmul(sm[2 * N4 + vp], w2), cmulc(sm[2 * N4 + vm], w2));
+        const float2 dd = ce::cadd(a, ce::cadd(c1, c2));
+        return make_float2(-dd.y, dd.x);   // i D
+      }
       const float2 a = ce::cadd(sm[vp], sm[vm]);
       const float2 c1 = ce::cadd(cmul(sm[N4 + vp], w1), cmulc(sm[N4 + vm], w1));
       const float2 c2 = ce::cadd(cmul(sm[2 * N4 + vp], w2), cmulc(sm[2 * N4 + vm], w2));

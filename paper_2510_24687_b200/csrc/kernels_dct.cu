@@ -97,7 +97,10 @@ __global__ void __launch_bounds__(512) k4_dct_fast(DevPlan P, int r) {
     for (int u = 0; u < 8; ++u) {   // NL <= nf = 8 * blockDim.x
       const int jj = threadIdx.x + u * (nf / 8);
       if (jj < NL) {
-        const float2 y = cscale(cadd(X(jj), X(jj == 0 ? 0 : M2 - jj)), 0.5f);
+        // cosine: (X(u) + X(-u)) / 2;  sine (C.dct_sine): i (X(u) - X(-u)) / 2
+        const float2 xp = X(jj), xm = X(jj == 0 ? 0 : M2 - jj);
+        const float2 y = C.dct_sine ? cscale(make_float2(xm.y - xp.y, xp.x - xm.x), 0.5f)
+                                    : cscale(cadd(xp, xm), 0.5f);
         out[jj] = mul_ipow_d(cscale(y, om * mloc[u]), -k);
       }
     }

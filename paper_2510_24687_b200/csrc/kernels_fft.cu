@@ -519,6 +519,14 @@ cudaError_t launch_k2(const DevPlan& P, cudaStream_t s) {
   TAT_DISPATCH_N(k2_fwd<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P));
   return cudaGetLastError();
 }
+cudaError_t launch_k2tb(const DevPlan& P, cudaStream_t s) {   // K2Tb only (targets in Rc)
+  const Consts& C = P.C;
+  if (col_ok(C)) return launch_k2c_adj(P, s);
+  const dim3 grid((C.ncols + kStrip - 1) / kStrip, C.batch);
+  TAT_DISPATCH_N(k2t_adj<NN><<<grid, fft_threads(C), smem_k2t(C), s>>>(P));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = launch_k2t_sum(P, s);

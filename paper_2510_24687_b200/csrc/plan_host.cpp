@@ -348,3 +348,82 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
 }
 
 }  // namespace tat
+
+namespace tat {
+
+// Inverse tables (Algorithm 3; readings G21-G23, see oracle/tat_oracle.py "Inverse").
+void build_inverse_tables(const Consts& C, const std::vector<int>& node_perm, InvTables& I) {
+  const int N = C.N, nphi = C.n_ring, half = C.half, NL = C.NL, Kp = C.Kp;
+  // ---- step 3 multiplier (with step 2's 1/n_phi and step 6's dxi^2 / 2pi folded in)
+  I.mult.assign((size_t)Kp * NL, 0.f);
+  {
+    std::vector<double> row(Kp + 1);
+    const double scale = (C.dxi * C.dxi / (2.0 * kPi)) / nphi * C.dt;
+    for (int j = 0; j < NL; ++j) {
+      bessel_row(j * C.dlam, C.K + 1, row.data());
+      for (int k = 0; k < Kp; ++k) {
+        const double jp = (k == 0) ? -row[1] : 0.5 * (row[k - 1] - row[k + 1]);   // J'_k
+        I.mult[(size_t)k * NL + j] = (float)(scale * (-2.0 * jp));
+      }
+    }
+  }
+  // ---- step 5 targets: Cartesian (p, q), p in [0, N/2], |xi| < lambda_max
+  const int Q0 = 16 * C.Lres;
+  auto code = [&](int j, long l) {
+    const long lp = ((l + nphi / 4) % nphi + nphi) % nphi;
+    if (lp < half) return node_perm[(size_t)j * half + lp];
+    return -(node_perm[(size_t)j * half + (lp - half)] + 1);
+  };
+  struct Tg { int key, q; int4 nd; float4 w; };
+  std::vector<Tg> col;
+  I.colptr.assign(C.ncols + 1, 0);
+  I.nodes.clear();
+  I.w.clear();
+  I.tq.clear();
+  I.max_per_col = 0;
+  const double rscale = C.dxi / C.dlam, tscale = nphi / (2.0 * kPi);
+  for (int p = 0; p < C.ncols; ++p) {
+    col.clear();
+    for (int q = -N / 2; q < N / 2; ++q) {
+      const double rho = std::hypot((double)p, (double)q) * rscale;
+      if (!(rho < C.J - 1e-9)) continue;
+      double th = std::fmod(std::atan2((double)q, (double)p), 2.0 * kPi);
+      if (th < 0) th += 2.0 * kPi;
+      th *= tscale;
+      const int j0 = std::min((int)std::floor(rho), C.J - 1);
+      const double a = rho - j0;
+      const double l0f = std::floor(th), bb = th - l0f;
+      const long l0 = (((long)l0f) % nphi + nphi) % nphi, l1 = (l0 + 1) % nphi;
+      const double hw = (p == 0) ? 0.5 : 1.0;   // Hermitian half spectrum (K1T doubles p = 0)
+      Tg t;
+      t.q = ((q % N) + N) % N;
+      t.key = (t.q % Q0) * (N / Q0) + t.q / Q0;
+      t.nd = make_int4(code(j0, l0), code(j0 + 1, l0), code(j0, l1), code(j0 + 1, l1));
+      t.w = make_float4((float)(hw * (1 - a) * (1 - bb)), (float)(hw * a * (1 - bb)),
+                        (float)(hw * (1 - a) * bb), (float)(hw * a * bb));
+      col.push_back(t);
+    }
+    std::sort(col.begin(), col.end(), [](const Tg& x, const Tg& y) { return x.key < y.key; });
+    for (const Tg& t : col) {
+      I.nodes.push_back(t.nd);
+      I.w.push_back(t.w);
+      I.tq.push_back(t.q);
+    }
+    I.colptr[p + 1] = I.colptr[p] + (int)col.size();
+    I.max_per_col = std::max(I.max_per_col, (int)col.size());
+  }
+  I.mask.clear();
+  I.base.clear();
+  if (col_ok(C)) {
+    I.mask.assign((size_t)C.ncols * Q0, 0u);
+    I.base.assign((size_t)C.ncols * Q0, 0);
+    for (int p = 0; p < C.ncols; ++p)
+      for (int t = I.colptr[p + 1] - 1; t >= I.colptr[p]; --t) {
+        const int q = I.tq[t], q0 = q % Q0, q1 = q / Q0;
+        I.mask[(size_t)p * Q0 + q0] |= 1u << q1;
+        I.base[(size_t)p * Q0 + q0] = t;
+      }
+  }
+}
+
+}  // namespace tat

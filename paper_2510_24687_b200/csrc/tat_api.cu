@@ -23,6 +23,14 @@ struct tat_plan {
   float* stage_out = nullptr;   // [B][n_t][n_det]
   float* pw_img = nullptr;      // power iteration: second image buffer [B][n][n]
   float* pw_part = nullptr;     // kUtilBlocks partial dot products
+  // inverse (built on first use)
+  std::vector<int> node_perm;   // host copy: (j, l') -> adjoint S2 position
+  bool inv_ready = false;
+  DevPlan Pinv;                 // P with the inverse tables swapped in
+  double inv_r0 = -1.0;
+  unsigned char* inv_region = nullptr;
+  float* inv_csum = nullptr;
+  int inv_annulus = 0;
   // profiling
   int prof_max = 0, prof_fwd = 0, prof_adj = 0;
   std::vector<cudaEvent_t> prof_ev;   // (prof_max) sets of 6 events
@@ -157,6 +165,7 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     if ((e = upload(p, H.k2_colptr, &P.k2_colptr, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2_nodes, &P.k2_nodes, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.node_perm, &P.node_perm, tb)) != cudaSuccess) break;
+    p->node_perm = H.node_perm;
     if ((e = upload(p, H.k2t_colptr, &P.k2t_colptr, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2t_tq, &P.k2t_tq, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2t_rec, &P.k2t_rec, tb)) != cudaSuccess) break;
@@ -325,6 +334,80 @@ tat_status tat_forward_scaled(const tat_plan* plan, const float* f, float* g, fl
   Q.epi_scale = alpha;
   cudaError_t e = launch_forward(Q, plan->tm_s1, f, g, stream, nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "tat_forward_scaled launch");
+  return TAT_OK;
+}
+
+// ------------------------------------------------------------------ inverse (Algorithm 3)
+static tat_status inverse_setup(tat_plan* p) {
+  if (p->inv_ready) return TAT_OK;
+  const Consts& C = p->P.C;
+  InvTables I;
+  build_inverse_tables(C, p->node_perm, I);
+  DevPlan Q = p->P;
+  size_t tb = 0;
+  cudaError_t e = cudaSuccess;
+  do {
+    if ((e = upload(p, I.mult, &Q.mult, tb)) != cudaSuccess) break;
+    if ((e = upload(p, I.nodes, &Q.inv_nodes, tb)) != cudaSuccess) break;
+    if ((e = upload(p, I.w, &Q.inv_w, tb)) != cudaSuccess) break;
+    if ((e = upload(p, I.colptr, &Q.k2t_colptr, tb)) != cudaSuccess) break;
+    if ((e = upload(p, I.tq, &Q.k2t_tq, tb)) != cudaSuccess) break;
+    if ((e = upload(p, I.mask, &Q.k2c_mask, tb)) != cudaSuccess) break;
+    if ((e = upload(p, I.base, &Q.k2c_base, tb)) != cudaSuccess) break;
+    Q.C.ntargets = (int)I.tq.size();
+    Q.C.ntpad = (Q.C.ntargets + 1) & ~1;
+    Q.C.k2c_rbuf = (I.max_per_col + 3) & ~1;
+    Q.C.omega = 1.0;
+    Q.C.dct_sine = 1;
+    void* d = nullptr;
+    if ((e = alloc_ws(p, (size_t)C.batch * Q.C.ntpad * sizeof(float2) + 16, &d)) != cudaSuccess) break;
+    Q.Rc = (float2*)d;
+    if ((e = alloc_ws(p, (size_t)C.n * C.n, &d)) != cudaSuccess) break;
+    p->inv_region = (unsigned char*)d;
+    if ((e = alloc_ws(p, (size_t)C.batch * sizeof(float), &d)) != cudaSuccess) break;
+    p->inv_csum = (float*)d;
+  } while (false);
+  p->table_bytes += tb;
+  if (e != cudaSuccess) return cuda_fail(e, "inverse tables");
+  if (col_ok(Q.C) && smem_k2c_adj(Q.C) > 227 * 1024)
+    return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: column target buffer exceeds shared memory");
+  p->Pinv = Q;
+  p->inv_ready = true;
+  return TAT_OK;
+}
+
+tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0,
+                       cudaStream_t stream) {
+  if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  const Consts& C = plan->P.C;
+  if (!(r0 > 0.0 && r0 < C.R)) return fail(TAT_ERR_INVALID_ARGUMENT, "r0 must lie in (0, R)");
+  if (C.R != 1.0 || C.c != 1.0)
+    return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: the paper derives A^-1 for R = c = 1");
+  if (!dct4_ok(C) && !dct_fast_r(C))
+    return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: no sine-transform kernel for this 2M");
+  tat_plan* p = const_cast<tat_plan*>(plan);
+  tat_status st = inverse_setup(p);
+  if (st != TAT_OK) return st;
+  cudaError_t e = cudaSuccess;
+  if (r0 != p->inv_r0) {   // region mask of Pi_Omega0 and the annulus (float64 decisions)
+    std::vector<unsigned char> reg((size_t)C.n * C.n);
+    int cnt = 0;
+    for (int iy = 0; iy < C.n; ++iy)
+      for (int ix = 0; ix < C.n; ++ix) {
+        const double r = std::hypot((ix - C.n / 2) * C.h, (iy - C.n / 2) * C.h);
+        unsigned char v = 0;
+        if (r <= r0) v = 1;
+        else if (r < C.R) { v = 2; ++cnt; }
+        reg[(size_t)iy * C.n + ix] = v;
+      }
+    e = cudaMemcpy(p->inv_region, reg.data(), reg.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "inverse region upload");
+    p->inv_r0 = r0;
+    p->inv_annulus = cnt;
+  }
+  e = launch_inverse(p->Pinv, p->tm_s1, g, f, stream);
+  if (e == cudaSuccess) e = launch_k2i_finish(p->Pinv, f, p->inv_region, p->inv_csum, p->inv_annulus, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_inverse launch");
   return TAT_OK;
 }
 

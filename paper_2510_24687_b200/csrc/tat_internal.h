@@ -14,6 +14,7 @@ namespace tat {
 struct Consts {
   int n = 0, n_det = 0, n_t = 0, batch = 0;
   int b0 = 0;       // first image of a launch (sub-batch pipelining); batch = images in it
+  int dct_sine = 0; // K4T computes sum_m G~ sin(c lambda_j t_m) (the inverse, Alg. 3 step 3)
   double R = 1, c = 1, T = 1;
   double h = 0, T_new0 = 0, T_new = 0, Lbox = 0, dxi = 0, dt = 0, dlam = 0, lam_max = 0;
   double wJ = 1, omega = 0;
@@ -88,6 +89,10 @@ struct DevPlan {
   const int* ring = nullptr;
   const uint32_t* k2c_mask = nullptr;
   const int* k2c_base = nullptr;
+  // inverse (Alg. 3 step 5): per Cartesian target 4 polar corners (sorted node index, or
+  // -(index + 1) for the conjugate mirror node) and bilinear weights
+  const int4* inv_nodes = nullptr;
+  const float4* inv_w = nullptr;
   // workspace
   float2* S1 = nullptr;   // [B][ncols][n]
   float2* S2 = nullptr;   // [B][half * NL]: forward ring-major [j][l'], adjoint K2 node order
@@ -139,6 +144,7 @@ cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out);
 cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
 cudaError_t launch_k2(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s);   // target sums + column IDFT
+cudaError_t launch_k2tb(const DevPlan& P, cudaStream_t s);  // column IDFT of the targets in Rc
 cudaError_t launch_k1t(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s);
 // kernels_ring.cu: K3, K3T, K5, K5T on n_phi-point register FFTs
 bool ring_fast_ok(const Consts& C);
@@ -166,6 +172,25 @@ size_t smem_k4c(const Consts& C);
 cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s);
 cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
 cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s);
+
+// kernels_inv.cu: inverse-specific stages (Alg. 3 steps 5, 7, 8)
+cudaError_t launch_k2i_interp(const DevPlan& P, cudaStream_t s);
+cudaError_t launch_k2i_finish(const DevPlan& P, float* f, const unsigned char* region, float* csum,
+                              int annulus_count, cudaStream_t s);
+// host tables of the inverse (built on first use)
+struct InvTables {
+  std::vector<float> mult;          // [Kp][NL]: (dxi^2/2pi)(1/n_phi) dt (-2 J'_k(lambda_j))
+  std::vector<int4> nodes;          // [T] corner codes
+  std::vector<float4> w;            // [T] corner weights (x 1/2 on column p = 0)
+  std::vector<int> colptr;          // [ncols + 1]
+  std::vector<int> tq;              // [T] q mod N
+  std::vector<uint32_t> mask;       // [ncols][16L] (col_ok only)
+  std::vector<int> base;            // [ncols][16L]
+  int max_per_col = 0;
+};
+void build_inverse_tables(const Consts& C, const std::vector<int>& node_perm, InvTables& I);
+cudaError_t launch_inverse(const DevPlan& P, const CUtensorMap& tm, const float* g, float* f,
+                           cudaStream_t s);
 
 // kernels_util.cu: setup vector kernels (power iteration)
 constexpr int kUtilBlocks = 296;

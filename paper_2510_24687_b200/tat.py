@@ -24,7 +24,7 @@ STATUS = {0: "TAT_OK", 1: "TAT_ERR_INVALID_ARGUMENT", 2: "TAT_ERR_UNSUPPORTED_GE
 EXPORTS = ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
            "tat_adjoint_host", "tat_plan_destroy", "tat_plan_info", "tat_plan_derive",
            "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
-           "tat_transpose", "tat_forward_scaled",
+           "tat_transpose", "tat_forward_scaled", "tat_inverse",
            "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm",
            "tat_status_string", "tat_last_error")
 
@@ -79,6 +79,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.tat_profile_end.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ip, ip]
     f32 = ctypes.c_float
     lib.tat_transpose.argtypes = [vp, vp, vp, vp]
+    lib.tat_inverse.argtypes = [vp, vp, vp, d, vp]
     lib.tat_forward_scaled.argtypes = [vp, vp, vp, f32, vp]
     lib.tat_residual.argtypes = [vp, vp, vp, vp, vp]
     lib.tat_adjoint_step.argtypes = [vp, vp, vp, f32, i, vp, vp]
@@ -91,7 +92,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
                  "tat_adjoint_host", "tat_plan_info", "tat_plan_derive",
                  "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
-                 "tat_transpose", "tat_forward_scaled",
+                 "tat_transpose", "tat_forward_scaled", "tat_inverse",
                  "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -221,6 +222,17 @@ class Plan:
                                             ctypes.c_void_p(g.data_ptr()), float(alpha),
                                             self._stream(stream)))
         return g
+
+    def inverse(self, g, r0: float = 0.95, out=None, stream=None):
+        """f = A^{-1} g (Algorithm 3, approximate universal backprojection), support |x| <= r0."""
+        import torch
+        self._chk(g, (self.batch, self.n_t, self.n_det), "g")
+        f = out if out is not None else torch.empty((self.batch, self.n, self.n),
+                                                    device=g.device, dtype=torch.float32)
+        self._chk(f, (self.batch, self.n, self.n), "f")
+        _check(self._lib.tat_inverse(self._h, ctypes.c_void_p(g.data_ptr()),
+                                     ctypes.c_void_p(f.data_ptr()), float(r0), self._stream(stream)))
+        return f
 
     def A(self, f):
         """Differentiable A (torch.autograd): backward = A^T."""
