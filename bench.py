@@ -349,6 +349,22 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     e2e_value = world * B * e2e_steps / (e2e_ms / 1000.0)
 
     lw = landweber(plan, f, f_host, geo, name, dev, stream) if not args.no_loop else None
+    inv = None
+    if not args.no_loop:   # A^{-1} (Algorithm 3) over the batch, tables built before timing
+        try:
+            plan.inverse(g, 0.95, out=u)
+            torch.cuda.synchronize()
+            i0 = torch.cuda.Event(enable_timing=True)
+            i1 = torch.cuda.Event(enable_timing=True)
+            i0.record(stream)
+            for _ in range(3):
+                plan.inverse(g, 0.95, out=u)
+            i1.record(stream)
+            torch.cuda.synchronize()
+            inv_ms = i0.elapsed_time(i1) / 3
+            inv = {"ms_per_call": inv_ms, "images_per_s": B / (inv_ms / 1000.0), "r0": 0.95}
+        except Exception as exc:   # geometry outside the inverse's support
+            inv = {"unavailable": str(exc)}
 
     if rank != 0:
         return 0
@@ -399,6 +415,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         "gpu_launches": (info["launches_forward"] + info["launches_adjoint"]) * args.steps,
         "clocks": clocks,
         "landweber": lw,
+        "inverse": inv,
         "paper_context": "A alone: 0.0055 s at 257^2, 360x513, batch 1 on an Nvidia A2000 "
                          "(PAPER.md L822-825); not this workload",
     }
