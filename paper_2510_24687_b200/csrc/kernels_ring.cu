@@ -136,6 +136,13 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
       }
     }
   }
+  int perm[NOUT];   // output node positions, loaded before the transform (latency hidden)
+#pragma unroll
+  for (int u = 0; u < NOUT; ++u) {
+    const int idx = threadIdx.x + u * T;
+    const int jj = idx / half, lp = idx - jj * half, j = j0 + jj;
+    perm[u] = j < NL ? __ldg(&P.node_perm[(size_t)j * half + lp]) : 0;
+  }
   const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
   float2* S2 = P.S2 + (size_t)b * half * NL;
 #pragma unroll
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
       const float2 zh = X[gg * rs + phys((l + half) & (nf - 1))];
       const float2 Pv = (jj & 1) ? make_float2(0.5f * (z.y + zh.y), -0.5f * (z.x - zh.x))
                                  : make_float2(0.5f * (z.x + zh.x), 0.5f * (z.y - zh.y));
-      S2[__ldg(&P.node_perm[(size_t)j * half + lp])] = Pv;   // adjoint S2: node order
+      S2[perm[u]] = Pv;   // adjoint S2: node order
     }
   }
 }
@@ -195,11 +202,18 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
   }
   const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
   const int tt_n = min(2 * G, n_t - t0);
-  for (int idx = threadIdx.x; idx < tt_n * n_det; idx += blockDim.x) {
-    const int tt = idx / n_det, d = idx - tt * n_det;
-    const float2 z = X[(tt >> 1) * rs + phys(__ldg(&P.ring[d]))];
-    const size_t i = ((size_t)b * n_t + t0 + tt) * n_det + d;
-    gout[i] = epi_fwd(P, i, (tt & 1) ? z.y : z.x);
+  // detector-major loop (no integer division): thread d restricts all 2G samples of detector d
+  for (int d = threadIdx.x; d < n_det; d += blockDim.x) {
+    const int pos = phys(__ldg(&P.ring[d]));
+    const size_t i0 = ((size_t)b * n_t + t0) * n_det + d;
+#pragma unroll
+    for (int tt = 0; tt < 2 * G; ++tt) {
+      if (tt < tt_n) {
+        const float2 z = X[(tt >> 1) * rs + pos];
+        const size_t i = i0 + (size_t)tt * n_det;
+        gout[i] = epi_fwd(P, i, (tt & 1) ? z.y : z.x);
+      }
+    }
   }
 }
 
@@ -210,7 +224,6 @@ __global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restri
   constexpr int G = ring_G<nf>();
   constexpr int rs = rstride(nf);
   constexpr int T = G * nf / 8, Kp = nf / 2 + 1;
-  constexpr int NIN = 16;                     // >= 2G n_det / T for n_det <= nf
   constexpr int NOUT = (Kp * G + T - 1) / T;  // <= 5
   const Consts& C = P.C;
   const int n_t = C.n_t, n_det = C.n_det;
@@ -218,26 +231,19 @@ __global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restri
   float2* A = sm;
   float2* B = sm + G * rs;
   const int tt_n = min(2 * G, n_t - t0);
-  const int tot = tt_n * n_det;
-  float gv[NIN];
-  int gp[NIN];
-#pragma unroll
-  for (int u = 0; u < NIN; ++u) {
-    const int idx = threadIdx.x + u * T;
-    gv[u] = 0.f;
-    gp[u] = -1;
-    if (idx < tot) {
-      const int tt = idx / n_det, d = idx - tt * n_det;
-      gv[u] = gin[((size_t)b * n_t + t0 + tt) * n_det + d];
-      gp[u] = 2 * ((tt >> 1) * rs + phys(__ldg(&P.ring[d]))) + (tt & 1);
-    }
-  }
   for (int i = threadIdx.x; i < G * rs; i += blockDim.x) A[i] = make_float2(0.f, 0.f);
   __syncthreads();
   float* Af = reinterpret_cast<float*>(A);
+  // detector-major (no integer division): thread d places the 2G samples of detector d
+  for (int d = threadIdx.x; d < n_det; d += blockDim.x) {
+    const int pos = 2 * phys(__ldg(&P.ring[d]));
+    const float* gi = gin + ((size_t)b * n_t + t0) * n_det + d;
+    float gv[2 * G];
 #pragma unroll
-  for (int u = 0; u < NIN; ++u)
-    if (gp[u] >= 0) Af[gp[u]] = gv[u];
+    for (int tt = 0; tt < 2 * G; ++tt) gv[tt] = tt < tt_n ? gi[(size_t)tt * n_det] : 0.f;
+#pragma unroll
+    for (int tt = 0; tt < 2 * G; ++tt) Af[2 * (tt >> 1) * rs + pos + (tt & 1)] = gv[tt];
+  }
   const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
   float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
 #pragma unroll
