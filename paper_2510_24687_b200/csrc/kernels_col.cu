@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(128, 3) k2c_adj(DevPlan P) {
 // for p in [0, N/2].  One CTA (128 threads) per two row pairs (rows y0..y0+3); the [p][4 y]
 // output tiles are transposed into S1 by TMA tensor stores (32-byte rows per p).
 constexpr int kK1BoxP = 128;   // p extent of one S1 tile (= C.s1boxP on this path)
+constexpr int kK1TSlots = 8;   // K1T: S~1 tiles in flight (TMA loads issued ahead)
 
 template <int n>
 __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_constant__ CUtensorMap tm,
@@ -402,13 +403,12 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
   float2* W0 = sm;
   float2* W1 = sm + G::Q0 * G::J;
   float2* stg = sm + 2 * G::Q0 * G::J;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 2 * kK1BoxP * 4);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + kK1TSlots * kK1BoxP * 4);
   const int nch = (C.ncols + kK1BoxP - 1) / kK1BoxP;
   if (t == 0) {
-    ac::mbar_init(&bar[0], 1);
-    ac::mbar_init(&bar[1], 1);
+    for (int q = 0; q < kK1TSlots; ++q) ac::mbar_init(&bar[q], 1);
     ac::fence_mbar_init();
-    for (int c = 0; c < 2 && c < nch; ++c) {
+    for (int c = 0; c < kK1TSlots && c < nch; ++c) {
       ac::mbar_expect_tx(&bar[c], kK1BoxP * 32);
       ac::tma_load_3d(stg + c * kK1BoxP * 4, &tm, y0, c * kK1BoxP, b, &bar[c]);
     }
@@ -418,8 +418,8 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   __syncthreads();
   for (int c = 0; c < nch; ++c) {
-    const int slot = c & 1;
-    ac::mbar_wait(&bar[slot], (c >> 1) & 1);
+    const int slot = c % kK1TSlots;
+    ac::mbar_wait(&bar[slot], (c / kK1TSlots) & 1);
     const float4* tile = reinterpret_cast<const float4*>(stg + slot * kK1BoxP * 4);
     const int p = c * kK1BoxP + t;
     if (p < C.ncols) {
@@ -437,10 +437,10 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
       }
     }
     __syncthreads();   // tile consumed
-    if (t == 0 && c + 2 < nch) {
+    if (t == 0 && c + kK1TSlots < nch) {
       ac::fence_proxy_async();
       ac::mbar_expect_tx(&bar[slot], kK1BoxP * 32);
-      ac::tma_load_3d(stg + slot * kK1BoxP * 4, &tm, y0, (c + 2) * kK1BoxP, b, &bar[slot]);
+      ac::tma_load_3d(stg + slot * kK1BoxP * 4, &tm, y0, (c + kK1TSlots) * kK1BoxP, b, &bar[slot]);
     }
   }
   stage_b<G, 1>(W0, t);
@@ -625,6 +625,9 @@ size_t smem_k2c_adj(const Consts& C) {
 }
 
 size_t smem_k1c(const Consts& C) { return (size_t)2 * 128 * (C.n / 16) * 8 + 2 * kK1BoxP * 32 + 64; }
+size_t smem_k1c_adj(const Consts& C) {
+  return (size_t)2 * 128 * (C.n / 16) * 8 + (size_t)kK1TSlots * kK1BoxP * 32 + 128;
+}
 
 template <int n>
 static cudaError_t cfg_col() {
@@ -673,8 +676,8 @@ cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float*
 cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s) {
   const Consts& C = P.C;
   const dim3 grid(C.n / 4, C.batch);
-  if (C.n == 512) k1c_adj<512><<<grid, 128, smem_k1c(C), s>>>(P, tm, f);
-  else k1c_adj<256><<<grid, 128, smem_k1c(C), s>>>(P, tm, f);
+  if (C.n == 512) k1c_adj<512><<<grid, 128, smem_k1c_adj(C), s>>>(P, tm, f);
+  else k1c_adj<256><<<grid, 128, smem_k1c_adj(C), s>>>(P, tm, f);
   return cudaGetLastError();
 }
 
