@@ -345,20 +345,29 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
   const int b = C.b0 + blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
   float2* W0 = sm;
   float2* W1 = sm + G::Q0 * G::J;
-  float2* stg = sm + 2 * G::Q0 * G::J;   // 2 tiles [kK1BoxP][4]
+  float2* stg = sm + 2 * G::Q0 * G::J;   // 2 tiles [kK1BoxP][4]; first holds the 4 input rows
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 2 * kK1BoxP * 4);
+  const float* rows = reinterpret_cast<const float*>(stg);
+  if (t == 0) {   // the 4 rows y0..y0+3 are one contiguous 16n-byte range of f
+    ac::mbar_init(bar, 1);
+    ac::fence_mbar_init();
+    ac::mbar_expect_tx(bar, 16 * n);
+    ac::bulk_g2s(stg, f + ((size_t)b * n + y0) * n, 16 * n, bar);
+  }
   float2 A[G::NRES][16];
   Pow16<kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
-  const float* r0 = f + ((size_t)b * n + y0) * n;
+  __syncthreads();
+  ac::mbar_wait(bar, 0);
 #pragma unroll 1
   for (int pr = 0; pr < 2; ++pr) {
     float2 x[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r)
-      x[r] = make_float2(__ldg(&r0[(2 * pr) * n + j + G::J * r]), __ldg(&r0[(2 * pr + 1) * n + j + G::J * r]));
+      x[r] = make_float2(rows[(2 * pr) * n + j + G::J * r], rows[(2 * pr + 1) * n + j + G::J * r]);
     stage_a_fwd<G>(x, A, pw, pr ? W1 : W0, j, sg);
   }
-  __syncthreads();
+  __syncthreads();   // (also: every thread is done with the rows before stg is reused)
   stage_b<G, -1>(W0, t);
   stage_b<G, -1>(W1, t);
   __syncthreads();
