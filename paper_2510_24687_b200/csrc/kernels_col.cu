@@ -204,10 +204,6 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
       ac::mbar_expect_tx(&bar[slot ^ 1], n * 8);
       ac::bulk_g2s(xbuf + (slot ^ 1) * n, S1 + (size_t)(p + 1) * n, n * 8, &bar[slot ^ 1]);
     }
-    const int e0 = (p > P0) ? __ldg(&P.k2_colptr[p - 1]) : 0;
-    const int e1 = (p > P0) ? __ldg(&P.k2_colptr[p]) : 0;
-    int4 nd0 = make_int4(0, 0, 0, 0);
-    if (e0 + t < e1) nd0 = __ldg(&P.k2_nodes[e0 + t]);
     ac::mbar_wait(&bar[slot], (it >> 1) & 1);
     {   // stage A
       const float2* xs = xbuf + slot * n;
@@ -216,6 +212,12 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
       for (int r = 0; r < R; ++r) x[r] = xs[j + J * r];
       stage_a_fwd<G>(x, A, pw, Fcur, j, sg);
     }
+    // first node record of this column's gather, loaded while stage B runs (after stage A, whose
+    // registers are dead by then)
+    const int e0 = (p > P0) ? __ldg(&P.k2_colptr[p - 1]) : 0;
+    const int e1 = (p > P0) ? __ldg(&P.k2_colptr[p]) : 0;
+    int4 nd0 = make_int4(0, 0, 0, 0);
+    if (e0 + t < e1) nd0 = __ldg(&P.k2_nodes[e0 + t]);
     __syncthreads();
     stage_b<G, -1>(Fcur, t);   // stage B (in place)
     __syncthreads();
