@@ -498,7 +498,9 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
   const float2* in_all = ADJ ? P.S4 : P.S3;
   float2* W = sm + e * N4;
   float2* ibuf = sm + 3 * N4;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ibuf + 2 * IB);
+  const int U = ADJ ? NL : n_t + 1;               // output twiddle index range u in [0, U)
+  float4* tws = reinterpret_cast<float4*>(ibuf + 2 * IB);   // (W^u, W^{2u}), W = W_2M
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tws + U);
   const long rbase = (long)C.b0 * C.Kp;   // global row of local row 0
   auto issue = [&](int r, int slot) {   // thread 0: row r -> ibuf[slot] (16-B aligned range)
     const long s0 = ((rbase + r) * cnt) & ~1L, s1 = ((rbase + r) * cnt + cnt + 1) & ~1L;
@@ -514,6 +516,11 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
   float2 A[G::NRES][16];
   Pow16<kFactPow> pw;
   col_twiddles<G>(P.tw_dct4, P.tw_n, 0, j, sg, A, pw);
+  for (int u = t; u < U; u += blockDim.x) {   // output twiddles, once per CTA
+    const int u2 = 2 * u >= M2 ? 2 * u - M2 : 2 * u;
+    const float2 a = __ldg(&P.tw_dct[u]), c = __ldg(&P.tw_dct[u2]);
+    tws[u] = make_float4(a.x, a.y, c.x, c.y);
+  }
   __syncthreads();
   int it = 0;
   for (int row = blockIdx.x; row < rows; row += gridDim.x, ++it) {
@@ -554,25 +561,25 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
       const float2 c2 = ce::cadd(cmul(sm[2 * N4 + vp], w2), cmulc(sm[2 * N4 + vm], w2));
       return ce::cadd(a, ce::cadd(c1, c2));
     };
-    constexpr int U = 4;
+    constexpr int U4 = 4;
     const int nout = ADJ ? NL : n_t;
     const float2 hJ = (!ADJ && NL == 3 * n + 1) ? in[3 * n] : make_float2(0.f, 0.f);
     const float om = (float)C.omega;
     float2* out = ADJ ? P.S3 + (size_t)(rbase + row) * NL : P.S4 + (size_t)(rbase + row) * n_t;
-    for (int o0 = t; o0 < nout; o0 += U * (int)blockDim.x) {
-      float2 w1[U], w2[U];
-      float ml[U];
+    for (int o0 = t; o0 < nout; o0 += U4 * (int)blockDim.x) {
+      float2 w1[U4], w2[U4];
+      float ml[U4];
 #pragma unroll
-      for (int q = 0; q < U; ++q) {
+      for (int q = 0; q < U4; ++q) {
         const int o = o0 + q * blockDim.x;
         const int u = ADJ ? o : o + 1;
-        const int u2 = 2 * u >= M2 ? 2 * u - M2 : 2 * u;
-        w1[q] = o < nout ? __ldg(&P.tw_dct[u]) : make_float2(0.f, 0.f);
-        w2[q] = o < nout ? __ldg(&P.tw_dct[u2]) : make_float2(0.f, 0.f);
+        const float4 tw = o < nout ? tws[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+        w1[q] = make_float2(tw.x, tw.y);
+        w2[q] = make_float2(tw.z, tw.w);
         ml[q] = (ADJ && o < nout) ? __ldg(&P.mult[(size_t)k * NL + o]) : 0.f;
       }
 #pragma unroll
-      for (int q = 0; q < U; ++q) {
+      for (int q = 0; q < U4; ++q) {
         const int o = o0 + q * blockDim.x;
         if (o >= nout) break;
         const int u = ADJ ? o : o + 1;
@@ -606,7 +613,8 @@ bool dct4_ok(const Consts& C) {
 }
 size_t smem_k4c(const Consts& C) {
   const int cnt = std::max(C.NL, C.n_t);
-  return (size_t)3 * 4 * C.n * 8 + (size_t)2 * ((cnt + 3) & ~1) * 8 + 64;
+  return (size_t)3 * 4 * C.n * 8 + (size_t)2 * ((cnt + 3) & ~1) * 8 +
+         (size_t)std::max(C.NL, C.n_t + 1) * 16 + 64;
 }
 
 cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s) {
