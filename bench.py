@@ -214,6 +214,27 @@ def run_reference(args, rank: int, world: int):
     return 0
 
 
+# ----------------------------------------------------------------------------- multi-GPU host logic
+def rank_images(name: str, rank: int) -> np.ndarray:
+    """The batch of rank `rank` (replicas): images rank*B .. rank*B + B - 1 of
+    the workload's seeded phantom family, so every rank processes distinct images."""
+    B = synth.geometry(name).batch
+    return np.stack([synth.phantom(name, rank * B + b) for b in range(B)]).astype(np.float32)
+
+
+def reduce_timing(total_ms: float, units: float, world: int, device=None):
+    """(max over ranks of the timed region in ms, sum over ranks of the units processed)."""
+    if world <= 1:
+        return total_ms, units
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+    u = torch.tensor([units], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def landweber(plan, f, f_host, geo, name, dev, stream, iters: int = 50, reps: int = 3):
     """BASELINE configs[2] workload: projected-Landweber / NNLS (§4.2) on
@@ -269,7 +290,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     B = geo.batch
     plan = Plan(geo.n, geo.n_det, geo.n_t, geo.R, geo.c, geo.T, B, geo.angles_array())
     info = plan.info
-    f_host = synth.phantom_batch(name)                      # identical batch on every rank
+    f_host = rank_images(name, rank)                        # distinct images per rank
     f = torch.from_numpy(f_host).to(dev)
     g = torch.empty((B, geo.n_t, geo.n_det), device=dev)
     u = torch.empty((B, geo.n, geo.n), device=dev)
@@ -312,13 +333,9 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     stage_ms, nf, na = plan.profile_end()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms, units = reduce_timing(sum(step_ms), B * args.steps, world, dev)
     ms_per_step = total_ms / args.steps
-    value = world * B * args.steps / (total_ms / 1000.0)
+    value = units / (total_ms / 1000.0)
 
     # ---- end to end: pinned H2D of f, A, A*, D2H of the result, every step
     f_pin = torch.from_numpy(f_host).pin_memory()
@@ -341,12 +358,8 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         u_pin.copy_(u, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = world * B * e2e_steps / (e2e_ms / 1000.0)
+    e2e_ms, e2e_units = reduce_timing(e0.elapsed_time(e1), B * e2e_steps, world, dev)
+    e2e_value = e2e_units / (e2e_ms / 1000.0)
 
     lw = landweber(plan, f, f_host, geo, name, dev, stream) if not args.no_loop else None
     inv = None
