@@ -185,3 +185,33 @@ def test_parity_full_size(torch_cuda, name, images):
     for b in images:
         ref = O.adjoint(g_gpu[b].astype(np.float64), C)
         _check(u_gpu[b], ref, f"{name} A* image {b}")
+
+
+def test_parity_mixed_engines_and_arc_at_n256(torch_cuda):
+    """n = 256 runs the two-stage K1/K2/K2T/K1T; n_t = n gives 2M = 6n, which runs the
+    first-generation DCT kernels (r = 3); a 3/4 arc of the ring and an odd batch of 3."""
+    n, n_det, n_t = 256, 192, 256
+    geo = synth.Geometry(n, n_det, n_t, batch=3, angles=synth.ring_angles(n_det, 256, 224))
+    from paper_2510_24687_b200 import derive
+    info, _, st = derive(n, n_det, n_t, 1.0, 1.0, 2.0, 3, geo.angles_array())
+    assert st == 0, "geometry must be supported"
+    C = O.derive_geom(geo)
+    plan = _plan(geo)
+    f = np.stack([synth.phantom("C2", b, n=n) for b in range(3)])
+    g_gpu = _run(torch_cuda, plan, f=f)
+    for b in range(3):
+        _check(g_gpu[b], O.forward(f[b].astype(np.float64), C), f"n256 arc A {b}")
+    gr = np.stack([synth.random_data(n_t, n_det, 70 + b) for b in range(3)])
+    u_gpu = _run(torch_cuda, plan, g=gr)
+    for b in range(3):
+        _check(u_gpu[b], O.adjoint(gr[b].astype(np.float64), C), f"n256 arc A* {b}")
+
+
+def test_nan_propagates(torch_cuda):
+    """NaN/Inf in the input propagate to the output (include/tat.h: no scan pass)."""
+    geo = synth.geometry("C2")
+    plan = _plan(geo, batch=1)
+    f = synth.phantom("C2")[None].copy()
+    f[0, geo.n // 2, geo.n // 3] = np.nan
+    g = _run(torch_cuda, plan, f=f)
+    assert np.isnan(g).any()
