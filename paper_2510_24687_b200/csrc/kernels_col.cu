@@ -187,6 +187,8 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float2* S1 = P.S1 + (size_t)b * C.ncols * n;
   float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
+  pdl_wait();
+  pdl_trigger();
   if (t == 0) {
     ac::mbar_init(&bar[0], 1);
     ac::mbar_init(&bar[1], 1);
@@ -284,6 +286,8 @@ __global__ void __launch_bounds__(128, 3) k2c_adj(DevPlan P) {
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ac::smem_u32(&bar[slot])) : "memory");
     }
   };
+  pdl_wait();
+  pdl_trigger();
   if (t == 0) {
     ac::mbar_init(&bar[0], 1);
     ac::mbar_init(&bar[1], 1);
@@ -350,15 +354,17 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
   float2* stg = sm + 2 * G::Q0 * G::J;   // 2 tiles [kK1BoxP][4]; first holds the 4 input rows
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 2 * kK1BoxP * 4);
   const float* rows = reinterpret_cast<const float*>(stg);
+  float2 A[G::NRES][16];
+  Pow16<kFactPow> pw;
+  col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
+  pdl_wait();
+  pdl_trigger();
   if (t == 0) {   // the 4 rows y0..y0+3 are one contiguous 16n-byte range of f
     ac::mbar_init(bar, 1);
     ac::fence_mbar_init();
     ac::mbar_expect_tx(bar, 16 * n);
     ac::bulk_g2s(stg, f + ((size_t)b * n + y0) * n, 16 * n, bar);
   }
-  float2 A[G::NRES][16];
-  Pow16<kFactPow> pw;
-  col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   __syncthreads();
   ac::mbar_wait(bar, 0);
 #pragma unroll 1
@@ -415,6 +421,11 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
   float2* W1 = sm + G::Q0 * G::J;
   float2* stg = sm + 2 * G::Q0 * G::J;
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + kK1TSlots * kK1BoxP * 4);
+  float2 A[G::NRES][16];
+  Pow16<kFactPow> pw;
+  col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
+  pdl_wait();
+  pdl_trigger();
   const int nch = (C.ncols + kK1BoxP - 1) / kK1BoxP;
   if (t == 0) {
     for (int q = 0; q < kK1TSlots; ++q) ac::mbar_init(&bar[q], 1);
@@ -424,9 +435,6 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
       ac::tma_load_3d(stg + c * kK1BoxP * 4, &tm, y0, c * kK1BoxP, b, &bar[c]);
     }
   }
-  float2 A[G::NRES][16];
-  Pow16<kFactPow> pw;
-  col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   __syncthreads();
   for (int c = 0; c < nch; ++c) {
     const int slot = c % kK1TSlots;
@@ -507,12 +515,6 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
     ac::mbar_expect_tx(&bar[slot], (uint32_t)(s1 - s0) * 8);
     ac::bulk_g2s(ibuf + slot * IB, in_all + s0, (uint32_t)(s1 - s0) * 8, &bar[slot]);
   };
-  if (t == 0) {
-    ac::mbar_init(&bar[0], 1);
-    ac::mbar_init(&bar[1], 1);
-    ac::fence_mbar_init();
-    if ((int)blockIdx.x < rows) issue(blockIdx.x, 0);
-  }
   float2 A[G::NRES][16];
   Pow16<kFactPow> pw;
   col_twiddles<G>(P.tw_dct4, P.tw_n, 0, j, sg, A, pw);
@@ -520,6 +522,14 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
     const int u2 = 2 * u >= M2 ? 2 * u - M2 : 2 * u;
     const float2 a = __ldg(&P.tw_dct[u]), c = __ldg(&P.tw_dct[u2]);
     tws[u] = make_float4(a.x, a.y, c.x, c.y);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (t == 0) {
+    ac::mbar_init(&bar[0], 1);
+    ac::mbar_init(&bar[1], 1);
+    ac::fence_mbar_init();
+    if ((int)blockIdx.x < rows) issue(blockIdx.x, 0);
   }
   __syncthreads();
   int it = 0;
@@ -619,17 +629,18 @@ size_t smem_k4c(const Consts& C) {
 
 cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s) {
   const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
   const int rows = C.Kp * C.batch;
   const dim3 grid(std::min(rows, 2 * 148));
   const size_t sm = smem_k4c(C);
   if (C.n == 512) {
-    if (adj) k4c_dct<512, true><<<grid, 192, sm, s>>>(P);
-    else k4c_dct<512, false><<<grid, 192, sm, s>>>(P);
+    if (adj) e = launch_pdl(C.pdl, k4c_dct<512, true>, grid, dim3(192), sm, s, P);
+    else e = launch_pdl(C.pdl, k4c_dct<512, false>, grid, dim3(192), sm, s, P);
   } else {
-    if (adj) k4c_dct<256, true><<<grid, 192, sm, s>>>(P);
-    else k4c_dct<256, false><<<grid, 192, sm, s>>>(P);
+    if (adj) e = launch_pdl(C.pdl, k4c_dct<256, true>, grid, dim3(192), sm, s, P);
+    else e = launch_pdl(C.pdl, k4c_dct<256, false>, grid, dim3(192), sm, s, P);
   }
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 bool col_ok(const Consts& C) { return C.Lres == 8 && (C.n == 256 || C.n == 512); }
@@ -670,34 +681,38 @@ cudaError_t configure_col_kernels(const Consts& C) {
 
 cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
   const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
-  if (C.n == 512) k2c_fwd<512><<<grid, 128, smem_k2c_fwd(C), s>>>(P);
-  else k2c_fwd<256><<<grid, 128, smem_k2c_fwd(C), s>>>(P);
-  return cudaGetLastError();
+  if (C.n == 512) e = launch_pdl(C.pdl, k2c_fwd<512>, grid, dim3(128), smem_k2c_fwd(C), s, P);
+  else e = launch_pdl(C.pdl, k2c_fwd<256>, grid, dim3(128), smem_k2c_fwd(C), s, P);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
   const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
-  if (C.n == 512) k2c_adj<512><<<grid, 128, smem_k2c_adj(C), s>>>(P);
-  else k2c_adj<256><<<grid, 128, smem_k2c_adj(C), s>>>(P);
-  return cudaGetLastError();
+  if (C.n == 512) e = launch_pdl(C.pdl, k2c_adj<512>, grid, dim3(128), smem_k2c_adj(C), s, P);
+  else e = launch_pdl(C.pdl, k2c_adj<256>, grid, dim3(128), smem_k2c_adj(C), s, P);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s) {
   const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
   const dim3 grid(C.n / 4, C.batch);
-  if (C.n == 512) k1c_fwd<512><<<grid, 128, smem_k1c(C), s>>>(P, tm, f);
-  else k1c_fwd<256><<<grid, 128, smem_k1c(C), s>>>(P, tm, f);
-  return cudaGetLastError();
+  if (C.n == 512) e = launch_pdl(C.pdl, k1c_fwd<512>, grid, dim3(128), smem_k1c(C), s, P, tm, f);
+  else e = launch_pdl(C.pdl, k1c_fwd<256>, grid, dim3(128), smem_k1c(C), s, P, tm, f);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s) {
   const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
   const dim3 grid(C.n / 4, C.batch);
-  if (C.n == 512) k1c_adj<512><<<grid, 128, smem_k1c_adj(C), s>>>(P, tm, f);
-  else k1c_adj<256><<<grid, 128, smem_k1c_adj(C), s>>>(P, tm, f);
-  return cudaGetLastError();
+  if (C.n == 512) e = launch_pdl(C.pdl, k1c_adj<512>, grid, dim3(128), smem_k1c_adj(C), s, P, tm, f);
+  else e = launch_pdl(C.pdl, k1c_adj<256>, grid, dim3(128), smem_k1c_adj(C), s, P, tm, f);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace tat

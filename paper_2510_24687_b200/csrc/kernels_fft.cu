@@ -285,6 +285,8 @@ __global__ void __launch_bounds__(kSumThreads) k2t_sum(DevPlan P) {
     rec[k] = (t < tb) ? __ldg(&P.k2t_rec[t]) : make_int4(0, 0, 0, 0);
   }
   const float2* S2 = P.S2 + (size_t)b * C.half * C.NL + n0;
+  pdl_wait();
+  pdl_trigger();
   for (int i = tid; i < nw; i += kSumThreads) win[i] = __ldg(&S2[i]);
   __syncthreads();
   float2* Rc = P.Rc + (size_t)b * C.ntpad;
@@ -299,8 +301,9 @@ __global__ void __launch_bounds__(kSumThreads) k2t_sum(DevPlan P) {
 
 static cudaError_t launch_k2t_sum(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
-  k2t_sum<<<dim3(C.ncols, C.batch), kSumThreads, (size_t)C.k2t_win * sizeof(float2), s>>>(P);
-  return cudaGetLastError();
+  const cudaError_t e = launch_pdl(C.pdl, k2t_sum, dim3(C.ncols, C.batch), dim3(kSumThreads),
+                                   (size_t)C.k2t_win * sizeof(float2), s, P);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // ================================================================== K2Tb (transpose of K2)

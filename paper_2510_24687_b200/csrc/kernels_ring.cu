@@ -53,6 +53,15 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S2 = P.S2 + (size_t)b * half * NL;
+  float mo[NOUT];   // multiplier values of the output phase, loaded early
+#pragma unroll
+  for (int u = 0; u < NOUT; ++u) {
+    const int idx = threadIdx.x + u * T;
+    const int k = idx / (2 * G), j = j0 + (idx - k * (2 * G));
+    mo[u] = (idx < Kp * 2 * G && j < NL) ? __ldg(&P.mult[(size_t)k * NL + j]) : 0.f;
+  }
+  pdl_wait();
+  pdl_trigger();
   float2 va[NIN], vb[NIN];
 #pragma unroll
   for (int u = 0; u < NIN; ++u) {
@@ -61,13 +70,6 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
     const int ja = j0 + 2 * gg;
     va[u] = ja < NL ? S2[(size_t)ja * half + lp] : make_float2(0.f, 0.f);
     vb[u] = ja + 1 < NL ? S2[(size_t)(ja + 1) * half + lp] : make_float2(0.f, 0.f);
-  }
-  float mo[NOUT];   // multiplier values of the output phase, loaded early
-#pragma unroll
-  for (int u = 0; u < NOUT; ++u) {
-    const int idx = threadIdx.x + u * T;
-    const int k = idx / (2 * G), j = j0 + (idx - k * (2 * G));
-    mo[u] = (idx < Kp * 2 * G && j < NL) ? __ldg(&P.mult[(size_t)k * NL + j]) : 0.f;
   }
 #pragma unroll
   for (int u = 0; u < NIN; ++u) {
@@ -114,6 +116,8 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
+  pdl_wait();
+  pdl_trigger();
   float2 e1[NIN], e2[NIN];
 #pragma unroll
   for (int u = 0; u < NIN; ++u) {
@@ -176,6 +180,8 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
+  pdl_wait();
+  pdl_trigger();
   float2 w0[NIN], w1[NIN];
 #pragma unroll
   for (int u = 0; u < NIN; ++u) {
@@ -232,6 +238,8 @@ __global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restri
   float2* B = sm + G * rs;
   const int tt_n = min(2 * G, n_t - t0);
   for (int i = threadIdx.x; i < G * rs; i += blockDim.x) A[i] = make_float2(0.f, 0.f);
+  pdl_wait();
+  pdl_trigger();
   __syncthreads();
   float* Af = reinterpret_cast<float*>(A);
   // detector-major (no integer division): thread d places the 2G samples of detector d
@@ -299,39 +307,43 @@ cudaError_t configure_ring_kernels(const Consts& C) {
 
 cudaError_t launch_k3(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
-    k3_ring<NF><<<dim3((C.NL + 2 * G - 1) / (2 * G), C.batch), G * NF / 8, sm, s>>>(P);
+    e = launch_pdl(C.pdl, k3_ring<NF>, dim3((C.NL + 2 * G - 1) / (2 * G), C.batch), dim3(G * NF / 8), sm, s, P);
   });
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 cudaError_t launch_k3t(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
-    k3t_ring<NF><<<dim3((C.NL + 2 * G - 1) / (2 * G), C.batch), G * NF / 8, sm, s>>>(P);
+    e = launch_pdl(C.pdl, k3t_ring<NF>, dim3((C.NL + 2 * G - 1) / (2 * G), C.batch), dim3(G * NF / 8), sm, s, P);
   });
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 cudaError_t launch_k5(const DevPlan& P, float* g, cudaStream_t s) {
   const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
-    k5_ring<NF><<<dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), G * NF / 8, sm, s>>>(P, g);
+    e = launch_pdl(C.pdl, k5_ring<NF>, dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), dim3(G * NF / 8), sm, s, P, g);
   });
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 cudaError_t launch_k5t(const DevPlan& P, const float* g, cudaStream_t s) {
   const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
-    k5t_ring<NF><<<dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), G * NF / 8, sm, s>>>(P, g);
+    e = launch_pdl(C.pdl, k5t_ring<NF>, dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), dim3(G * NF / 8), sm, s, P, g);
   });
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace tat

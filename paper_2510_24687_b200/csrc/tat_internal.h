@@ -15,6 +15,7 @@ struct Consts {
   int n = 0, n_det = 0, n_t = 0, batch = 0;
   int b0 = 0;       // first image of a launch (sub-batch pipelining); batch = images in it
   int dct_sine = 0; // K4T computes sum_m G~ sin(c lambda_j t_m) (the inverse, Alg. 3 step 3)
+  int pdl = 1;      // launch the chain kernels with programmatic dependent launch
   double R = 1, c = 1, T = 1;
   double h = 0, T_new0 = 0, T_new = 0, Lbox = 0, dxi = 0, dt = 0, dlam = 0, lam_max = 0;
   double wJ = 1, omega = 0;
@@ -111,6 +112,29 @@ struct DevPlan {
 };
 
 #ifdef __CUDACC__
+// Programmatic dependent launch (sm_90+): a kernel launched with the PDL attribute may start
+// while its predecessor in the stream drains; everything before pdl_wait() (plan-table loads,
+// shared-memory and barrier setup) overlaps the predecessor's tail, and pdl_wait() blocks until
+// the predecessor has completed and its memory is visible.  Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // forward epilogue: value at flat output index i of g
 __device__ __forceinline__ float epi_fwd(const DevPlan& P, size_t i, float v) {
   v *= P.epi_scale;
