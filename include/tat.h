@@ -28,6 +28,10 @@
  * Errors: arguments are validated on the host before any launch; a failed call writes
  * nothing.  The thread-local message of the last failure is tat_last_error().
  * NaN/Inf in f or g propagate (no scan pass).
+ *
+ * Kernels of a call are launched with programmatic dependent launch (each kernel's table loads
+ * overlap its predecessor's tail); the environment variable TAT_PDL=0, read at plan creation,
+ * disables it (debugging).
  */
 #ifndef TAT_H
 #define TAT_H

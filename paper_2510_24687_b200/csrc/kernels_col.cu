@@ -26,7 +26,6 @@ namespace tat {
 
 namespace {
 
-constexpr int kStripC = 16;   // columns per CTA (k2c_fwd recomputes one halo column)
 #ifndef TAT_FACT_POW
 #define TAT_FACT_POW 1
 #endif
@@ -175,8 +174,8 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
   const int N1 = C.N - 1;
   const int t = threadIdx.x, j = t % J, sg = t / J;
   const int b = C.b0 + blockIdx.y;
-  const int P0 = blockIdx.x * kStripC;
-  const int Pend = min(P0 + kStripC, C.ncols);
+  const int P0 = blockIdx.x * C.col_strip;
+  const int Pend = min(P0 + C.col_strip, C.ncols);
   const int plast = min(Pend, C.ncols - 1);
   float2* Fa = sm;
   float2* Fb = sm + G::Q0 * J;
@@ -265,8 +264,8 @@ __global__ void __launch_bounds__(128, 3) k2c_adj(DevPlan P) {
   const Consts& C = P.C;
   const int t = threadIdx.x, j = t % J, sg = t / J;
   const int b = C.b0 + blockIdx.y;
-  const int P0 = blockIdx.x * kStripC;
-  const int Pend = min(P0 + kStripC, C.ncols);
+  const int P0 = blockIdx.x * C.col_strip;
+  const int Pend = min(P0 + C.col_strip, C.ncols);
   const int RB = C.k2c_rbuf;                                  // entries per target buffer
   float2* Wb = sm;
   float2* rbuf = sm + Q0 * J;
@@ -682,7 +681,7 @@ cudaError_t configure_col_kernels(const Consts& C) {
 cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
-  const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
+  const dim3 grid((C.ncols + C.col_strip - 1) / C.col_strip, C.batch);
   if (C.n == 512) e = launch_pdl(C.pdl, k2c_fwd<512>, grid, dim3(128), smem_k2c_fwd(C), s, P);
   else e = launch_pdl(C.pdl, k2c_fwd<256>, grid, dim3(128), smem_k2c_fwd(C), s, P);
   return e != cudaSuccess ? e : cudaGetLastError();
@@ -691,7 +690,7 @@ cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s) {
 cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
-  const dim3 grid((C.ncols + kStripC - 1) / kStripC, C.batch);
+  const dim3 grid((C.ncols + C.col_strip - 1) / C.col_strip, C.batch);
   if (C.n == 512) e = launch_pdl(C.pdl, k2c_adj<512>, grid, dim3(128), smem_k2c_adj(C), s, P);
   else e = launch_pdl(C.pdl, k2c_adj<256>, grid, dim3(128), smem_k2c_adj(C), s, P);
   return e != cudaSuccess ? e : cudaGetLastError();

@@ -196,7 +196,7 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
       for (int q = 0; q < C.ncols; ++q)
         mw = std::max(mw, H.k2_colptr[q + 1] - H.k2_colptr[q > 0 ? q - 1 : 0]);
       P.C.k2t_win = std::max(mw, 1);
-      const char* pdl = getenv("TAT_PDL");
+      const char* pdl = getenv("TAT_PDL");   // debugging switch: TAT_PDL=0 disables PDL
       P.C.pdl = pdl ? atoi(pdl) : 1;
     }
     if ((size_t)P.C.k2t_win * 8 > 227 * 1024) {

@@ -16,6 +16,8 @@ struct Consts {
   int b0 = 0;       // first image of a launch (sub-batch pipelining); batch = images in it
   int dct_sine = 0; // K4T computes sum_m G~ sin(c lambda_j t_m) (the inverse, Alg. 3 step 3)
   int pdl = 1;      // launch the chain kernels with programmatic dependent launch
+  int col_strip = 16; // K2 / K2Tb: columns per CTA (k2c_fwd recomputes one halo column;
+                      // 12-16 measured best at C3, 20-32 slower)
   double R = 1, c = 1, T = 1;
   double h = 0, T_new0 = 0, T_new = 0, Lbox = 0, dxi = 0, dt = 0, dlam = 0, lam_max = 0;
   double wJ = 1, omega = 0;
