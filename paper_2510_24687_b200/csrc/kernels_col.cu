@@ -29,15 +29,18 @@ namespace {
 #ifndef TAT_FACT_POW
 #define TAT_FACT_POW 1
 #endif
-constexpr bool kFactPow = TAT_FACT_POW;   // K1/K1T/K4/K4T post-twiddle powers (Pow16)
+constexpr bool kFactPow = TAT_FACT_POW;   // post-twiddle powers of the stage-A jobs (PowR)
 
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+
+// R points per thread in stage A: 16 for n <= 512, 32 for n = 1024 (keeps J = n / R <= 32)
 template <int n_, int L_ = 8>
 struct ColGeo {
-  static constexpr int n = n_, L = L_, R = 16, J = n / R, Q0 = R * L, T = Q0;
+  static constexpr int n = n_, L = L_, R = (n_ >= 1024) ? 32 : 16, J = n / R, Q0 = R * L, T = Q0;
   static constexpr int NG = T / J;        // residue groups (threads sharing j)
   static constexpr int NRES = J * L / T;  // residues per thread in stage A
-  static constexpr int LGQ0 = (L == 8) ? 7 : 6;   // log2 Q0
-  static_assert(J >= R && J <= 32 && (L == 8 || L == 4), "n in {256, 512}, L in {4, 8}");
+  static constexpr int LGQ0 = ilog2c(Q0); // log2 Q0
+  static_assert(J >= R && J <= 32 && (L == 8 || L == 4), "n in {256, 512, 1024}, L in {4, 8}");
   // element (q0, c) of a column buffer [Q0][J]: XOR swizzle, conflict-free for both stages
   __device__ static __forceinline__ int widx(int q0, int c) { return q0 * J + (c ^ (q0 & (J - 1))); }
   __device__ static __forceinline__ int fq(int q) { return widx(q & (Q0 - 1), q >> LGQ0); }
@@ -50,25 +53,25 @@ using ce::cmulc;
 using ce::csub;
 
 // ------------------------------------------------------------------ post-twiddle powers b^k
-// FULL: b^1..b^15 in registers (binary splitting).  FACT: b^k = b^(k mod 4) (b^4)^(k div 4) from
-// six registers (one extra multiply for 9 of the 15 k; lower register pressure).
-template <bool FACT>
-struct Pow16 {
-  float2 p[16];
-  __device__ __forceinline__ void init(float2 b) { ce::pow_tree<16>(b, p); }
+// FULL: b^1..b^(R-1) in registers (binary splitting).  FACT: b^k = b^(k mod 4) (b^4)^(k div 4)
+// from 3 + R/4 - 1 registers (one extra multiply for most k; lower register pressure).
+template <int R, bool FACT>
+struct PowR {
+  float2 p[R];
+  __device__ __forceinline__ void init(float2 b) { ce::pow_tree<R>(b, p); }
   __device__ __forceinline__ float2 mul(float2 v, int k) const { return cmul(v, p[k]); }
   __device__ __forceinline__ float2 mulc(float2 v, int k) const { return cmulc(v, p[k]); }
 };
-template <>
-struct Pow16<true> {
-  float2 lo[4], hi[4];
+template <int R>
+struct PowR<R, true> {
+  float2 lo[4], hi[R / 4];
   __device__ __forceinline__ void init(float2 b) {
     lo[1] = b;
     lo[2] = cmul(b, b);
     lo[3] = cmul(lo[2], b);
     hi[1] = cmul(lo[2], lo[2]);
-    hi[2] = cmul(hi[1], hi[1]);
-    hi[3] = cmul(hi[2], hi[1]);
+#pragma unroll
+    for (int i = 2; i < R / 4; ++i) hi[i] = cmul(hi[i / 2], hi[i - i / 2]);
   }
   __device__ __forceinline__ float2 mul(float2 v, int k) const {
     if (k & 3) v = cmul(v, lo[k & 3]);
@@ -87,30 +90,30 @@ struct Pow16<true> {
 // tab = tw_col, W_N^{s (y - n/2)}), pw[k] = b^k with b = W_n^{j - shift}.
 template <class G, class PW>
 __device__ __forceinline__ void col_twiddles(const float2* __restrict__ tab, const float2* __restrict__ tw_n,
-                                             int shift, int j, int sg, float2 (&A)[G::NRES][16], PW& pw) {
+                                             int shift, int j, int sg, float2 (&A)[G::NRES][G::R], PW& pw) {
   constexpr int n = G::n;
 #pragma unroll
   for (int i = 0; i < G::NRES; ++i)
 #pragma unroll
-    for (int r = 0; r < 16; ++r) A[i][r] = __ldg(&tab[(sg + G::NG * i) * n + j + G::J * r]);
+    for (int r = 0; r < G::R; ++r) A[i][r] = __ldg(&tab[(sg + G::NG * i) * n + j + G::J * r]);
   pw.init(__ldg(&tw_n[(j - shift) & (n - 1)]));
 }
 
 // stage A: samples x[r] = x[j + J r] -> W[(s + L k1, j)] for the thread's residues s
 template <class G, class PW>
-__device__ __forceinline__ void stage_a_fwd(const float2 (&x)[16], const float2 (&A)[G::NRES][16],
+__device__ __forceinline__ void stage_a_fwd(const float2 (&x)[G::R], const float2 (&A)[G::NRES][G::R],
                                             const PW& pw, float2* W, int j, int sg) {
 #pragma unroll
   for (int i = 0; i < G::NRES; ++i) {
     const int s = sg + G::NG * i;
-    float2 v[16];
+    float2 v[G::R];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = cmul(x[r], A[i][r]);
-    ce::dftr<16, -1>(v);
+    for (int r = 0; r < G::R; ++r) v[r] = cmul(x[r], A[i][r]);
+    ce::dftr<G::R, -1>(v);
 #pragma unroll
-    for (int k1 = 1; k1 < 16; ++k1) v[k1] = pw.mul(v[k1], k1);
+    for (int k1 = 1; k1 < G::R; ++k1) v[k1] = pw.mul(v[k1], k1);
 #pragma unroll
-    for (int k1 = 0; k1 < 16; ++k1) W[G::widx(s + G::L * k1, j)] = v[k1];
+    for (int k1 = 0; k1 < G::R; ++k1) W[G::widx(s + G::L * k1, j)] = v[k1];
   }
 }
 
@@ -127,19 +130,19 @@ __device__ __forceinline__ void stage_b(float2* W, int q0) {
 
 // stage A^H: W -> acc[r] = sum over the thread's residues of the conjugate chain at j + J r
 template <class G, class PW>
-__device__ __forceinline__ void stage_a_adj(const float2* W, const float2 (&A)[G::NRES][16],
-                                            const PW& pw, int j, int sg, float2 (&acc)[16]) {
+__device__ __forceinline__ void stage_a_adj(const float2* W, const float2 (&A)[G::NRES][G::R],
+                                            const PW& pw, int j, int sg, float2 (&acc)[G::R]) {
 #pragma unroll
   for (int i = 0; i < G::NRES; ++i) {
     const int s = sg + G::NG * i;
-    float2 v[16];
+    float2 v[G::R];
 #pragma unroll
-    for (int k1 = 0; k1 < 16; ++k1) v[k1] = W[G::widx(s + G::L * k1, j)];
+    for (int k1 = 0; k1 < G::R; ++k1) v[k1] = W[G::widx(s + G::L * k1, j)];
 #pragma unroll
-    for (int k1 = 1; k1 < 16; ++k1) v[k1] = pw.mulc(v[k1], k1);
-    ce::dftr<16, 1>(v);
+    for (int k1 = 1; k1 < G::R; ++k1) v[k1] = pw.mulc(v[k1], k1);
+    ce::dftr<G::R, 1>(v);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
+    for (int r = 0; r < G::R; ++r) {
       const float2 w = cmulc(v[r], A[i][r]);
       acc[r] = (i == 0) ? w : ce::cadd(acc[r], w);
     }
@@ -149,11 +152,11 @@ __device__ __forceinline__ void stage_a_adj(const float2* W, const float2 (&A)[G
 // residue-group partial sums -> W[0..n) (fixed order); starts with the barrier that ends the
 // stage-A^H reads of W, ends with a barrier (W[y] = sum, y in [0, n))
 template <class G>
-__device__ __forceinline__ void residue_reduce(float2* W, const float2 (&acc)[16], int j, int sg) {
+__device__ __forceinline__ void residue_reduce(float2* W, const float2 (&acc)[G::R], int j, int sg) {
   constexpr int n = G::n;
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < 16; ++r) W[sg * n + j + G::J * r] = acc[r];
+  for (int r = 0; r < G::R; ++r) W[sg * n + j + G::J * r] = acc[r];
   __syncthreads();
 }
 template <class G>
@@ -166,7 +169,7 @@ __device__ __forceinline__ float2 residue_sum(const float2* W, int y) {
 
 // ================================================================== forward
 template <int n>
-__global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
+__global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_fwd(DevPlan P) {
   using G = ColGeo<n>;
   constexpr int R = G::R, J = G::J, NRES = G::NRES;
   extern __shared__ __align__(128) float2 sm[];
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
   float2* xbuf = sm + 2 * G::Q0 * J;                          // 2 x n, TMA destination
   uint64_t* bar = reinterpret_cast<uint64_t*>(xbuf + 2 * n);
   float2 A[NRES][R];
-  Pow16<kFactPow> pw;
+  PowR<G::R, kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float2* S1 = P.S1 + (size_t)b * C.ncols * n;
   float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(128, 3) k2c_fwd(DevPlan P) {
 // column into a double buffer) -> stage B^H (thread q0, only the present q1 are read) ->
 // stage A^H (thread (j, s)) -> residue-group partial sums -> S~1[b][p][y].
 template <int n>
-__global__ void __launch_bounds__(128, 3) k2c_adj(DevPlan P) {
+__global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPlan P) {
   using G = ColGeo<n>;
   constexpr int R = G::R, J = G::J, NRES = G::NRES, Q0 = G::Q0;
   extern __shared__ __align__(128) float2 sm[];
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(128, 3) k2c_adj(DevPlan P) {
   float2* rbuf = sm + Q0 * J;
   uint64_t* bar = reinterpret_cast<uint64_t*>(rbuf + 2 * RB);
   float2 A[NRES][R];
-  Pow16<kFactPow> pw;
+  PowR<G::R, kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float2* Rc = P.Rc + (size_t)b * C.ntpad;
   float2* out = P.S1 + (size_t)b * C.ncols * n;
@@ -341,7 +344,7 @@ constexpr int kK1BoxP = 128;   // p extent of one S1 tile (= C.s1boxP on this pa
 constexpr int kK1TSlots = 8;   // K1T: S~1 tiles in flight (TMA loads issued ahead)
 
 template <int n>
-__global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPlan P, const __grid_constant__ CUtensorMap tm,
                                                   const float* __restrict__ f) {
   using G = ColGeo<n>;
   extern __shared__ __align__(128) float2 sm[];
@@ -350,11 +353,13 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
   const int b = C.b0 + blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
   float2* W0 = sm;
   float2* W1 = sm + G::Q0 * G::J;
-  float2* stg = sm + 2 * G::Q0 * G::J;   // 2 tiles [kK1BoxP][4]; first holds the 4 input rows
-  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 2 * kK1BoxP * 4);
+  // 2 tiles [kK1BoxP][4]; at the start the 4 input rows (2n float2)
+  float2* stg = sm + 2 * G::Q0 * G::J;
+  constexpr int STG = (2 * kK1BoxP * 4 > 2 * n) ? 2 * kK1BoxP * 4 : 2 * n;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + STG);
   const float* rows = reinterpret_cast<const float*>(stg);
-  float2 A[G::NRES][16];
-  Pow16<kFactPow> pw;
+  float2 A[G::NRES][G::R];
+  PowR<G::R, kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   pdl_wait();
   pdl_trigger();
@@ -368,9 +373,9 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
   ac::mbar_wait(bar, 0);
 #pragma unroll 1
   for (int pr = 0; pr < 2; ++pr) {
-    float2 x[16];
+    float2 x[G::R];
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
+    for (int r = 0; r < G::R; ++r)
       x[r] = make_float2(rows[(2 * pr) * n + j + G::J * r], rows[(2 * pr + 1) * n + j + G::J * r]);
     stage_a_fwd<G>(x, A, pw, pr ? W1 : W0, j, sg);
   }
@@ -386,7 +391,7 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
       __syncthreads();
     }
     const int p = c * kK1BoxP + t;
-    if (p < C.ncols) {
+    if (t < kK1BoxP && p < C.ncols) {
       const int ia = G::fq(p), im = G::fq((N - p) & (N - 1));
       const float2 za = W0[ia], zm = W0[im], zb = W1[ia], zn = W1[im];
       tile[2 * t] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y), 0.5f * (za.y + zm.y),
@@ -409,7 +414,7 @@ __global__ void __launch_bounds__(128, 3) k1c_fwd(DevPlan P, const __grid_consta
 // completion; C[0], C[N/2] -> 2 Re), conjugate transform, f~_y = Re z~, f~_{y+1} = Im z~.
 // Two row pairs per CTA; the [p][4 y] tiles of S~1 arrive by TMA tensor loads.
 template <int n>
-__global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPlan P, const __grid_constant__ CUtensorMap tm,
                                                   float* __restrict__ fout) {
   using G = ColGeo<n>;
   extern __shared__ __align__(128) float2 sm[];
@@ -420,8 +425,8 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
   float2* W1 = sm + G::Q0 * G::J;
   float2* stg = sm + 2 * G::Q0 * G::J;
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + kK1TSlots * kK1BoxP * 4);
-  float2 A[G::NRES][16];
-  Pow16<kFactPow> pw;
+  float2 A[G::NRES][G::R];
+  PowR<G::R, kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   pdl_wait();
   pdl_trigger();
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
     ac::mbar_wait(&bar[slot], (c / kK1TSlots) & 1);
     const float4* tile = reinterpret_cast<const float4*>(stg + slot * kK1BoxP * 4);
     const int p = c * kK1BoxP + t;
-    if (p < C.ncols) {
+    if (t < kK1BoxP && p < C.ncols) {
       const float4 a = tile[2 * t], cc = tile[2 * t + 1];   // (C_y, C_{y+1}), (C_{y+2}, C_{y+3})
       const int ia = G::fq(p);
       if (p == 0 || p == N / 2) {
@@ -467,7 +472,7 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
 #pragma unroll 1
   for (int pr = 0; pr < 2; ++pr) {
     float2* W = pr ? W1 : W0;
-    float2 acc[16];
+    float2 acc[G::R];
     stage_a_adj<G>(W, A, pw, j, sg, acc);
     residue_reduce<G>(W, acc, j, sg);
     const size_t o = ((size_t)b * n + y0 + 2 * pr) * n;
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__(128, 3) k1c_adj(DevPlan P, const __grid_consta
 // Persistent CTAs loop over the rows (b, k); the next row is prefetched into shared memory by a
 // 1-D bulk copy while the current one is transformed, and the per-thread twiddles are loaded once.
 template <int n, bool ADJ>
-__global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
+__global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : 2) k4c_dct(DevPlan P) {
   using G = ColGeo<n, 4>;
   constexpr int N4 = 4 * n;
   extern __shared__ __align__(128) float2 sm[];
@@ -514,8 +519,8 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
     ac::mbar_expect_tx(&bar[slot], (uint32_t)(s1 - s0) * 8);
     ac::bulk_g2s(ibuf + slot * IB, in_all + s0, (uint32_t)(s1 - s0) * 8, &bar[slot]);
   };
-  float2 A[G::NRES][16];
-  Pow16<kFactPow> pw;
+  float2 A[G::NRES][G::R];
+  PowR<G::R, kFactPow> pw;
   col_twiddles<G>(P.tw_dct4, P.tw_n, 0, j, sg, A, pw);
   for (int u = t; u < U; u += blockDim.x) {   // output twiddles, once per CTA
     const int u2 = 2 * u >= M2 ? 2 * u - M2 : 2 * u;
@@ -541,9 +546,9 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
     const int k = row % C.Kp;
     ac::mbar_wait(&bar[slot], (it >> 1) & 1);
     const float2* in = ibuf + slot * IB + (int)(((rbase + row) * cnt) & 1L);
-    float2 x[16];
+    float2 x[G::R];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
+    for (int r = 0; r < G::R; ++r) {
       const int i = 3 * (j + G::J * r) + e, src = ADJ ? i - 1 : i;
       x[r] = (src >= 0 && src < cnt) ? in[src] : make_float2(0.f, 0.f);
     }
@@ -616,8 +621,11 @@ __global__ void __launch_bounds__(192, 2) k4c_dct(DevPlan P) {
 }
 
 // ================================================================== dispatch
+int col_R(int n) { return n >= 1024 ? 32 : 16; }
+static int col_T(int n, int L) { return col_R(n) * L; }
+
 bool dct4_ok(const Consts& C) {
-  return (C.n == 256 || C.n == 512) && 2L * C.M == 12L * C.n && C.J <= 3 * C.n &&
+  return (C.n == 256 || C.n == 512 || C.n == 1024) && 2L * C.M == 12L * C.n && C.J <= 3 * C.n &&
          C.n_t <= 3 * C.n - 1;
 }
 size_t smem_k4c(const Consts& C) {
@@ -630,32 +638,38 @@ cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
   const int rows = C.Kp * C.batch;
-  const dim3 grid(std::min(rows, 2 * 148));
+  const dim3 grid(std::min(rows, (C.n >= 1024 ? 1 : 2) * 148));
+  const dim3 blk(3 * col_T(C.n, 4));
   const size_t sm = smem_k4c(C);
-  if (C.n == 512) {
-    if (adj) e = launch_pdl(C.pdl, k4c_dct<512, true>, grid, dim3(192), sm, s, P);
-    else e = launch_pdl(C.pdl, k4c_dct<512, false>, grid, dim3(192), sm, s, P);
+  if (C.n == 1024) {
+    if (adj) e = launch_pdl(C.pdl, k4c_dct<1024, true>, grid, blk, sm, s, P);
+    else e = launch_pdl(C.pdl, k4c_dct<1024, false>, grid, blk, sm, s, P);
+  } else if (C.n == 512) {
+    if (adj) e = launch_pdl(C.pdl, k4c_dct<512, true>, grid, blk, sm, s, P);
+    else e = launch_pdl(C.pdl, k4c_dct<512, false>, grid, blk, sm, s, P);
   } else {
-    if (adj) e = launch_pdl(C.pdl, k4c_dct<256, true>, grid, dim3(192), sm, s, P);
-    else e = launch_pdl(C.pdl, k4c_dct<256, false>, grid, dim3(192), sm, s, P);
+    if (adj) e = launch_pdl(C.pdl, k4c_dct<256, true>, grid, blk, sm, s, P);
+    else e = launch_pdl(C.pdl, k4c_dct<256, false>, grid, blk, sm, s, P);
   }
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-bool col_ok(const Consts& C) { return C.Lres == 8 && (C.n == 256 || C.n == 512); }
+bool col_ok(const Consts& C) { return C.Lres == 8 && (C.n == 256 || C.n == 512 || C.n == 1024); }
 
 size_t smem_k2c_fwd(const Consts& C) {
-  const int Q0 = 128, J = C.n / 16;
+  const int Q0 = col_R(C.n) * 8, J = C.n / col_R(C.n);
   return (size_t)2 * Q0 * J * 8 + (size_t)2 * C.n * 8 + 64;
 }
 size_t smem_k2c_adj(const Consts& C) {
-  const int Q0 = 128, J = C.n / 16;
+  const int Q0 = col_R(C.n) * 8, J = C.n / col_R(C.n);
   return (size_t)Q0 * J * 8 + (size_t)2 * C.k2c_rbuf * 8 + 64;
 }
 
-size_t smem_k1c(const Consts& C) { return (size_t)2 * 128 * (C.n / 16) * 8 + 2 * kK1BoxP * 32 + 64; }
+size_t smem_k1c(const Consts& C) {
+  return (size_t)2 * 8 * C.n * 8 + (size_t)std::max(2 * kK1BoxP * 4, 2 * C.n) * 8 + 64;
+}
 size_t smem_k1c_adj(const Consts& C) {
-  return (size_t)2 * 128 * (C.n / 16) * 8 + (size_t)kK1TSlots * kK1BoxP * 32 + 128;
+  return (size_t)2 * 8 * C.n * 8 + (size_t)kK1TSlots * kK1BoxP * 32 + 128;
 }
 
 template <int n>
@@ -675,15 +689,17 @@ static cudaError_t cfg_col() {
 
 cudaError_t configure_col_kernels(const Consts& C) {
   if (!col_ok(C) && !dct4_ok(C)) return cudaSuccess;
-  return C.n == 512 ? cfg_col<512>() : cfg_col<256>();
+  return C.n == 1024 ? cfg_col<1024>() : (C.n == 512 ? cfg_col<512>() : cfg_col<256>());
 }
 
 cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
   const dim3 grid((C.ncols + C.col_strip - 1) / C.col_strip, C.batch);
-  if (C.n == 512) e = launch_pdl(C.pdl, k2c_fwd<512>, grid, dim3(128), smem_k2c_fwd(C), s, P);
-  else e = launch_pdl(C.pdl, k2c_fwd<256>, grid, dim3(128), smem_k2c_fwd(C), s, P);
+  const dim3 blk(col_T(C.n, 8));
+  if (C.n == 1024) e = launch_pdl(C.pdl, k2c_fwd<1024>, grid, blk, smem_k2c_fwd(C), s, P);
+  else if (C.n == 512) e = launch_pdl(C.pdl, k2c_fwd<512>, grid, blk, smem_k2c_fwd(C), s, P);
+  else e = launch_pdl(C.pdl, k2c_fwd<256>, grid, blk, smem_k2c_fwd(C), s, P);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -691,8 +707,10 @@ cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
   const dim3 grid((C.ncols + C.col_strip - 1) / C.col_strip, C.batch);
-  if (C.n == 512) e = launch_pdl(C.pdl, k2c_adj<512>, grid, dim3(128), smem_k2c_adj(C), s, P);
-  else e = launch_pdl(C.pdl, k2c_adj<256>, grid, dim3(128), smem_k2c_adj(C), s, P);
+  const dim3 blk(col_T(C.n, 8));
+  if (C.n == 1024) e = launch_pdl(C.pdl, k2c_adj<1024>, grid, blk, smem_k2c_adj(C), s, P);
+  else if (C.n == 512) e = launch_pdl(C.pdl, k2c_adj<512>, grid, blk, smem_k2c_adj(C), s, P);
+  else e = launch_pdl(C.pdl, k2c_adj<256>, grid, blk, smem_k2c_adj(C), s, P);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -700,8 +718,10 @@ cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float*
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
   const dim3 grid(C.n / 4, C.batch);
-  if (C.n == 512) e = launch_pdl(C.pdl, k1c_fwd<512>, grid, dim3(128), smem_k1c(C), s, P, tm, f);
-  else e = launch_pdl(C.pdl, k1c_fwd<256>, grid, dim3(128), smem_k1c(C), s, P, tm, f);
+  const dim3 blk(col_T(C.n, 8));
+  if (C.n == 1024) e = launch_pdl(C.pdl, k1c_fwd<1024>, grid, blk, smem_k1c(C), s, P, tm, f);
+  else if (C.n == 512) e = launch_pdl(C.pdl, k1c_fwd<512>, grid, blk, smem_k1c(C), s, P, tm, f);
+  else e = launch_pdl(C.pdl, k1c_fwd<256>, grid, blk, smem_k1c(C), s, P, tm, f);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -709,8 +729,10 @@ cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cu
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
   const dim3 grid(C.n / 4, C.batch);
-  if (C.n == 512) e = launch_pdl(C.pdl, k1c_adj<512>, grid, dim3(128), smem_k1c_adj(C), s, P, tm, f);
-  else e = launch_pdl(C.pdl, k1c_adj<256>, grid, dim3(128), smem_k1c_adj(C), s, P, tm, f);
+  const dim3 blk(col_T(C.n, 8));
+  if (C.n == 1024) e = launch_pdl(C.pdl, k1c_adj<1024>, grid, blk, smem_k1c_adj(C), s, P, tm, f);
+  else if (C.n == 512) e = launch_pdl(C.pdl, k1c_adj<512>, grid, blk, smem_k1c_adj(C), s, P, tm, f);
+  else e = launch_pdl(C.pdl, k1c_adj<256>, grid, blk, smem_k1c_adj(C), s, P, tm, f);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

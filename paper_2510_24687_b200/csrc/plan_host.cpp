@@ -286,8 +286,8 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
     }
   }
   // two-pass stable counting sort: by key(q), then by p.  key(q) = (q mod Q0, q / Q0) with
-  // Q0 = 16 L orders a column's targets by the (q0, q1) split of kernels_col.cu
-  const int Q0 = 16 * L;
+  // Q0 = col_R(n) L orders a column's targets by the (q0, q1) split of kernels_col.cu
+  const int Q0 = col_R(n) * L;
   auto qkey = [&](int q) { return (q % Q0) * (N / Q0) + q / Q0; };
   {
     std::vector<int> cnt(N + 1, 0);
@@ -368,7 +368,7 @@ void build_inverse_tables(const Consts& C, const std::vector<int>& node_perm, In
     }
   }
   // ---- step 5 targets: Cartesian (p, q), p in [0, N/2], |xi| < lambda_max
-  const int Q0 = 16 * C.Lres;
+  const int Q0 = col_R(C.n) * C.Lres;
   auto code = [&](int j, long l) {
     const long lp = ((l + nphi / 4) % nphi + nphi) % nphi;
     if (lp < half) return node_perm[(size_t)j * half + lp];

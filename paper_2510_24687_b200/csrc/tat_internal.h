@@ -188,6 +188,7 @@ cudaError_t launch_k4_fast(const DevPlan& P, bool adj, cudaStream_t s);
 size_t max_smem_needed(const Consts& C);
 // kernels_col.cu: two-stage column transforms (L = 8, n in {256, 512})
 bool col_ok(const Consts& C);
+int col_R(int n);   // stage-A points per thread of the two-stage engine (Q0 = col_R(n) * L)
 size_t smem_k2c_fwd(const Consts& C);
 size_t smem_k2c_adj(const Consts& C);
 cudaError_t configure_col_kernels(const Consts& C);
