@@ -67,6 +67,8 @@ class Constants:
     ring: tuple       # ring index r_d of each detector
     K: int            # n_phi/2, harmonics k in [-K, K-1] (G11)
     omega: float      # L2 adjoint scale dt * 2 pi R / (n_ring h^2) (G18, G20)
+    dense: bool = False   # detectors off any canonical ring (reading G24): D6/D7 as dense sums
+    angles: tuple = ()    # detector angles (dense mode)
 
     @property
     def n_phi(self) -> int:
@@ -112,11 +114,21 @@ def derive(n, n_det, n_t, R, c, T, angles, L_override: float | None = None) -> C
     lam_max = math.pi / h                                        # G8
     J = int(math.floor(lam_max / dlam + 1e-9))
     wJ = 0.5 if abs(J * dlam - lam_max) <= 1e-9 * lam_max else 1.0
-    n_ring, ring = infer_ring(np.asarray(angles), n_det)
+    a = np.asarray(angles, dtype=np.float64)
+    if not np.all(np.isfinite(a)):
+        raise ValueError("detector angles must be finite")
+    dense = False
+    try:
+        n_ring, ring = infer_ring(a, n_det)
+    except ValueError:
+        # reading G24: detectors off every canonical ring -> polar grid n_phi = the smallest
+        # power of two >= max(n_det, 8); synthesis/analysis at the exact angles (dense sums)
+        n_ring, ring, dense = max(8, 1 << int(math.ceil(math.log2(max(n_det, 1))))), (), True
     K = n_ring // 2
     omega = dt * 2.0 * math.pi * R / (n_ring * h * h)
     return Constants(n, n_det, n_t, R, c, T, h, T_new, L, N, dxi, dt, M, dlam, J, wJ,
-                     n_ring, tuple(int(r) for r in ring), K, omega)
+                     n_ring, tuple(int(r) for r in ring), K, omega, dense,
+                     tuple(float(x) for x in a) if dense else ())
 
 
 def derive_geom(geom, **kw) -> Constants:
@@ -329,6 +341,27 @@ def restrict_adjoint(g: np.ndarray, C: Constants) -> np.ndarray:
     return out
 
 
+# ----------------------------------------------------------------------------- D6/D7, dense mode
+def _detector_phases(C: Constants) -> np.ndarray:
+    """E[k, d] = exp(i k theta_d), k in [-K, K-1] (reading G24)."""
+    k = _harmonics(C).astype(np.float64)
+    th = np.asarray(C.angles, dtype=np.float64)
+    return np.exp(1j * np.outer(k, th))
+
+
+def dense_synthesis(G: np.ndarray, C: Constants) -> np.ndarray:
+    """D6+D7 at arbitrary detector angles: g[m, d] = Re sum_{k=-K}^{K-1} G[m, k] e^{i k theta_d}
+    (E:FourSerForg P:L407-411 evaluated at the detectors, then D7's real part).  Off the polar
+    grid the unpaired harmonic k = -K has an imaginary part; D7's Re keeps G_{-K} cos(K theta_d),
+    the symmetric split of the Nyquist term (reading G24).  Im is not asserted to vanish."""
+    return (G @ _detector_phases(C)).real
+
+
+def dense_synthesis_adjoint(g: np.ndarray, C: Constants) -> np.ndarray:
+    """(D6 D7)^H: Gt[m, k] = sum_d g[m, d] e^{-i k theta_d}."""
+    return np.asarray(g, np.float64) @ _detector_phases(C).conj().T
+
+
 # ----------------------------------------------------------------------------- chains
 def forward_stages(f: np.ndarray, C: Constants) -> dict:
     """Algorithm 1 on one image, keeping every intermediate (full layout)."""
@@ -338,6 +371,9 @@ def forward_stages(f: np.ndarray, C: Constants) -> dict:
     st["fk"] = angular_coefficients(st["P"], C)    # step 4
     st["H"] = apply_multiplier(st["fk"], C)        # E:eq2 multiplier
     st["G"] = cosine_transform(st["H"], C)         # step 5
+    if C.dense:                                     # steps 6-7 at arbitrary angles (G24)
+        st["g"] = dense_synthesis(st["G"], C)
+        return st
     st["gfull"] = synthesis(st["G"], C)            # step 6
     st["g"] = restrict(st["gfull"], C)             # step 7
     return st
@@ -346,8 +382,11 @@ def forward_stages(f: np.ndarray, C: Constants) -> dict:
 def adjoint_stages(g: np.ndarray, C: Constants) -> dict:
     """Exact transpose of Algorithm 1, in Algorithm 2's step order."""
     st = {}
-    st["gfull"] = restrict_adjoint(np.asarray(g, np.float64), C)     # step 1
-    st["G"] = synthesis_adjoint(st["gfull"], C)                       # step 2
+    if C.dense:                                                       # steps 1-2 (G24)
+        st["G"] = dense_synthesis_adjoint(g, C)
+    else:
+        st["gfull"] = restrict_adjoint(np.asarray(g, np.float64), C)  # step 1
+        st["G"] = synthesis_adjoint(st["gfull"], C)                   # step 2
     st["Hc"] = cosine_transform_adjoint(st["G"], C)                   # step 3 (cos sums)
     st["H"] = apply_multiplier(st["Hc"], C, conj=True)                # step 3 ((-i)^|k| J)
     st["P"] = angular_coefficients_adjoint(st["H"], C)                # step 4
@@ -485,6 +524,8 @@ def inverse(g: np.ndarray, C: Constants, r0: float) -> np.ndarray:
     """A^{-1} g for one data set [n_t, n_det] (Algorithm 3, steps 1-8 above); [n, n] float64."""
     if C.R != 1.0 or C.c != 1.0:
         raise NotImplementedError("the paper derives A^{-1} for R = c = 1 (Appendix)")
+    if C.dense:
+        raise NotImplementedError("A^{-1} needs detectors on a canonical ring")
     if not (0.0 < r0 < C.R):
         raise ValueError("r0 must lie in (0, R)")
     gfull = restrict_adjoint(np.asarray(g, np.float64), C)                 # step 1
