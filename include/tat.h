@@ -14,9 +14,12 @@
  *       x = (ix - n/2) h, y = (iy - n/2) h, h = 2/n          (reading G1)
  *   - g[b][m][d] (float32, row-major, contiguous) is the trace at t_m = (m+1) T / n_t
  *       (reading G2) and detector d, in the caller's detector_angles order.
- *   - detector_angles are radians, counter-clockwise from +x, and must lie on a canonical
- *       uniform ring theta = 2 pi r / n_ring (reading G3); n_ring is inferred as the smallest
- *       multiple of 4 >= n_det that fits every angle within 1e-9 rad.
+ *   - detector_angles are radians, counter-clockwise from +x.  When they lie on a canonical
+ *       uniform ring theta = 2 pi r / n_ring (reading G3; n_ring = the smallest multiple of 4
+ *       >= n_det fitting every angle within 1e-9 rad) the angular synthesis/analysis are ring
+ *       FFTs; otherwise (dense mode, reading G24) n_ring = n_phi = the smallest power of two
+ *       >= max(n_det, 8) and the synthesis/analysis are dense sums at the exact angles
+ *       (tat_inverse is not available in dense mode).
  *   - Every call processes exactly `batch` images (the batch the plan was created for).
  *
  * Ownership: the plan owns its device tables and its workspace (allocated at create time).
@@ -49,8 +52,7 @@ typedef enum {
   TAT_OK = 0,
   TAT_ERR_INVALID_ARGUMENT = 1,     /* null pointer, n < 8 / odd / not a power of two, n_det < 1,
                                        n_t < 1, batch < 1, R, c, T not finite > 0, non-finite angle */
-  TAT_ERR_UNSUPPORTED_GEOMETRY = 2, /* angles not on a canonical ring (n_ring % 4 == 0,
-                                       n_ring >= n_det, distinct ring positions), or a size the
+  TAT_ERR_UNSUPPORTED_GEOMETRY = 2, /* two detectors on one ring position, or a size the
                                        sm_100a kernels do not implement (see tat_last_error()) */
   TAT_ERR_OUT_OF_MEMORY = 3,
   TAT_ERR_CUDA = 4                  /* CUDA API or launch failure */
@@ -147,7 +149,7 @@ typedef struct {
   int N;            /* Cartesian FFT size 2L/h */
   int J;            /* last radial index; N_lambda = J + 1 */
   int M;            /* DCT-I length; the lambda->t transform runs as a 2M-point FFT */
-  int n_ring;       /* canonical ring size = n_phi */
+  int n_ring;       /* canonical ring size = n_phi (dense mode: the polar grid's n_phi) */
   int K;            /* n_ring / 2; harmonics k in [-K, K-1] */
   int n_nodes_half; /* polar nodes in the half-plane store (n_ring/2 * (J+1)) */
   double L, T_new, dxi, dlam, omega, dt, h, wJ;

@@ -307,7 +307,8 @@ cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float*
   else k4_dct<<<dim3(C.Kp, B), kThreads, smem_dct(C), s>>>(P);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[4], s);
-  if (ring_fast_ok(C)) e = launch_k5(P, g, s);
+  if (C.dense) e = launch_k5d(P, g, s);
+  else if (ring_fast_ok(C)) e = launch_k5(P, g, s);
   else k5_synth_restrict<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[5], s);
@@ -321,7 +322,8 @@ cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float*
   const int JT = tile_ring(C.n_ring);
   if (ev) cudaEventRecord(ev[0], s);
   cudaError_t e = cudaSuccess;
-  if (ring_fast_ok(C)) e = launch_k5t(P, g, s);
+  if (C.dense) e = launch_k5dt(P, g, s);
+  else if (ring_fast_ok(C)) e = launch_k5t(P, g, s);
   else k5t_analysis<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);

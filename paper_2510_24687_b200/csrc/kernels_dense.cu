@@ -1,0 +1,138 @@
+// Dense angular synthesis / analysis for detectors off any canonical ring (reading G24; SURVEY
+// §8(f) f4 (ii)).  Steps 6-7 of Algorithm 1 (E:FourSerForg P:L407-411, restriction P:L562) and
+// steps 1-2 of Algorithm 2 evaluated at the exact detector angles theta_d:
+//
+//   K5d : g[b][m][d] = sum_{k=0}^{K} Re( S4[b][k][m] E5[k][d] ),  E5 = c_k e^{i s_k k theta_d}
+//   K5dT: S4[b][k][m] = sum_d g[b][m][d] conj(E5T[k][d]),        E5T = e^{i s_k k theta_d}
+//
+// (c_0 = c_K = 1, c_k = 2 otherwise; s_K = -1: row K holds the harmonic -K).  Both are real GEMMs
+// of shape [n_t x 2(K+1)] x [2(K+1) x n_det] per image, tiled 64 x 64 through shared memory
+// with 4 x 4 register blocks (exact fp32; the fp32 pipe, not tensor cores, keeps the 1e-4 bar).
+#include "tat_internal.h"
+
+namespace tat {
+
+constexpr int kDT = 64;   // output tile (both dims)
+constexpr int kDK = 16;   // reduction chunk
+
+// ---- K5d: out[m][d] over m-tile x d-tile, reduction over k
+__global__ void __launch_bounds__(256) k5d_synth(DevPlan P, float* __restrict__ gout) {
+  __shared__ float2 As[kDK][kDT];   // S4 rows k, columns m
+  __shared__ float2 Bs[kDK][kDT];   // E5 rows k, columns d
+  const Consts& C = P.C;
+  const int b = C.b0 + blockIdx.z;
+  const int m0 = blockIdx.y * kDT, d0 = blockIdx.x * kDT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const float2* S4 = P.S4 + (size_t)b * C.Kp * C.n_t;
+  float acc[4][4] = {};
+  pdl_wait();
+  pdl_trigger();
+  for (int k0 = 0; k0 < C.Kp; k0 += kDK) {
+    for (int i = threadIdx.x; i < kDK * kDT; i += 256) {
+      const int kk = i / kDT, c = i - kk * kDT;
+      const int k = k0 + kk;
+      As[kk][c] = (k < C.Kp && m0 + c < C.n_t) ? S4[(size_t)k * C.n_t + m0 + c] : make_float2(0.f, 0.f);
+      Bs[kk][c] = (k < C.Kp && d0 + c < C.n_det) ? __ldg(&P.dense_e5[(size_t)k * C.n_det + d0 + c])
+                                                 : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kDK; ++kk) {
+      float2 a[4], e[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) e[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i].x, e[j].x, fmaf(-a[i].y, e[j].y, acc[i][j]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= C.n_t) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int d = d0 + tx * 4 + j;
+      if (d < C.n_det) {
+        const size_t o = ((size_t)b * C.n_t + m) * C.n_det + d;
+        gout[o] = epi_fwd(P, o, acc[i][j]);
+      }
+    }
+  }
+}
+
+// ---- K5dT: out[k][m] (complex) over k-tile x m-tile, reduction over d
+__global__ void __launch_bounds__(256) k5d_anal(DevPlan P, const float* __restrict__ gin) {
+  __shared__ float2 Es[kDK][kDT + 1];   // E5T rows d (chunk), columns k
+  __shared__ float Gs[kDK][kDT + 1];    // g rows d (chunk), columns m
+  const Consts& C = P.C;
+  const int b = C.b0 + blockIdx.z;
+  const int k0 = blockIdx.y * kDT, m0 = blockIdx.x * kDT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const float* g = gin + (size_t)b * C.n_t * C.n_det;
+  float2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  pdl_wait();
+  pdl_trigger();
+  for (int dd0 = 0; dd0 < C.n_det; dd0 += kDK) {
+    for (int i = threadIdx.x; i < kDK * kDT; i += 256) {
+      const int r = i / kDK, c = i - r * kDK;    // r: k or m within the tile, c: d within the chunk
+      const int d = dd0 + c;
+      Es[c][r] = (k0 + r < C.Kp && d < C.n_det) ? __ldg(&P.dense_e5t[(size_t)(k0 + r) * C.n_det + d])
+                                                : make_float2(0.f, 0.f);
+      Gs[c][r] = (m0 + r < C.n_t && d < C.n_det) ? g[(size_t)(m0 + r) * C.n_det + d] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < kDK; ++c) {
+      float2 e[4];
+      float gv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) e[i] = Es[c][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) gv[j] = Gs[c][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[i][j].x = fmaf(e[i].x, gv[j], acc[i][j].x);
+          acc[i][j].y = fmaf(-e[i].y, gv[j], acc[i][j].y);
+        }
+    }
+    __syncthreads();
+  }
+  float2* S4 = P.S4 + (size_t)b * C.Kp * C.n_t;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = k0 + ty * 4 + i;
+    if (k >= C.Kp) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + tx * 4 + j;
+      if (m < C.n_t) S4[(size_t)k * C.n_t + m] = acc[i][j];
+    }
+  }
+}
+
+cudaError_t launch_k5d(const DevPlan& P, float* g, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid((C.n_det + kDT - 1) / kDT, (C.n_t + kDT - 1) / kDT, C.batch);
+  const cudaError_t e = launch_pdl(C.pdl, k5d_synth, grid, dim3(256), 0, s, P, g);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_k5dt(const DevPlan& P, const float* g, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid((C.n_t + kDT - 1) / kDT, (C.Kp + kDT - 1) / kDT, C.batch);
+  const cudaError_t e = launch_pdl(C.pdl, k5d_anal, grid, dim3(256), 0, s, P, g);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+}  // namespace tat

@@ -80,8 +80,14 @@ std::string derive_consts(int n, int n_det, int n_t, double R, double c, double 
     }
     if (ok) n_ring = cand;
   }
-  if (!n_ring) return "detector angles are not on a canonical uniform ring 2*pi*r/n_ring";
-  {
+  if (!n_ring) {
+    // reading G24: detectors off every canonical ring -> dense mode, polar grid n_phi = the
+    // smallest power of two >= max(n_det, 8); synthesis/analysis at the exact angles
+    n_ring = 8;
+    while (n_ring < n_det) n_ring *= 2;
+    C.dense = 1;
+    std::fill(ring.begin(), ring.end(), -1);
+  } else {
     std::vector<int> s(ring);
     std::sort(s.begin(), s.end());
     if (std::adjacent_find(s.begin(), s.end()) != s.end())
@@ -177,7 +183,8 @@ static void unit_circle(int l, int n_phi, double& cs, double& sn) {
 
 static inline int fbits(float f) { int i; std::memcpy(&i, &f, 4); return i; }
 
-void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) {
+void build_tables(const Consts& C, const std::vector<int>& ring, const double* angles,
+                  HostTables& H) {
   const int n = C.n, N = C.N, L = C.Lres, NL = C.NL, Kp = C.Kp, nphi = C.n_ring;
   // ---- multiplier m'[k][j] (E:eq2 P:L463-466 + trapezoid in lambda; scale of D1 and D3)
   H.mult.assign((size_t)Kp * NL, 0.f);
@@ -212,6 +219,22 @@ void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H) 
   H.tw_dct.resize(2 * (size_t)C.M);
   for (int k = 0; k < 2 * C.M; ++k) H.tw_dct[k] = root(k, 2L * C.M, -1);
   H.ring = ring;
+  if (C.dense) {   // dense synthesis / analysis tables (reading G24), angles reduced in float64
+    H.dense_e5.resize((size_t)C.Kp * C.n_det);
+    H.dense_e5t.resize((size_t)C.Kp * C.n_det);
+    for (int k = 0; k < C.Kp; ++k) {
+      const double sk = (k == C.K) ? -1.0 : 1.0;            // row K holds the harmonic -K
+      const double ck = (k == 0 || k == C.K) ? 1.0 : 2.0;   // C2R weights
+      for (int d = 0; d < C.n_det; ++d) {
+        const double a = std::fmod(sk * k * angles[d], 2.0 * kPi);
+        // the harmonic -K enters through its real part only (G_{-K} is real for real f and
+        // even K = n_phi / 2; Re keeps G_{-K} cos(K theta), reading G24), so its row is real
+        const double cs = std::cos(a), sn = (k == C.K) ? 0.0 : std::sin(a);
+        H.dense_e5[(size_t)k * C.n_det + d] = make_float2((float)(ck * cs), (float)(ck * sn));
+        H.dense_e5t[(size_t)k * C.n_det + d] = make_float2((float)cs, (float)sn);
+      }
+    }
+  }
 
   // ---- half-plane polar nodes (Alg. 1 step 3; readings G12, G13)
   const int half = C.half;

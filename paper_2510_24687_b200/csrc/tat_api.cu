@@ -128,7 +128,7 @@ tat_status tat_plan_host_multiplier(int n, int n_det, int n_t, double R, double 
   if (!err.empty()) return fail(code == 2 ? TAT_ERR_UNSUPPORTED_GEOMETRY : TAT_ERR_INVALID_ARGUMENT, err);
   if (!out || out_len < (size_t)C.Kp * C.NL) return fail(TAT_ERR_INVALID_ARGUMENT, "out too small");
   HostTables H;
-  build_tables(C, ring, H);
+  build_tables(C, ring, detector_angles, H);
   std::memcpy(out, H.mult.data(), H.mult.size() * sizeof(float));
   return TAT_OK;
 }
@@ -149,7 +149,7 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
 
   HostTables H;
-  build_tables(C, ring, H);
+  build_tables(C, ring, detector_angles, H);
 
   tat_plan* p = new (std::nothrow) tat_plan();
   if (!p) return fail(TAT_ERR_OUT_OF_MEMORY, "host allocation");
@@ -172,6 +172,8 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     if ((e = upload(p, H.k2t_rec, &P.k2t_rec, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2t_ov, &P.k2t_ov, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.ring, &P.ring, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.dense_e5, &P.dense_e5, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.dense_e5t, &P.dense_e5t, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.tw_col, &P.tw_col, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.tw_dct4, &P.tw_dct4, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2c_mask, &P.k2c_mask, tb)) != cudaSuccess) break;
@@ -386,6 +388,8 @@ tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0
   if (!(r0 > 0.0 && r0 < C.R)) return fail(TAT_ERR_INVALID_ARGUMENT, "r0 must lie in (0, R)");
   if (C.R != 1.0 || C.c != 1.0)
     return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: the paper derives A^-1 for R = c = 1");
+  if (C.dense)
+    return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: needs detectors on a canonical ring");
   if (!dct4_ok(C) && !dct_fast_r(C))
     return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: no sine-transform kernel for this 2M");
   tat_plan* p = const_cast<tat_plan*>(plan);

@@ -16,6 +16,7 @@ struct Consts {
   int b0 = 0;       // first image of a launch (sub-batch pipelining); batch = images in it
   int dct_sine = 0; // K4T computes sum_m G~ sin(c lambda_j t_m) (the inverse, Alg. 3 step 3)
   int pdl = 1;      // launch the chain kernels with programmatic dependent launch
+  int dense = 0;    // detectors off any canonical ring: K5 / K5T as dense sums (reading G24)
   int col_strip = 16; // K2 / K2Tb: columns per CTA (k2c_fwd recomputes one halo column;
                       // 12-16 measured best at C3, 20-32 slower)
   double R = 1, c = 1, T = 1;
@@ -57,7 +58,9 @@ struct HostTables {
   // two: (src0, w0 bits, -(k+1), count) with entries 1..count-1 at k2t_ov[k ..]
   std::vector<int4> k2t_rec;        // [T]
   std::vector<int2> k2t_ov;         // overflow entries (src, w bits)
-  std::vector<int> ring;            // [n_det]
+  std::vector<int> ring;            // [n_det] (-1 in dense mode)
+  // dense mode: E5[k][d] = c_k (cos, sin)(s_k k theta_d), E5T without c_k (s_K = -1, c = 1, 2, 1)
+  std::vector<float2> dense_e5, dense_e5t;   // [Kp][n_det]
   // k2c_adj: per (column p, q0 = q mod 16L): bit q1 set if target (p, q0 + 16L q1) exists,
   // and the index of the first such target (targets of a column are ordered by (q0, q1))
   std::vector<uint32_t> k2c_mask;   // [ncols][16L] (only when col_ok)
@@ -68,7 +71,8 @@ struct HostTables {
 std::string derive_consts(int n, int n_det, int n_t, double R, double c, double T, int batch,
                           const double* angles, Consts& out, std::vector<int>& ring, int& code);
 std::string gpu_support(const Consts& C);    // "" if the sm_100a kernels implement C
-void build_tables(const Consts& C, const std::vector<int>& ring, HostTables& H);
+void build_tables(const Consts& C, const std::vector<int>& ring, const double* angles,
+                  HostTables& H);
 void bessel_row(double x, int kmax, double* out);   // J_0..J_kmax(x), Miller recurrence
 
 // Device-side view of a plan (pointers into device memory).
@@ -94,6 +98,8 @@ struct DevPlan {
   const int* k2c_base = nullptr;
   // inverse (Alg. 3 step 5): per Cartesian target 4 polar corners (sorted node index, or
   // -(index + 1) for the conjugate mirror node) and bilinear weights
+  const float2* dense_e5 = nullptr;
+  const float2* dense_e5t = nullptr;
   const int4* inv_nodes = nullptr;
   const float4* inv_w = nullptr;
   // workspace
@@ -200,6 +206,9 @@ cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s);
 cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
 cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s);
 
+// kernels_dense.cu: dense angular synthesis / analysis (reading G24)
+cudaError_t launch_k5d(const DevPlan& P, float* g, cudaStream_t s);
+cudaError_t launch_k5dt(const DevPlan& P, const float* g, cudaStream_t s);
 // kernels_inv.cu: inverse-specific stages (Alg. 3 steps 5, 7, 8)
 cudaError_t launch_k2i_interp(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k2i_finish(const DevPlan& P, float* f, const unsigned char* region, float* csum,

@@ -64,10 +64,15 @@ def test_argument_validation(args, code):
     assert st == code
 
 
-def test_off_ring_angles_rejected():
+def test_off_ring_angles_dense_mode():
+    """Angles off every canonical ring select the dense mode (reading G24): n_ring = the
+    smallest power of two >= max(n_det, 8), ring indices -1, same n_ring as the oracle."""
     ang = np.array([0.0, 0.1234567, 1.0, 2.0])
-    _, _, st = tat.derive(64, 4, 128, 1.0, 1.0, 2.0, 1, ang)
-    assert st == 2
+    info, ring, st = tat.derive(64, 4, 128, 1.0, 1.0, 2.0, 1, ang)
+    assert st == 0 and info["n_ring"] == 8 and (ring == -1).all()
+    C = O.derive(64, 4, 128, 1.0, 1.0, 2.0, ang)
+    assert C.dense and C.n_ring == info["n_ring"]
+    assert info["omega"] == pytest.approx(C.omega, rel=1e-14)
     bad = np.array(synth.ring_angles(8))
     bad[3] = np.nan
     _, _, st = tat.derive(64, 8, 128, 1.0, 1.0, 2.0, 1, bad)
