@@ -275,6 +275,7 @@ cudaError_t configure_kernels(const DevPlan& P) {
   if (e == cudaSuccess) e = configure_col_kernels(C);
   if (e == cudaSuccess) e = configure_ring_kernels(C);
   if (e == cudaSuccess) e = configure_dct_kernels(C);
+  if (e == cudaSuccess) e = configure_dense_kernels(C);
   SETSM(k3_angular_mult, smem_ring(C));
   SETSM(k4_dct, smem_dct(C));
   SETSM(k5_synth_restrict, smem_ring(C));
@@ -307,7 +308,7 @@ cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float*
   else k4_dct<<<dim3(C.Kp, B), kThreads, smem_dct(C), s>>>(P);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[4], s);
-  if (C.dense) e = launch_k5d(P, g, s);
+  if (C.dense) e = C.k5tc_kp > 0 ? launch_k5d_tc(P, g, s) : launch_k5d(P, g, s);
   else if (ring_fast_ok(C)) e = launch_k5(P, g, s);
   else k5_synth_restrict<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);
   if (e != cudaSuccess) return e;

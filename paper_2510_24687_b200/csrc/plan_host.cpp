@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -86,6 +87,10 @@ std::string derive_consts(int n, int n_det, int n_t, double R, double c, double 
     n_ring = 8;
     while (n_ring < n_det) n_ring *= 2;
     C.dense = 1;
+    {
+      const char* ev = std::getenv("TAT_DENSE_TC");   // debug switch: 0 = SIMT synthesis
+      C.k5tc_kp = (ev && ev[0] == '0') ? 0 : (2 * (n_ring / 2 + 1) + kK5tcKC - 1) / kK5tcKC * kK5tcKC;
+    }
     std::fill(ring.begin(), ring.end(), -1);
   } else {
     std::vector<int> s(ring);
@@ -233,6 +238,37 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
         H.dense_e5[(size_t)k * C.n_det + d] = make_float2((float)(ck * cs), (float)(ck * sn));
         H.dense_e5t[(size_t)k * C.n_det + d] = make_float2((float)cs, (float)sn);
       }
+    }
+    if (C.k5tc_kp > 0) {   // tcgen05 synthesis operand B[2k][d] = Re E5, B[2k+1][d] = -Im E5
+      const int KP = C.k5tc_kp, D = (C.n_det + 127) / 128 * 128;
+      auto tf32 = [](float x) {   // round to nearest (ties away) at 10 mantissa bits, as cvt.rna
+        uint32_t u;
+        std::memcpy(&u, &x, 4);
+        u = (u + 0x1000u) & 0xFFFFE000u;
+        float r;
+        std::memcpy(&r, &u, 4);
+        return r;
+      };
+      // packed [d block][chunk][hi, lo][core layout]: element (r, k') of a 128 x KC tile at float
+      // offset (r / 8) * 8 KC + (k' / 4) * 32 + (r % 8) * 4 + k' % 4 (8-row x 16-byte cores,
+      // K-adjacent cores 128 B apart, row groups 32 KC bytes apart: the no-swizzle K-major layout)
+      constexpr int KC = kK5tcKC;
+      const int nch = KP / KC;
+      H.k5tc_b.assign((size_t)D * KP * 2, 0.f);
+      for (int k = 0; k < C.Kp; ++k)
+        for (int d = 0; d < C.n_det; ++d) {
+          const float2 e = H.dense_e5[(size_t)k * C.n_det + d];
+          const float v[2] = {e.x, -e.y};
+          const int r = d % 128, db = d / 128;
+          for (int j = 0; j < 2; ++j) {
+            const int kp = 2 * k + j, ch = kp / KC, kk = kp % KC;
+            const size_t tile = ((size_t)db * nch + ch) * 2;
+            const size_t off = (size_t)(r / 8) * 8 * KC + (kk / 4) * 32 + (r % 8) * 4 + kk % 4;
+            const float hi = tf32(v[j]);
+            H.k5tc_b[tile * 128 * KC + off] = hi;
+            H.k5tc_b[(tile + 1) * 128 * KC + off] = tf32(v[j] - hi);
+          }
+        }
     }
   }
 

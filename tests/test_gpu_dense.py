@@ -25,10 +25,16 @@ def _check(out, ref, what):
     assert rel <= 1e-4 and mx <= 1e-3, f"{what}: rel-L2 {rel:.3e}, max {mx:.3e}"
 
 
-@pytest.mark.parametrize("n,n_det,n_t,batch", [(64, 48, 128, 2), (256, 200, 512, 2)])
-def test_dense_parity_and_adjoint(torch_cuda, n, n_det, n_t, batch):
+# K5 on tcgen05 (3xTF32 GEMM; 288 leaves a ragged 32-row time tile and a 3-tile multicast
+# cluster falls back to 1 CTA, 81 an odd ragged one, 200 / 100 a ragged detector tile);
+# TAT_DENSE_TC=0: the SIMT synthesis kernel
+@pytest.mark.parametrize("n,n_det,n_t,batch,tc", [(64, 48, 128, 2, "1"), (256, 200, 512, 2, "1"),
+                                                  (128, 100, 288, 3, "1"), (64, 48, 81, 2, "1"),
+                                                  (64, 48, 128, 2, "0")])
+def test_dense_parity_and_adjoint(torch_cuda, monkeypatch, n, n_det, n_t, batch, tc):
     torch = torch_cuda
     from paper_2510_24687_b200 import Plan
+    monkeypatch.setenv("TAT_DENSE_TC", tc)
     ang = np.sort(np.random.default_rng(n).uniform(0.0, 2 * np.pi, n_det))
     C = O.derive(n, n_det, n_t, 1.0, 1.0, 2.0, ang)
     assert C.dense
