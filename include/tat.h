@@ -18,7 +18,9 @@
  *       uniform ring theta = 2 pi r / n_ring (reading G3; n_ring = the smallest multiple of 4
  *       >= n_det fitting every angle within 1e-9 rad) the angular synthesis/analysis are ring
  *       FFTs; otherwise (dense mode, reading G24) n_ring = n_phi = the smallest power of two
- *       >= max(n_det, 8) and the synthesis/analysis are dense sums at the exact angles
+ *       >= max(n_det, 8) and the synthesis/analysis are dense sums at the exact angles,
+ *       run as 3xTF32 tcgen05 GEMMs (fp32-level accuracy; TAT_DENSE_TC=0 at plan creation
+ *       selects the exact-fp32 SIMT kernels, =2 the SIMT analysis only; debugging)
  *       (tat_inverse is not available in dense mode).
  *   - Every call processes exactly `batch` images (the batch the plan was created for).
  *

@@ -323,7 +323,7 @@ cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float*
   const int JT = tile_ring(C.n_ring);
   if (ev) cudaEventRecord(ev[0], s);
   cudaError_t e = cudaSuccess;
-  if (C.dense) e = launch_k5dt(P, g, s);
+  if (C.dense) e = C.k5ttc_kp > 0 ? launch_k5dt_tc(P, g, s) : launch_k5dt(P, g, s);
   else if (ring_fast_ok(C)) e = launch_k5t(P, g, s);
   else k5t_analysis<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);
   if (e != cudaSuccess) return e;

@@ -6,9 +6,10 @@
 //   K5dT: S4[b][k][m] = sum_d g[b][m][d] conj(E5T[k][d]),        E5T = e^{i s_k k theta_d}
 //
 // (c_0 = c_K = 1, c_k = 2 otherwise; s_K = -1: row K holds the harmonic -K; its row is real,
-// reading G24).  Both are real GEMMs of shape [n_t x 2(K+1)] x [2(K+1) x n_det] per image, tiled
-// through shared memory with 8 x 8 (K5d, register-staged next chunk) / 4 x 4 register blocks
-// (exact fp32: single-pass TF32 tensor cores would miss the 1e-4 bar).
+// reading G24).  Both are real GEMMs of shape [n_t x 2(K+1)] x [2(K+1) x n_det] per image.  They
+// run on the tensor cores as 3xTF32 GEMMs (k5d_tc / k5dt_tc below; single-pass TF32 would miss
+// the 1e-4 bar); k5d_synth / k5d_anal are exact-fp32 SIMT versions (shared-memory tiles, 8 x 8 /
+// 4 x 4 register blocks) kept behind TAT_DENSE_TC=0.
 #include "tat_internal.h"
 #include "async_copy.cuh"
 
@@ -205,6 +206,54 @@ constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT 
 // exact in fp32 and the MMA reads the low part's top 19 bits, so the split keeps ~21 significant
 // bits of every operand: fp32-level products.
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// instruction descriptor of kind::tf32 with f32 accumulation, K-major A and B, M x N
+__device__ __forceinline__ uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// D[tmem d] (+)= A[tmem a] B[smem desc b]
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, bool acc) {
+  asm volatile(
+      "{\n\t.reg .pred pa;\n\tsetp.ne.b32 pa, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, pa;\n\t}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"((uint32_t)acc));
+}
+// arrive on the mbarrier at this offset in every CTA of cmask once all prior MMAs retired
+__device__ __forceinline__ void commit_mc(uint64_t* bar, uint16_t cmask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)), "h"(cmask));
+}
+// 1-D bulk copy global -> the same shared offset in every CTA of cmask (complete_tx on each bar)
+__device__ __forceinline__ void bulk_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t cmask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(cmask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31]));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 }  // namespace tc
 
 __global__ void __launch_bounds__(192, 1) k5d_tc(DevPlan P, float* __restrict__ gout) {
@@ -241,7 +290,7 @@ __global__ void __launch_bounds__(192, 1) k5d_tc(DevPlan P, float* __restrict__ 
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   // peers multicast into this CTA's slots and barriers: all barriers initialised cluster-wide first
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  cluster_sync();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tslot;
   pdl_wait();
@@ -254,12 +303,7 @@ __global__ void __launch_bounds__(192, 1) k5d_tc(DevPlan P, float* __restrict__ 
         if (ch >= kSlots) ac::mbar_wait(done + sl, ((ch - kSlots) / kSlots) & 1);
         unsigned char* dst = ring + sl * kSlot;
         ac::mbar_expect_tx(full + sl, 2 * kTile);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-            "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst + crank * bpiece)),
-            "l"(Bsrc + (size_t)ch * 2 * kTile + crank * bpiece), "r"(bpiece), "r"(smem_u32(full + sl)),
-            "h"(cmask)
-            : "memory");
+        bulk_mc(dst + crank * bpiece, Bsrc + (size_t)ch * 2 * kTile + crank * bpiece, bpiece, full + sl, cmask);
       }
   } else if (warp == 1) {
     // ---- MMA issuer: 3 TF32 products per K-step of 8, all chunks into one TMEM accumulator
@@ -275,20 +319,12 @@ __global__ void __launch_bounds__(192, 1) k5d_tc(DevPlan P, float* __restrict__ 
           const uint32_t off = k8 * 2 * kLBO;
           const uint32_t ah = ta + k8 * 8, al = ta + KC + k8 * 8;
           const uint64_t bh = desc_kmajor(b0 + off), bl = desc_kmajor(b0 + kTile + off);
-          const uint32_t xa[3] = {ah, ah, al};
-          const uint64_t xb[3] = {bh, bl, bh};
-#pragma unroll
-          for (int p = 0; p < 3; ++p) {
-            const uint32_t acc = (ch > 0 || k8 > 0 || p > 0) ? 1u : 0u;
-            asm volatile(
-                "{\n\t.reg .pred pa;\n\tsetp.ne.b32 pa, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, pa;\n\t}\n" ::"r"(tmem),
-                "r"(xa[p]), "l"(xb[p]), "r"(kIdesc), "r"(acc));
-          }
+          const bool first = ch == 0 && k8 == 0;
+          mma_tf32_ts(tmem, ah, bh, kIdesc, !first);
+          mma_tf32_ts(tmem, ah, bl, kIdesc, true);
+          mma_tf32_ts(tmem, al, bh, kIdesc, true);
         }
-        asm volatile(
-            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-            "[%0], %1;" ::"r"(smem_u32(done + sl)), "h"(cmask));
+        commit_mc(done + sl, cmask);
       }
   } else {
     // ---- converters (warps 2..5): row m = TMEM lane; raw S4 -> TF32 hi / lo columns of TMEM
@@ -327,15 +363,7 @@ __global__ void __launch_bounds__(192, 1) k5d_tc(DevPlan P, float* __restrict__ 
         v[KC + 2 * kl] = __float_as_uint(x.x - hx);
         v[KC + 2 * kl + 1] = __float_as_uint(x.y - hy);
       }
-      asm volatile(
-          "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-          "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
-          "%28, %29, %30, %31, %32};" ::"r"(tl + NT + ab * 2 * KC),
-          "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-          "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
-          "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
-          "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
-          "r"(v[29]), "r"(v[30]), "r"(v[31]));
+      tmem_st32(tl + NT + ab * 2 * KC, v);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(conv + ab)) : "memory");
@@ -346,7 +374,7 @@ __global__ void __launch_bounds__(192, 1) k5d_tc(DevPlan P, float* __restrict__ 
     __syncwarp();
     asm volatile("tcgen05.fence::before_thread_sync;");
     // no CTA leaves while a peer may still multicast into its shared memory / barriers
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    cluster_sync();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
     return;
   }
@@ -390,21 +418,194 @@ __global__ void __launch_bounds__(192, 1) k5d_tc(DevPlan P, float* __restrict__ 
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  cluster_sync();
 }
 
 size_t smem_k5d_tc() {
   return (size_t)tc::kSlots * tc::kSlot + tc::kRawD * tc::kRawA + 16 * tc::kSlots + 8 * tc::kABufs + 16;
 }
 
-cudaError_t launch_k5d_tc(const DevPlan& P, float* g, cudaStream_t s) {
+// ================================================================== K5dT on tcgen05 (3xTF32)
+// The analysis as a GEMM D[m][j] = sum_d A[m][d] B[d][j]: A = g (the traces, K-major: detectors
+// contiguous), B[d][2k] = Re E5T[k][d], B[d][2k+1] = -Im E5T[k][d] (host-packed TF32 hi / lo,
+// N tile nt = 2 (K+1) split into C.k5ttc_nb blocks of C.k5ttc_nt <= 256 columns), D[m][2k + c]
+// = (Re, Im) S4[k][m].  The same 6-warp pipeline as k5d_tc: warp 0 multicasts B chunks (16
+// detectors) across the cluster, warps 2..5 cp.async their row's 16 trace values (kRawD
+// chunks ahead), split them hi / lo into TMEM, warp 1 issues the 6 MMAs per chunk (M 128, N nt,
+// K 8; A from TMEM).  Epilogue: (Re, Im) column pairs of lane m -> S4[k][m] (coalesced in m).
+namespace tct {
+constexpr int MT = 128, KC = kK5tcKC, kSlots = 4, kABufs = 4, kRawD = 8, kNTMax = 256;
+constexpr uint32_t kRawA = MT * KC * 4;            // 16 trace values of 128 rows (8 KB)
+constexpr uint32_t kSlotMax = 2 * kNTMax * KC * 4; // B hi + lo at the widest tile (32 KB)
+constexpr uint32_t kTmemCols = 512;                // accumulator [0, 256) + A buffers [256, 384)
+}  // namespace tct
+
+__global__ void __launch_bounds__(192, 1) k5dt_tc(DevPlan P, const float* __restrict__ gin) {
+  using namespace tct;
+  extern __shared__ __align__(1024) unsigned char smraw[];
   const Consts& C = P.C;
-  const dim3 grid((C.n_det + tc::NT - 1) / tc::NT, (C.n_t + tc::MT - 1) / tc::MT, C.batch);
-  const int cs = grid.y % 4 == 0 ? 4 : grid.y % 2 == 0 ? 2 : 1;   // B multicast cluster
+  const int NTa = C.k5ttc_nt;                                   // columns of this N tile
+  const uint32_t slotb = (uint32_t)NTa * KC * 4 * 2;            // B hi + lo bytes per chunk
+  unsigned char* ring = smraw;                                   // kSlots x (B hi, B lo)
+  unsigned char* rawr = smraw + kSlots * kSlotMax;               // kRawD x raw A (cp.async)
+  uint64_t* full = reinterpret_cast<uint64_t*>(rawr + kRawD * kRawA);
+  uint64_t* done = full + kSlots;
+  uint64_t* conv = done + kSlots;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(conv + kABufs);
+  const int t = threadIdx.x, warp = t >> 5;
+  const int b = C.b0 + blockIdx.z;
+  const int m0 = blockIdx.y * MT, n0 = blockIdx.x * NTa;
+  const int nch = C.k5ttc_kp / KC;
+  const int mrows = min(MT, C.n_t - m0);
+  const unsigned char* Bsrc = reinterpret_cast<const unsigned char*>(P.k5ttc_b) + (size_t)blockIdx.x * nch * slotb;
+  uint32_t cs, crank;
+  asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(cs));
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const uint16_t cmask = (uint16_t)((1u << cs) - 1);
+  const uint32_t bpiece = slotb / cs;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tslot)), "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    for (int i = 0; i < kSlots; ++i) ac::mbar_init(full + i, 1);
+    for (int i = 0; i < kSlots; ++i) ac::mbar_init(done + i, cs);
+    for (int i = 0; i < kABufs; ++i) ac::mbar_init(conv + i, 128);
+    ac::fence_mbar_init();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  tc::cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tslot;
+  pdl_wait();
+  pdl_trigger();
+  if (warp == 0) {
+    if (t == 0)
+      for (int ch = 0; ch < nch; ++ch) {
+        const int sl = ch % kSlots;
+        if (ch >= kSlots) ac::mbar_wait(done + sl, ((ch - kSlots) / kSlots) & 1);
+        ac::mbar_expect_tx(full + sl, slotb);
+        tc::bulk_mc(ring + sl * kSlotMax + crank * bpiece, Bsrc + (size_t)ch * slotb + crank * bpiece, bpiece,
+                    full + sl, cmask);
+      }
+  } else if (warp == 1) {
+    if (t == 32) {
+      const uint32_t idesc = tc::idesc_tf32(MT, NTa);
+      for (int ch = 0; ch < nch; ++ch) {
+        const int sl = ch % kSlots, ab = ch % kABufs;
+        ac::mbar_wait(full + sl, (ch / kSlots) & 1);
+        ac::mbar_wait(conv + ab, (ch / kABufs) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t ta = tmem + kNTMax + ab * 2 * KC, b0 = tc::smem_u32(ring + sl * kSlotMax);
+        const uint32_t btile = (uint32_t)NTa * KC * 4;
+#pragma unroll
+        for (int k8 = 0; k8 < KC / 8; ++k8) {
+          const uint32_t off = k8 * 2 * tc::kLBO;
+          const uint64_t bh = tc::desc_kmajor(b0 + off), bl = tc::desc_kmajor(b0 + btile + off);
+          const bool first = ch == 0 && k8 == 0;
+          tc::mma_tf32_ts(tmem, ta + k8 * 8, bh, idesc, !first);
+          tc::mma_tf32_ts(tmem, ta + k8 * 8, bl, idesc, true);
+          tc::mma_tf32_ts(tmem, ta + KC + k8 * 8, bh, idesc, true);
+        }
+        tc::commit_mc(done + sl, cmask);
+      }
+    }
+  } else {
+    const int quarter = warp & 3, r = 32 * quarter + (t & 31);
+    const bool mok = r < mrows;
+    const uint32_t tl = tmem + ((uint32_t)(32 * quarter) << 16);
+    const float* grow = gin + ((size_t)b * C.n_t + m0 + r) * C.n_det;
+    const bool vec = (C.n_det & 3) == 0;
+    const int sw = (r >> 1) & 3;   // 16-B group swizzle: conflict-free LDS.128 read-back
+    unsigned char* rawme = rawr + r * KC * 4;
+    auto issue = [&](int ch) {
+      if (ch < nch && mok) {
+        unsigned char* d = rawme + (ch % kRawD) * kRawA;
+        const int d0 = ch * KC;
+        if (vec) {
+#pragma unroll
+          for (int q = 0; q < KC / 4; ++q)
+            if (d0 + 4 * q < C.n_det)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(d + 16 * (q ^ sw))),
+                           "l"(grow + d0 + 4 * q) : "memory");
+        } else {
+#pragma unroll
+          for (int i = 0; i < KC; ++i)
+            if (d0 + i < C.n_det)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_u32(d + 16 * ((i >> 2) ^ sw) + 4 * (i & 3))),
+                           "l"(grow + d0 + i) : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll 1
+    for (int c = 0; c < kRawD; ++c) issue(c);
+    for (int ch = 0; ch < nch; ++ch) {
+      const int ab = ch % kABufs;
+      asm volatile("cp.async.wait_group %0;" ::"n"(kRawD - 1) : "memory");
+      if (ch >= kABufs) ac::mbar_wait(done + (ch - kABufs) % kSlots, ((ch - kABufs) / kSlots) & 1);
+      const unsigned char* raw = rawme + (ch % kRawD) * kRawA;
+      const int d0 = ch * KC;
+      uint32_t v[2 * KC];
+#pragma unroll
+      for (int q = 0; q < KC / 4; ++q) {
+        float4 x = *reinterpret_cast<const float4*>(raw + 16 * (q ^ sw));
+        const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float xv = (mok && d0 + 4 * q + e < C.n_det) ? xs[e] : 0.f;
+          const float h = tc::tf32_hi(xv);
+          v[4 * q + e] = __float_as_uint(h);
+          v[KC + 4 * q + e] = __float_as_uint(xv - h);
+        }
+      }
+      tc::tmem_st32(tl + kNTMax + ab * 2 * KC, v);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(conv + ab)) : "memory");
+      issue(ch + kRawD);
+    }
+  }
+  if (warp < 2) {
+    __syncwarp();
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    tc::cluster_sync();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    return;
+  }
+  ac::mbar_wait(done + (nch - 1) % kSlots, ((nch - 1) / kSlots) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int quarter = warp & 3, row = 32 * quarter + (t & 31), m = m0 + row;
+  float2* S4 = P.S4 + (size_t)b * C.Kp * C.n_t;
+#pragma unroll 1
+  for (int cb = 0; cb < NTa / 16; ++cb) {
+    uint32_t v[16];
+    tc::tmem_ld16(tmem + ((uint32_t)(32 * quarter) << 16) + cb * 16, v);
+    if (m < C.n_t) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = (n0 + cb * 16) / 2 + q;
+        if (k < C.Kp) S4[(size_t)k * C.n_t + m] = make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  tc::cluster_sync();
+}
+
+size_t smem_k5dt_tc() {
+  return (size_t)tct::kSlots * tct::kSlotMax + tct::kRawD * tct::kRawA + 16 * tct::kSlots + 8 * tct::kABufs + 16;
+}
+
+// launch with a (1, cs, 1) cluster along the time tiles (B multicast) and optional PDL
+template <typename Kern, typename Arg>
+static cudaError_t launch_cluster(const Consts& C, Kern kern, dim3 grid, size_t smem, cudaStream_t s,
+                                  const DevPlan& P, Arg a) {
+  const int cs = grid.y % 4 == 0 ? 4 : grid.y % 2 == 0 ? 2 : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(192);
-  cfg.dynamicSmemBytes = smem_k5d_tc();
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -415,13 +616,28 @@ cudaError_t launch_k5d_tc(const DevPlan& P, float* g, cudaStream_t s) {
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = C.pdl ? 2 : 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, k5d_tc, P, g);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P, a);
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_k5d_tc(const DevPlan& P, float* g, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid((C.n_det + tc::NT - 1) / tc::NT, (C.n_t + tc::MT - 1) / tc::MT, C.batch);
+  return launch_cluster(C, k5d_tc, grid, smem_k5d_tc(), s, P, g);
+}
+
+cudaError_t launch_k5dt_tc(const DevPlan& P, const float* g, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid(C.k5ttc_nb, (C.n_t + tct::MT - 1) / tct::MT, C.batch);
+  return launch_cluster(C, k5dt_tc, grid, smem_k5dt_tc(), s, P, g);
 }
 
 cudaError_t configure_dense_kernels(const Consts& C) {
   if (!C.dense) return cudaSuccess;
-  return cudaFuncSetAttribute(k5d_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k5d_tc());
+  cudaError_t e = cudaFuncSetAttribute(k5d_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k5d_tc());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k5dt_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k5dt_tc());
+  return e;
 }
 
 }  // namespace tat

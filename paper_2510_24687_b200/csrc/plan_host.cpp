@@ -88,8 +88,13 @@ std::string derive_consts(int n, int n_det, int n_t, double R, double c, double 
     while (n_ring < n_det) n_ring *= 2;
     C.dense = 1;
     {
-      const char* ev = std::getenv("TAT_DENSE_TC");   // debug switch: 0 = SIMT synthesis
-      C.k5tc_kp = (ev && ev[0] == '0') ? 0 : (2 * (n_ring / 2 + 1) + kK5tcKC - 1) / kK5tcKC * kK5tcKC;
+      const char* ev = std::getenv("TAT_DENSE_TC");   // debug switch: 0 = SIMT K5d / K5dT, 2 = SIMT K5dT
+      const bool tc = !(ev && ev[0] == '0');
+      const int nt2 = 2 * (n_ring / 2 + 1);   // real columns of the complex harmonics 0..K
+      C.k5tc_kp = tc ? (nt2 + kK5tcKC - 1) / kK5tcKC * kK5tcKC : 0;
+      C.k5ttc_kp = (tc && !(ev && ev[0] == '2')) ? (n_det + kK5tcKC - 1) / kK5tcKC * kK5tcKC : 0;
+      C.k5ttc_nb = (nt2 + 255) / 256;
+      C.k5ttc_nt = ((nt2 + C.k5ttc_nb - 1) / C.k5ttc_nb + 15) / 16 * 16;
     }
     std::fill(ring.begin(), ring.end(), -1);
   } else {
@@ -188,6 +193,37 @@ static void unit_circle(int l, int n_phi, double& cs, double& sn) {
 
 static inline int fbits(float f) { int i; std::memcpy(&i, &f, 4); return i; }
 
+// TF32 split operand for the tcgen05 GEMMs (kernels_dense.cu): B[row][k] for nb tiles of nt rows
+// and KP (a multiple of kK5tcKC) reduction indices, packed [tile][chunk][hi, lo][nt x KC] in the
+// no-swizzle K-major core layout: element (r, k) of a tile at float offset (r / 8) * 8 KC +
+// (k / 4) * 32 + (r % 8) * 4 + k % 4.  hi = round-to-nearest TF32 (10 mantissa bits), lo = its
+// residual, rounded the same way.
+template <typename F>
+static void pack_kmajor(std::vector<float>& out, int nb, int nt, int KP, F val) {
+  constexpr int KC = kK5tcKC;
+  auto tf32 = [](float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u = (u + 0x1000u) & 0xFFFFE000u;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+  };
+  const int nch = KP / KC;
+  out.assign((size_t)nb * nt * KP * 2, 0.f);
+  for (int tb = 0; tb < nb; ++tb)
+    for (int r = 0; r < nt; ++r)
+      for (int k = 0; k < KP; ++k) {
+        const float v = val(tb * nt + r, k);
+        const size_t tile = ((size_t)tb * nch + k / KC) * 2;
+        const int kk = k % KC;
+        const size_t off = (size_t)(r / 8) * 8 * KC + (kk / 4) * 32 + (r % 8) * 4 + kk % 4;
+        const float hi = tf32(v);
+        out[tile * nt * KC + off] = hi;
+        out[(tile + 1) * nt * KC + off] = tf32(v - hi);
+      }
+}
+
 void build_tables(const Consts& C, const std::vector<int>& ring, const double* angles,
                   HostTables& H) {
   const int n = C.n, N = C.N, L = C.Lres, NL = C.NL, Kp = C.Kp, nphi = C.n_ring;
@@ -241,35 +277,18 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
     }
     if (C.k5tc_kp > 0) {   // tcgen05 synthesis operand B[2k][d] = Re E5, B[2k+1][d] = -Im E5
       const int KP = C.k5tc_kp, D = (C.n_det + 127) / 128 * 128;
-      auto tf32 = [](float x) {   // round to nearest (ties away) at 10 mantissa bits, as cvt.rna
-        uint32_t u;
-        std::memcpy(&u, &x, 4);
-        u = (u + 0x1000u) & 0xFFFFE000u;
-        float r;
-        std::memcpy(&r, &u, 4);
-        return r;
-      };
-      // packed [d block][chunk][hi, lo][core layout]: element (r, k') of a 128 x KC tile at float
-      // offset (r / 8) * 8 KC + (k' / 4) * 32 + (r % 8) * 4 + k' % 4 (8-row x 16-byte cores,
-      // K-adjacent cores 128 B apart, row groups 32 KC bytes apart: the no-swizzle K-major layout)
-      constexpr int KC = kK5tcKC;
-      const int nch = KP / KC;
-      H.k5tc_b.assign((size_t)D * KP * 2, 0.f);
-      for (int k = 0; k < C.Kp; ++k)
-        for (int d = 0; d < C.n_det; ++d) {
-          const float2 e = H.dense_e5[(size_t)k * C.n_det + d];
-          const float v[2] = {e.x, -e.y};
-          const int r = d % 128, db = d / 128;
-          for (int j = 0; j < 2; ++j) {
-            const int kp = 2 * k + j, ch = kp / KC, kk = kp % KC;
-            const size_t tile = ((size_t)db * nch + ch) * 2;
-            const size_t off = (size_t)(r / 8) * 8 * KC + (kk / 4) * 32 + (r % 8) * 4 + kk % 4;
-            const float hi = tf32(v[j]);
-            H.k5tc_b[tile * 128 * KC + off] = hi;
-            H.k5tc_b[(tile + 1) * 128 * KC + off] = tf32(v[j] - hi);
-          }
-        }
+      pack_kmajor(H.k5tc_b, D / 128, 128, KP, [&](int d, int kp) -> float {
+        if (d >= C.n_det || kp >= 2 * C.Kp) return 0.f;
+        const float2 e = H.dense_e5[(size_t)(kp / 2) * C.n_det + d];
+        return (kp & 1) ? -e.y : e.x;
+      });
     }
+    if (C.k5ttc_kp > 0)   // tcgen05 analysis operand B[d][2k] = Re E5T, B[d][2k+1] = -Im E5T
+      pack_kmajor(H.k5ttc_b, C.k5ttc_nb, C.k5ttc_nt, C.k5ttc_kp, [&](int j, int d) -> float {
+        if (d >= C.n_det || j >= 2 * C.Kp) return 0.f;
+        const float2 e = H.dense_e5t[(size_t)(j / 2) * C.n_det + d];
+        return (j & 1) ? -e.y : e.x;
+      });
   }
 
   // ---- half-plane polar nodes (Alg. 1 step 3; readings G12, G13)

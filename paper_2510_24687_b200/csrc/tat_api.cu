@@ -175,6 +175,7 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     if ((e = upload(p, H.dense_e5, &P.dense_e5, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.dense_e5t, &P.dense_e5t, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k5tc_b, &P.k5tc_b, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k5ttc_b, &P.k5ttc_b, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.tw_col, &P.tw_col, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.tw_dct4, &P.tw_dct4, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2c_mask, &P.k2c_mask, tb)) != cudaSuccess) break;

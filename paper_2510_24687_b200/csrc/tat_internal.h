@@ -17,7 +17,10 @@ struct Consts {
   int dct_sine = 0; // K4T computes sum_m G~ sin(c lambda_j t_m) (the inverse, Alg. 3 step 3)
   int pdl = 1;      // launch the chain kernels with programmatic dependent launch
   int dense = 0;    // detectors off any canonical ring: K5 / K5T as dense sums (reading G24)
-  int k5tc_kp = 0;  // dense K5 on tcgen05: padded K' = 2 (K+1) rounded up to 32 (0: SIMT path)
+  int k5tc_kp = 0;  // dense K5 on tcgen05: padded K' = 2 (K+1) rounded up to kK5tcKC (0: SIMT path)
+  int k5ttc_kp = 0; // dense K5T on tcgen05: n_det rounded up to kK5tcKC (0: SIMT path)
+  int k5ttc_nt = 0; // its N tile (<= 256, multiple of 16) and number of N tiles over 2 (K+1)
+  int k5ttc_nb = 0;
   int col_strip = 16; // K2 / K2Tb: columns per CTA (k2c_fwd recomputes one halo column;
                       // 12-16 measured best at C3, 20-32 slower)
   double R = 1, c = 1, T = 1;
@@ -62,6 +65,7 @@ struct HostTables {
   std::vector<int> ring;            // [n_det] (-1 in dense mode)
   // dense mode: E5[k][d] = c_k (cos, sin)(s_k k theta_d), E5T without c_k (s_K = -1, c = 1, 2, 1)
   std::vector<float2> dense_e5, dense_e5t;   // [Kp][n_det]
+  std::vector<float> k5ttc_b;                // tcgen05 K5dT operand B (hi / lo TF32 parts, packed)
   std::vector<float> k5tc_b;                 // tcgen05 K5d operand B (hi / lo TF32 parts, packed)
   // k2c_adj: per (column p, q0 = q mod 16L): bit q1 set if target (p, q0 + 16L q1) exists,
   // and the index of the first such target (targets of a column are ordered by (q0, q1))
@@ -102,6 +106,7 @@ struct DevPlan {
   // -(index + 1) for the conjugate mirror node) and bilinear weights
   const float2* dense_e5 = nullptr;
   const float2* dense_e5t = nullptr;
+  const float* k5ttc_b = nullptr;  // tcgen05 K5dT operand B: [n block][chunk][hi, lo][nt x 16 core layout]
   const float* k5tc_b = nullptr;   // tcgen05 K5d operand B: [d block][chunk][hi, lo][128 x 32 core layout]
   const int4* inv_nodes = nullptr;
   const float4* inv_w = nullptr;
@@ -214,6 +219,7 @@ cudaError_t launch_k5d(const DevPlan& P, float* g, cudaStream_t s);
 cudaError_t launch_k5dt(const DevPlan& P, const float* g, cudaStream_t s);
 constexpr int kK5tcKC = 16;   // tcgen05 K5d: K' chunk (real values) per pipeline slot
 cudaError_t launch_k5d_tc(const DevPlan& P, float* g, cudaStream_t s);
+cudaError_t launch_k5dt_tc(const DevPlan& P, const float* g, cudaStream_t s);
 cudaError_t configure_dense_kernels(const Consts& C);
 // kernels_inv.cu: inverse-specific stages (Alg. 3 steps 5, 7, 8)
 cudaError_t launch_k2i_interp(const DevPlan& P, cudaStream_t s);

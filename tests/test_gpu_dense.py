@@ -27,10 +27,10 @@ def _check(out, ref, what):
 
 # K5 on tcgen05 (3xTF32 GEMM; 288 leaves a ragged 32-row time tile and a 3-tile multicast
 # cluster falls back to 1 CTA, 81 an odd ragged one, 200 / 100 a ragged detector tile);
-# TAT_DENSE_TC=0: the SIMT synthesis kernel
+# TAT_DENSE_TC=0: the SIMT synthesis / analysis kernels, =2 SIMT analysis only
 @pytest.mark.parametrize("n,n_det,n_t,batch,tc", [(64, 48, 128, 2, "1"), (256, 200, 512, 2, "1"),
                                                   (128, 100, 288, 3, "1"), (64, 48, 81, 2, "1"),
-                                                  (64, 48, 128, 2, "0")])
+                                                  (64, 48, 128, 2, "0"), (256, 200, 512, 2, "2")])
 def test_dense_parity_and_adjoint(torch_cuda, monkeypatch, n, n_det, n_t, batch, tc):
     torch = torch_cuda
     from paper_2510_24687_b200 import Plan
