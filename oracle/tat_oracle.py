@@ -414,6 +414,37 @@ def adjoint(g: np.ndarray, C: Constants) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------------------------
+# Low-harmonic quadrature variant (reading G25).  PAPER.md L510-513: for
+# k in {-1, 0, 1} "a quadrature rule with discretization points clustering toward lambda = 0".
+# The paper gives no law or node count.  Reading G25: the variant adds what such a rule
+# converges to, the Euler-Maclaurin endpoint term of the trapezoid rule at lambda = 0,
+#     int_0^Lam phi = sum_j w_j dlam phi(lambda_j) + (dlam^2/12) phi'(0) + O(dlam^4),
+# with phi_k(lambda) = lambda J_|k|(R lambda) fhat_k(lambda) cos(c lambda t) (D4-D5).  For k = 0,
+# phi_0'(0) = fhat_0(0) = F(0, 0) = (h^2/2pi) sum f (D1 at the origin: every polar node at
+# lambda = 0 is the Cartesian origin); for k = +-1, phi ~ lambda^3 and the term vanishes.  So
+# G_0(t) gains the constant (dlam^2/12)(h^2/2pi) sum f, and D6-D7 carry it unchanged to every
+# (t_m, detector).  The adjoint gains the transpose of that rank-one term, times omega.
+
+def lowk_coefficient(C: Constants) -> float:
+    """(dlam^2 / 12) (h^2 / 2 pi): the G25 constant per unit sum of f."""
+    return (C.dlam ** 2 / 12.0) * (C.h * C.h / (2.0 * math.pi))
+
+
+def forward_lowk(f: np.ndarray, C: Constants) -> np.ndarray:
+    """A f with the G25 low-harmonic quadrature: forward(f) + c_G25 sum(f) on every sample."""
+    f = np.asarray(f, np.float64)
+    s = f.sum(axis=(-2, -1))
+    return forward(f, C) + (lowk_coefficient(C) * s)[..., None, None]
+
+
+def adjoint_lowk(g: np.ndarray, C: Constants) -> np.ndarray:
+    """The L2 adjoint of forward_lowk: adjoint(g) + omega c_G25 sum(g) on every pixel."""
+    g = np.asarray(g, np.float64)
+    s = g.sum(axis=(-2, -1))
+    return adjoint(g, C) + (C.omega * lowk_coefficient(C) * s)[..., None, None]
+
+
+# ---------------------------------------------------------------------------------------------
 # Iterative reconstruction (SURVEY §8(f) f2): NNLS as projected gradient descent,
 # PAPER.md §4.2 "Reconstruction methods" L838-850, with the gradient of the data fidelity
 # E:operators (L164-167): grad ||A f - g||^2 = 2 A*(A f - g).
