@@ -105,6 +105,23 @@ tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_
 tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0,
                        cudaStream_t stream);
 
+/* ---- Quadrature in lambda (DESIGN reading G25).  PAPER.md L510-513 asks
+ * for "a quadrature rule with discretization points clustering toward lambda = 0" for the
+ * harmonics k in {-1, 0, 1} without a law; the default is the uniform trapezoid for every k
+ * (reading G9), whose k = 0 endpoint error is the t-independent offset -(dlam^2/12) fhat_0(0).
+ *   TAT_QUAD_TRAPEZOID  the base definition (default).
+ *   TAT_QUAD_LOWK       adds the trapezoid's Euler-Maclaurin endpoint term at lambda = 0, what a
+ *                       rule clustering at 0 converges to: A f gains (dlam^2/12)(h^2/2pi) sum f
+ *                       on every sample (k = +-1 need no term at this order), A* the adjoint
+ *                       omega (dlam^2/12)(h^2/2pi) sum g on every pixel; one extra reduction
+ *                       kernel per call, added in the last kernel's epilogue.
+ * Applies to tat_forward / tat_adjoint and everything built on them (scaled forward, transpose,
+ * residual, adjoint step, NNLS, power norm); tat_inverse is unaffected.  Not thread-safe with
+ * calls in flight on the plan (the per-image constants live in the plan's workspace). */
+#define TAT_QUAD_TRAPEZOID 0
+#define TAT_QUAD_LOWK 1
+tat_status tat_plan_set_quadrature(tat_plan* plan, int rule);
+
 /* ---- Euclidean transposes for reverse-mode autodiff.  A* is the L2
  * adjoint omega A^T (reading G20); a framework's backward pass needs the Euclidean transpose:
  *   d/df <A f, w>  = A^T w      -> tat_transpose(g = w, f = out):  out = A^T w = A* w / omega

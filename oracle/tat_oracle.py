@@ -445,6 +445,34 @@ def adjoint_lowk(g: np.ndarray, C: Constants) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------------------------
+# De-apodised bilinear variant (reading G26; not in the paper).  Bilinear
+# interpolation of F on the Cartesian frequency grid (pitch dxi = pi/L, D2) is, to leading order,
+# the exact polar sampling of the transform of K f, K(x) = sinc^2(x1/2L) sinc^2(x2/2L) with
+# sinc(u) = sin(pi u)/(pi u) (the Fourier dual of the hat kernel; DESIGN G9 error model).  The
+# variant pre-divides f by K on the image nodes: A_D = A D, D = diag(1/K(x)), so A_D f ~ A_cont f.
+# Its L2 adjoint (the X inner product has a constant weight) is D A*.
+
+def deapod_weights(C: Constants) -> np.ndarray:
+    """D[iy, ix] = 1 / (K(x_ix) K(y_iy)), x_i = (i - n/2) h (the D1 node positions)."""
+    x = (np.arange(C.n) - C.n // 2) * C.h
+    k = np.sinc(x / (2.0 * C.L)) ** 2
+    return 1.0 / np.outer(k, k)
+
+
+def forward_variant(f: np.ndarray, C: Constants, lowk: bool = False, deapod: bool = False) -> np.ndarray:
+    """A with the f4 variants: fd = D f (deapod), then forward (+ the G25 term on fd if lowk)."""
+    f = np.asarray(f, np.float64)
+    fd = f * deapod_weights(C) if deapod else f
+    return forward_lowk(fd, C) if lowk else forward(fd, C)
+
+
+def adjoint_variant(g: np.ndarray, C: Constants, lowk: bool = False, deapod: bool = False) -> np.ndarray:
+    """The L2 adjoint of forward_variant: (adjoint_lowk or adjoint)(g), then times D."""
+    u = adjoint_lowk(g, C) if lowk else adjoint(g, C)
+    return u * deapod_weights(C) if deapod else u
+
+
+# ---------------------------------------------------------------------------------------------
 # Iterative reconstruction (SURVEY §8(f) f2): NNLS as projected gradient descent,
 # PAPER.md §4.2 "Reconstruction methods" L838-850, with the gradient of the data fidelity
 # E:operators (L164-167): grad ||A f - g||^2 = 2 A*(A f - g).

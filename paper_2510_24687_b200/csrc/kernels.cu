@@ -293,7 +293,11 @@ cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float*
   const int B = C.batch;
   const int JT = tile_ring(C.n_ring);
   if (ev) cudaEventRecord(ev[0], s);
-  cudaError_t e = launch_k1(P, tm, f, s);
+  cudaError_t e = cudaSuccess;
+  if (P.lowk_add)   // reading G25: c sum(f) per image, added in the last kernel's epilogue
+    e = launch_lowk_sum(P, f, (size_t)C.n * C.n, C.lowk_c, s);
+  if (e != cudaSuccess) return e;
+  e = launch_k1(P, tm, f, s);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
   e = launch_k2(P, s);
@@ -323,6 +327,10 @@ cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float*
   const int JT = tile_ring(C.n_ring);
   if (ev) cudaEventRecord(ev[0], s);
   cudaError_t e = cudaSuccess;
+  if (P.lowk_add)   // reading G25: omega c sum(g) per image, added in K1T's epilogue
+    e = launch_lowk_sum(P, g, (size_t)C.n_t * C.n_det,
+                        C.omega * C.lowk_c, s);
+  if (e != cudaSuccess) return e;
   if (C.dense) e = C.k5ttc_kp > 0 ? launch_k5dt_tc(P, g, s) : launch_k5dt(P, g, s);
   else if (ring_fast_ok(C)) e = launch_k5t(P, g, s);
   else k5t_analysis<<<dim3((C.n_t + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P, g);

@@ -52,4 +52,39 @@ cudaError_t launch_dot_partial(const float* a, const float* b, size_t count, flo
   return cudaGetLastError();
 }
 
+// Reading G25 (low-harmonic quadrature variant): out[b] = coef * sum of image b, accumulated in
+// float64 by one 1024-thread CTA per image (16-byte loads when the image is 16-byte aligned).
+__global__ void __launch_bounds__(1024) k_lowk_sum(const float* __restrict__ x, size_t per, int b0, double coef,
+                                                   float* __restrict__ out) {
+  __shared__ double red[32];
+  pdl_trigger();
+  const int b = b0 + blockIdx.x;
+  const float* p = x + (size_t)b * per;
+  double acc = 0.0;
+  if ((per & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+    for (size_t i = threadIdx.x; i < per / 4; i += blockDim.x) {
+      const float4 v = __ldg(q + i);
+      acc += ((double)v.x + (double)v.y) + ((double)v.z + (double)v.w);
+    }
+  } else {
+    for (size_t i = threadIdx.x; i < per; i += blockDim.x) acc += (double)__ldg(p + i);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = red[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) out[b] = (float)(coef * acc);
+  }
+}
+
+cudaError_t launch_lowk_sum(const DevPlan& P, const float* x, size_t per_image, double coef, cudaStream_t s) {
+  k_lowk_sum<<<P.C.batch, 1024, 0, s>>>(x, per_image, P.C.b0, coef, P.lowk_add);
+  return cudaGetLastError();
+}
+
 }  // namespace tat

@@ -57,6 +57,7 @@ std::string derive_consts(int n, int n_det, int n_t, double R, double c, double 
   C.M = (int)Mf;
   C.T_new = C.M * c * C.dt;
   C.dlam = kPi / C.T_new;
+  C.lowk_c = (C.dlam * C.dlam / 12.0) * (C.h * C.h / (2.0 * kPi));
   C.lam_max = kPi / C.h;
   C.J = (int)std::floor(C.lam_max / C.dlam + 1e-9);
   C.NL = C.J + 1;

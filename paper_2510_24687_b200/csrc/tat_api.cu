@@ -24,6 +24,7 @@ struct tat_plan {
   float* stage_out = nullptr;   // [B][n_t][n_det]
   float* pw_img = nullptr;      // power iteration: second image buffer [B][n][n]
   float* pw_part = nullptr;     // kUtilBlocks partial dot products
+  float* lowk_buf = nullptr;    // [B] G25 per-image constants (tat_plan_set_quadrature)
   // inverse (built on first use)
   std::vector<int> node_perm;   // host copy: (j, l') -> adjoint S2 position
   bool inv_ready = false;
@@ -333,6 +334,24 @@ tat_status tat_transpose(const tat_plan* plan, const float* g, float* f, cudaStr
   return TAT_OK;
 }
 
+tat_status tat_plan_set_quadrature(tat_plan* plan, int rule) {
+  if (!plan) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (rule != TAT_QUAD_TRAPEZOID && rule != TAT_QUAD_LOWK)
+    return fail(TAT_ERR_INVALID_ARGUMENT, "unknown quadrature rule");
+  if (rule == TAT_QUAD_TRAPEZOID) {
+    plan->P.lowk_add = nullptr;
+    return TAT_OK;
+  }
+  if (!plan->lowk_buf) {
+    void* d = nullptr;
+    cudaError_t e = alloc_ws(plan, (size_t)plan->P.C.batch * sizeof(float), &d);
+    if (e != cudaSuccess) return cuda_fail(e, "tat_plan_set_quadrature alloc");
+    plan->lowk_buf = (float*)d;
+  }
+  plan->P.lowk_add = plan->lowk_buf;
+  return TAT_OK;
+}
+
 tat_status tat_forward_scaled(const tat_plan* plan, const float* f, float* g, float alpha,
                               cudaStream_t stream) {
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
@@ -378,6 +397,7 @@ static tat_status inverse_setup(tat_plan* p) {
   if (e != cudaSuccess) return cuda_fail(e, "inverse tables");
   if (col_ok(Q.C) && smem_k2c_adj(Q.C) > 227 * 1024)
     return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: column target buffer exceeds shared memory");
+  Q.lowk_add = nullptr;   // A^{-1} (Algorithm 3) has no quadrature variant
   p->Pinv = Q;
   p->inv_ready = true;
   return TAT_OK;

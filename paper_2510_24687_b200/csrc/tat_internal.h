@@ -26,6 +26,7 @@ struct Consts {
   double R = 1, c = 1, T = 1;
   double h = 0, T_new0 = 0, T_new = 0, Lbox = 0, dxi = 0, dt = 0, dlam = 0, lam_max = 0;
   double wJ = 1, omega = 0;
+  double lowk_c = 0;   // reading G25: (dlam^2 / 12) (h^2 / 2 pi)
   int N = 0;        // Cartesian FFT size
   int Lres = 0;     // residues N / n (oversampling factor, power of two)
   int log2L = 0;
@@ -125,6 +126,10 @@ struct DevPlan {
   float epi_scale = 1.f;   // forward: stores epi_scale * (A f) (- epi_sub)
   float epi_tau = 0.f;
   int epi_update = 0;
+  // low-harmonic quadrature variant (reading G25; tat_plan_set_quadrature): when set, [batch]
+  // per-image constants (coef * sum of the call's input image / data), written by k_lowk_sum
+  // at the start of each forward / adjoint call and added to every output in the epilogues
+  float* lowk_add = nullptr;
 };
 
 #ifdef __CUDACC__
@@ -153,11 +158,13 @@ cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, 
 
 // forward epilogue: value at flat output index i of g
 __device__ __forceinline__ float epi_fwd(const DevPlan& P, size_t i, float v) {
+  if (P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n_t * P.C.n_det)];
   v *= P.epi_scale;
   return P.epi_sub ? v - __ldg(&P.epi_sub[i]) : v;
 }
 // adjoint epilogue: store value v of A* g at flat index i of f (pixel ixy = i mod n^2)
 __device__ __forceinline__ void epi_adj_store(const DevPlan& P, float* f, size_t i, int ixy, float v) {
+  if (P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n * P.C.n)];
   if (P.epi_update) {
     float o = f[i] - P.epi_tau * v;
     if (P.epi_update == 2) o = fmaxf(o, 0.f);
@@ -245,6 +252,8 @@ constexpr int kUtilBlocks = 296;
 cudaError_t launch_fill_random(float* v, size_t count, unsigned long long seed, cudaStream_t s);
 cudaError_t launch_scale(float* v, size_t count, float f, cudaStream_t s);
 cudaError_t launch_dot_partial(const float* a, const float* b, size_t count, float* partial, cudaStream_t s);
+// G25: P.lowk_add[b] = coef * sum of image b of x (per_image floats each), b = b0 .. b0 + batch - 1
+cudaError_t launch_lowk_sum(const DevPlan& P, const float* x, size_t per_image, double coef, cudaStream_t s);
 
 constexpr int kLaunchesForward = 5;
 constexpr int kLaunchesAdjoint = 6;   // K5T K4T K3T K2Ta K2Tb K1T

@@ -26,7 +26,9 @@ EXPORTS = ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
            "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
            "tat_transpose", "tat_forward_scaled", "tat_inverse",
            "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm",
-           "tat_status_string", "tat_last_error")
+           "tat_plan_set_quadrature", "tat_status_string", "tat_last_error")
+
+QUAD_TRAPEZOID, QUAD_LOWK = 0, 1   # tat_plan_set_quadrature rules (DESIGN reading G25)
 
 
 class TatError(RuntimeError):
@@ -79,6 +81,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.tat_profile_end.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ip, ip]
     f32 = ctypes.c_float
     lib.tat_transpose.argtypes = [vp, vp, vp, vp]
+    lib.tat_plan_set_quadrature.argtypes = [vp, i]
     lib.tat_inverse.argtypes = [vp, vp, vp, d, vp]
     lib.tat_forward_scaled.argtypes = [vp, vp, vp, f32, vp]
     lib.tat_residual.argtypes = [vp, vp, vp, vp, vp]
@@ -93,7 +96,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "tat_adjoint_host", "tat_plan_info", "tat_plan_derive",
                  "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
                  "tat_transpose", "tat_forward_scaled", "tat_inverse",
-                 "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm"):
+                 "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm",
+                 "tat_plan_set_quadrature"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -152,6 +156,7 @@ class Plan:
                                          a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         self._h = h
         self.n, self.n_det, self.n_t, self.batch = n, n_det, n_t, batch
+        self.quadrature = "trapezoid"
         self.info = self._info()
 
     def _info(self):
@@ -199,6 +204,13 @@ class Plan:
         _check(self._lib.tat_adjoint(self._h, ctypes.c_void_p(g.data_ptr()),
                                      ctypes.c_void_p(f.data_ptr()), self._stream(stream)))
         return f
+
+    def set_quadrature(self, rule):
+        """"trapezoid" (default, reading G9) or "lowk" (reading G25: the trapezoid plus its
+        Euler-Maclaurin endpoint term at lambda = 0 for the k = 0 harmonic)."""
+        code = {"trapezoid": QUAD_TRAPEZOID, "lowk": QUAD_LOWK}.get(rule, rule)
+        _check(self._lib.tat_plan_set_quadrature(self._h, int(code)))
+        self.quadrature = {QUAD_TRAPEZOID: "trapezoid", QUAD_LOWK: "lowk"}[int(code)]
 
     def transpose(self, g, out=None, stream=None):
         """f = A^T g (Euclidean transpose, = A* g / omega): the backward of A."""
