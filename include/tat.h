@@ -122,6 +122,18 @@ tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0
 #define TAT_QUAD_LOWK 1
 tat_status tat_plan_set_quadrature(tat_plan* plan, int rule);
 
+/* ---- Cartesian -> polar interpolation (DESIGN reading G26; not in the
+ * paper).  Bilinear interpolation on the frequency grid of pitch pi/L samples, to leading order,
+ * the transform of K f with K(x) = sinc^2(x1/2L) sinc^2(x2/2L), sinc(u) = sin(pi u)/(pi u).
+ *   TAT_INTERP_BILINEAR  the paper's rule (default).
+ *   TAT_INTERP_DEAPOD    A_D = A D, D = diag(1/K) on the pixel nodes x_i = (i - n/2) h: K1 scales
+ *                        its input rows, and A_D* = D A* (K1T's epilogue).  No extra launches.
+ * Same scope and caveats as tat_plan_set_quadrature (tat_inverse unaffected); the two combine
+ * (the G25 term is then taken on D f). */
+#define TAT_INTERP_BILINEAR 0
+#define TAT_INTERP_DEAPOD 1
+tat_status tat_plan_set_interpolation(tat_plan* plan, int rule);
+
 /* ---- Euclidean transposes for reverse-mode autodiff.  A* is the L2
  * adjoint omega A^T (reading G20); a framework's backward pass needs the Euclidean transpose:
  *   d/df <A f, w>  = A^T w      -> tat_transpose(g = w, f = out):  out = A^T w = A* w / omega

@@ -295,7 +295,7 @@ cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float*
   if (ev) cudaEventRecord(ev[0], s);
   cudaError_t e = cudaSuccess;
   if (P.lowk_add)   // reading G25: c sum(f) per image, added in the last kernel's epilogue
-    e = launch_lowk_sum(P, f, (size_t)C.n * C.n, C.lowk_c, s);
+    e = launch_lowk_sum(P, f, (size_t)C.n * C.n, C.lowk_c, true, s);
   if (e != cudaSuccess) return e;
   e = launch_k1(P, tm, f, s);
   if (e != cudaSuccess) return e;
@@ -328,8 +328,7 @@ cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float*
   if (ev) cudaEventRecord(ev[0], s);
   cudaError_t e = cudaSuccess;
   if (P.lowk_add)   // reading G25: omega c sum(g) per image, added in K1T's epilogue
-    e = launch_lowk_sum(P, g, (size_t)C.n_t * C.n_det,
-                        C.omega * C.lowk_c, s);
+    e = launch_lowk_sum(P, g, (size_t)C.n_t * C.n_det, C.omega * C.lowk_c, false, s);
   if (e != cudaSuccess) return e;
   if (C.dense) e = C.k5ttc_kp > 0 ? launch_k5dt_tc(P, g, s) : launch_k5dt(P, g, s);
   else if (ring_fast_ok(C)) e = launch_k5t(P, g, s);

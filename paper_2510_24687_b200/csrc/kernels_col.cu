@@ -377,6 +377,15 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPl
 #pragma unroll
     for (int r = 0; r < G::R; ++r)
       x[r] = make_float2(rows[(2 * pr) * n + j + G::J * r], rows[(2 * pr + 1) * n + j + G::J * r]);
+    if (P.deapod) {   // reading G26: f / K on the nodes, K separable
+      const float w0 = P.deapod[y0 + 2 * pr], w1 = P.deapod[y0 + 2 * pr + 1];
+#pragma unroll
+      for (int r = 0; r < G::R; ++r) {
+        const float cw = P.deapod[j + G::J * r];
+        x[r].x *= cw * w0;
+        x[r].y *= cw * w1;
+      }
+    }
     stage_a_fwd<G>(x, A, pw, pr ? W1 : W0, j, sg);
   }
   __syncthreads();   // (also: every thread is done with the rows before stg is reused)

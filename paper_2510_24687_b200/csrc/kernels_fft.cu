@@ -193,6 +193,17 @@ __global__ void __launch_bounds__(1024) k1_fwd(DevPlan P, const __grid_constant_
       xa[r] = make_float2(__ldg(&r0[xi]), __ldg(&r0[n + xi]));
       xb[r] = make_float2(__ldg(&r0[2 * n + xi]), __ldg(&r0[3 * n + xi]));
     }
+    if (P.deapod) {   // reading G26: f / K on the nodes, K separable
+      const float w0 = P.deapod[y0], w1 = P.deapod[y0 + 1], w2 = P.deapod[y0 + 2], w3 = P.deapod[y0 + 3];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const float cw = P.deapod[j + (r < 4 ? n / 2 + r * (n / 8) : (r - 4) * (n / 8))];
+        xa[r].x *= cw * w0;
+        xa[r].y *= cw * w1;
+        xb[r].x *= cw * w2;
+        xb[r].y *= cw * w3;
+      }
+    }
   }
   int iA, iB;
   {

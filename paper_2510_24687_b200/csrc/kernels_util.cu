@@ -55,13 +55,19 @@ cudaError_t launch_dot_partial(const float* a, const float* b, size_t count, flo
 // Reading G25 (low-harmonic quadrature variant): out[b] = coef * sum of image b, accumulated in
 // float64 by one 1024-thread CTA per image (16-byte loads when the image is 16-byte aligned).
 __global__ void __launch_bounds__(1024) k_lowk_sum(const float* __restrict__ x, size_t per, int b0, double coef,
-                                                   float* __restrict__ out) {
+                                                   const float* __restrict__ dw, int n, float* __restrict__ out) {
   __shared__ double red[32];
   pdl_trigger();
   const int b = b0 + blockIdx.x;
   const float* p = x + (size_t)b * per;
   double acc = 0.0;
-  if ((per & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+  if (dw) {   // image sum of D f (reading G26)
+    for (int iy = threadIdx.x >> 5; iy < n; iy += blockDim.x >> 5) {
+      double row = 0.0;
+      for (int ix = threadIdx.x & 31; ix < n; ix += 32) row += (double)__ldg(p + (size_t)iy * n + ix) * dw[ix];
+      acc += row * dw[iy];
+    }
+  } else if ((per & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
     const float4* q = reinterpret_cast<const float4*>(p);
     for (size_t i = threadIdx.x; i < per / 4; i += blockDim.x) {
       const float4 v = __ldg(q + i);
@@ -82,8 +88,10 @@ __global__ void __launch_bounds__(1024) k_lowk_sum(const float* __restrict__ x, 
   }
 }
 
-cudaError_t launch_lowk_sum(const DevPlan& P, const float* x, size_t per_image, double coef, cudaStream_t s) {
-  k_lowk_sum<<<P.C.batch, 1024, 0, s>>>(x, per_image, P.C.b0, coef, P.lowk_add);
+cudaError_t launch_lowk_sum(const DevPlan& P, const float* x, size_t per_image, double coef, bool image,
+                            cudaStream_t s) {
+  k_lowk_sum<<<P.C.batch, 1024, 0, s>>>(x, per_image, P.C.b0, coef, image ? P.deapod : nullptr, P.C.n,
+                                        P.lowk_add);
   return cudaGetLastError();
 }
 

@@ -25,6 +25,7 @@ struct tat_plan {
   float* pw_img = nullptr;      // power iteration: second image buffer [B][n][n]
   float* pw_part = nullptr;     // kUtilBlocks partial dot products
   float* lowk_buf = nullptr;    // [B] G25 per-image constants (tat_plan_set_quadrature)
+  const float* deapod_buf = nullptr;   // [n] G26 factors (tat_plan_set_interpolation)
   // inverse (built on first use)
   std::vector<int> node_perm;   // host copy: (j, l') -> adjoint S2 position
   bool inv_ready = false;
@@ -352,6 +353,32 @@ tat_status tat_plan_set_quadrature(tat_plan* plan, int rule) {
   return TAT_OK;
 }
 
+tat_status tat_plan_set_interpolation(tat_plan* plan, int rule) {
+  if (!plan) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (rule != TAT_INTERP_BILINEAR && rule != TAT_INTERP_DEAPOD)
+    return fail(TAT_ERR_INVALID_ARGUMENT, "unknown interpolation rule");
+  if (rule == TAT_INTERP_BILINEAR) {
+    plan->P.deapod = nullptr;
+    return TAT_OK;
+  }
+  if (!plan->deapod_buf) {
+    const Consts& C = plan->P.C;
+    std::vector<float> w(C.n);
+    for (int i = 0; i < C.n; ++i) {   // 1 / sinc^2(x / 2L), x = (i - n/2) h, sinc(u) = sin(pi u)/(pi u)
+      const double u = 3.14159265358979323846 * (i - C.n / 2) * C.h / (2.0 * C.Lbox);
+      const double s = (u == 0.0) ? 1.0 : std::sin(u) / u;
+      w[i] = (float)(1.0 / (s * s));
+    }
+    size_t tb = 0;
+    const float* d = nullptr;
+    cudaError_t e = upload(plan, w, &d, tb);
+    if (e != cudaSuccess) return cuda_fail(e, "tat_plan_set_interpolation upload");
+    plan->deapod_buf = d;
+  }
+  plan->P.deapod = plan->deapod_buf;
+  return TAT_OK;
+}
+
 tat_status tat_forward_scaled(const tat_plan* plan, const float* f, float* g, float alpha,
                               cudaStream_t stream) {
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
@@ -397,7 +424,8 @@ static tat_status inverse_setup(tat_plan* p) {
   if (e != cudaSuccess) return cuda_fail(e, "inverse tables");
   if (col_ok(Q.C) && smem_k2c_adj(Q.C) > 227 * 1024)
     return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: column target buffer exceeds shared memory");
-  Q.lowk_add = nullptr;   // A^{-1} (Algorithm 3) has no quadrature variant
+  Q.lowk_add = nullptr;   // A^{-1} (Algorithm 3) has no quadrature / interpolation variant
+  Q.deapod = nullptr;
   p->Pinv = Q;
   p->inv_ready = true;
   return TAT_OK;

@@ -130,6 +130,9 @@ struct DevPlan {
   // per-image constants (coef * sum of the call's input image / data), written by k_lowk_sum
   // at the start of each forward / adjoint call and added to every output in the epilogues
   float* lowk_add = nullptr;
+  // de-apodised bilinear variant (reading G26; tat_plan_set_interpolation): [n] factors
+  // 1 / sinc^2(x_i / 2L); K1 scales f[iy][ix] by d[ix] d[iy], K1T's epilogue its output likewise
+  const float* deapod = nullptr;
 };
 
 #ifdef __CUDACC__
@@ -165,6 +168,7 @@ __device__ __forceinline__ float epi_fwd(const DevPlan& P, size_t i, float v) {
 // adjoint epilogue: store value v of A* g at flat index i of f (pixel ixy = i mod n^2)
 __device__ __forceinline__ void epi_adj_store(const DevPlan& P, float* f, size_t i, int ixy, float v) {
   if (P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n * P.C.n)];
+  if (P.deapod) v *= P.deapod[ixy % P.C.n] * P.deapod[ixy / P.C.n];
   if (P.epi_update) {
     float o = f[i] - P.epi_tau * v;
     if (P.epi_update == 2) o = fmaxf(o, 0.f);
@@ -253,7 +257,9 @@ cudaError_t launch_fill_random(float* v, size_t count, unsigned long long seed, 
 cudaError_t launch_scale(float* v, size_t count, float f, cudaStream_t s);
 cudaError_t launch_dot_partial(const float* a, const float* b, size_t count, float* partial, cudaStream_t s);
 // G25: P.lowk_add[b] = coef * sum of image b of x (per_image floats each), b = b0 .. b0 + batch - 1
-cudaError_t launch_lowk_sum(const DevPlan& P, const float* x, size_t per_image, double coef, cudaStream_t s);
+// (forward: weighted by the G26 factors when P.deapod is set)
+cudaError_t launch_lowk_sum(const DevPlan& P, const float* x, size_t per_image, double coef, bool image,
+                            cudaStream_t s);
 
 constexpr int kLaunchesForward = 5;
 constexpr int kLaunchesAdjoint = 6;   // K5T K4T K3T K2Ta K2Tb K1T

@@ -26,9 +26,11 @@ EXPORTS = ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
            "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
            "tat_transpose", "tat_forward_scaled", "tat_inverse",
            "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm",
-           "tat_plan_set_quadrature", "tat_status_string", "tat_last_error")
+           "tat_plan_set_quadrature", "tat_plan_set_interpolation", "tat_status_string",
+           "tat_last_error")
 
-QUAD_TRAPEZOID, QUAD_LOWK = 0, 1   # tat_plan_set_quadrature rules (DESIGN reading G25)
+QUAD_TRAPEZOID, QUAD_LOWK = 0, 1        # tat_plan_set_quadrature rules (DESIGN reading G25)
+INTERP_BILINEAR, INTERP_DEAPOD = 0, 1   # tat_plan_set_interpolation rules (reading G26)
 
 
 class TatError(RuntimeError):
@@ -82,6 +84,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     f32 = ctypes.c_float
     lib.tat_transpose.argtypes = [vp, vp, vp, vp]
     lib.tat_plan_set_quadrature.argtypes = [vp, i]
+    lib.tat_plan_set_interpolation.argtypes = [vp, i]
     lib.tat_inverse.argtypes = [vp, vp, vp, d, vp]
     lib.tat_forward_scaled.argtypes = [vp, vp, vp, f32, vp]
     lib.tat_residual.argtypes = [vp, vp, vp, vp, vp]
@@ -97,7 +100,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
                  "tat_transpose", "tat_forward_scaled", "tat_inverse",
                  "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm",
-                 "tat_plan_set_quadrature"):
+                 "tat_plan_set_quadrature", "tat_plan_set_interpolation"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -157,6 +160,7 @@ class Plan:
         self._h = h
         self.n, self.n_det, self.n_t, self.batch = n, n_det, n_t, batch
         self.quadrature = "trapezoid"
+        self.interpolation = "bilinear"
         self.info = self._info()
 
     def _info(self):
@@ -211,6 +215,13 @@ class Plan:
         code = {"trapezoid": QUAD_TRAPEZOID, "lowk": QUAD_LOWK}.get(rule, rule)
         _check(self._lib.tat_plan_set_quadrature(self._h, int(code)))
         self.quadrature = {QUAD_TRAPEZOID: "trapezoid", QUAD_LOWK: "lowk"}[int(code)]
+
+    def set_interpolation(self, rule):
+        """"bilinear" (default, the paper's) or "deapod" (reading G26: f pre-divided by the
+        bilinear window K(x), A_D = A diag(1/K))."""
+        code = {"bilinear": INTERP_BILINEAR, "deapod": INTERP_DEAPOD}.get(rule, rule)
+        _check(self._lib.tat_plan_set_interpolation(self._h, int(code)))
+        self.interpolation = {INTERP_BILINEAR: "bilinear", INTERP_DEAPOD: "deapod"}[int(code)]
 
     def transpose(self, g, out=None, stream=None):
         """f = A^T g (Euclidean transpose, = A* g / omega): the backward of A."""

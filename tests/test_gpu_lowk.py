@@ -83,3 +83,35 @@ def test_lowk_driver_and_transpose(torch_cuda):
         ref_r = O.forward_lowk(f[b].astype(np.float64), C) - gobs[b]
         _check(r[b].cpu().numpy(), ref_r, f"residual {b}")
         _check(wt[b].cpu().numpy(), O.adjoint_lowk(gobs[b].astype(np.float64), C) / C.omega, f"A^T {b}")
+
+
+@pytest.mark.parametrize("name,lowk,n_override", [("C1", False, None), ("C2", True, None),
+                                                 ("C1", True, 64)])
+def test_deapod_parity_and_adjoint(torch_cuda, name, lowk, n_override):
+    """G26 (with and without G25) on the first-generation engine (n = 128, 64) and the
+    two-stage engine (n = 256), against forward_variant / adjoint_variant."""
+    torch = torch_cuda
+    from paper_2510_24687_b200 import Plan
+    base = _geo(name, 2)
+    n = n_override or base.n
+    geo = synth.Geometry(n, base.n_det, base.n_t, base.R, base.c, base.T, 2, angles=base.angles)
+    C = O.derive_geom(geo)
+    plan = Plan(geo.n, geo.n_det, geo.n_t, geo.R, geo.c, geo.T, 2, geo.angles_array())
+    plan.set_interpolation("deapod")
+    if lowk:
+        plan.set_quadrature("lowk")
+    f = np.stack([synth.phantom("C1", b, n=n) for b in range(2)])
+    gd = np.stack([synth.random_data(geo.n_t, geo.n_det, 70 + b) for b in range(2)])
+    g = plan.forward(torch.from_numpy(f).cuda())
+    u = plan.adjoint(torch.from_numpy(gd).cuda())
+    torch.cuda.synchronize()
+    gh, uh = g.cpu().numpy(), u.cpu().numpy()
+    for b in range(2):
+        _check(gh[b], O.forward_variant(f[b], C, lowk, True), f"A_D {b}")
+        _check(uh[b], O.adjoint_variant(gd[b], C, lowk, True), f"A_D* {b}")
+    wY = C.dt * 2 * np.pi * C.R / C.n_ring
+    wX = C.h * C.h
+    Af = gh.astype(np.float64)
+    lhs = wY * np.sum(Af * gd)
+    rhs = wX * np.sum(f.astype(np.float64) * uh)
+    assert abs(lhs - rhs) <= 1e-5 * np.sqrt(wY * np.sum(Af * Af)) * np.sqrt(wY * np.sum(gd.astype(np.float64) ** 2))
