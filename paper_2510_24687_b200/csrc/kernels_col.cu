@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPl
 constexpr int kK1BoxP = 128;   // p extent of one S1 tile (= C.s1boxP on this path)
 constexpr int kK1TSlots = 8;   // K1T: S~1 tiles in flight (TMA loads issued ahead)
 
-template <int n>
+template <int n, bool VAR>
 __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPlan P, const __grid_constant__ CUtensorMap tm,
                                                   const float* __restrict__ f) {
   using G = ColGeo<n>;
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPl
 #pragma unroll
     for (int r = 0; r < G::R; ++r)
       x[r] = make_float2(rows[(2 * pr) * n + j + G::J * r], rows[(2 * pr + 1) * n + j + G::J * r]);
-    if (P.deapod) {   // reading G26: f / K on the nodes, K separable
+    if (VAR && P.deapod) {   // reading G26: f / K on the nodes, K separable
       const float w0 = P.deapod[y0 + 2 * pr], w1 = P.deapod[y0 + 2 * pr + 1];
 #pragma unroll
       for (int r = 0; r < G::R; ++r) {
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPl
 // Z[p] = C_y[p] + i C_{y+1}[p] and Z[-p] = conj C_y[p] + i conj C_{y+1}[p] (Hermitian
 // completion; C[0], C[N/2] -> 2 Re), conjugate transform, f~_y = Re z~, f~_{y+1} = Im z~.
 // Two row pairs per CTA; the [p][4 y] tiles of S~1 arrive by TMA tensor loads.
-template <int n>
+template <int n, bool VAR>
 __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPlan P, const __grid_constant__ CUtensorMap tm,
                                                   float* __restrict__ fout) {
   using G = ColGeo<n>;
@@ -488,8 +488,8 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
     const int oxy = (y0 + 2 * pr) * n;
     for (int xx = t; xx < n; xx += G::T) {
       const float2 z = residue_sum<G>(W, xx);
-      epi_adj_store(P, fout, o + xx, oxy + xx, z.x);
-      epi_adj_store(P, fout, o + n + xx, oxy + n + xx, z.y);
+      epi_adj_store<VAR>(P, fout, o + xx, oxy + xx, z.x);
+      epi_adj_store<VAR>(P, fout, o + n + xx, oxy + n + xx, z.y);
     }
   }
 }
@@ -688,8 +688,10 @@ static cudaError_t cfg_col() {
 #define SETC(k) if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   SETC((k2c_fwd<n>));
   SETC((k2c_adj<n>));
-  SETC((k1c_fwd<n>));
-  SETC((k1c_adj<n>));
+  SETC((k1c_fwd<n, false>));
+  SETC((k1c_adj<n, false>));
+  SETC((k1c_fwd<n, true>));
+  SETC((k1c_adj<n, true>));
   SETC((k4c_dct<n, false>));
   SETC((k4c_dct<n, true>));
 #undef SETC
@@ -723,25 +725,32 @@ cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s) {
+template <int n>
+static cudaError_t launch_k1c_n(const DevPlan& P, const CUtensorMap& tm, const float* f, float* fo, cudaStream_t s) {
   const Consts& C = P.C;
-  cudaError_t e = cudaSuccess;
   const dim3 grid(C.n / 4, C.batch);
   const dim3 blk(col_T(C.n, 8));
-  if (C.n == 1024) e = launch_pdl(C.pdl, k1c_fwd<1024>, grid, blk, smem_k1c(C), s, P, tm, f);
-  else if (C.n == 512) e = launch_pdl(C.pdl, k1c_fwd<512>, grid, blk, smem_k1c(C), s, P, tm, f);
-  else e = launch_pdl(C.pdl, k1c_fwd<256>, grid, blk, smem_k1c(C), s, P, tm, f);
+  if (f) {   // forward: only the G26 input scaling is a K1 variant
+    if (P.deapod) return launch_pdl(C.pdl, k1c_fwd<n, true>, grid, blk, smem_k1c(C), s, P, tm, f);
+    return launch_pdl(C.pdl, k1c_fwd<n, false>, grid, blk, smem_k1c(C), s, P, tm, f);
+  }
+  if (P.deapod || P.lowk_add) return launch_pdl(C.pdl, k1c_adj<n, true>, grid, blk, smem_k1c_adj(C), s, P, tm, fo);
+  return launch_pdl(C.pdl, k1c_adj<n, false>, grid, blk, smem_k1c_adj(C), s, P, tm, fo);
+}
+
+cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s) {
+  const int n = P.C.n;
+  const cudaError_t e = n == 1024 ? launch_k1c_n<1024>(P, tm, f, nullptr, s)
+                        : n == 512 ? launch_k1c_n<512>(P, tm, f, nullptr, s)
+                                   : launch_k1c_n<256>(P, tm, f, nullptr, s);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_k1c_adj(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s) {
-  const Consts& C = P.C;
-  cudaError_t e = cudaSuccess;
-  const dim3 grid(C.n / 4, C.batch);
-  const dim3 blk(col_T(C.n, 8));
-  if (C.n == 1024) e = launch_pdl(C.pdl, k1c_adj<1024>, grid, blk, smem_k1c_adj(C), s, P, tm, f);
-  else if (C.n == 512) e = launch_pdl(C.pdl, k1c_adj<512>, grid, blk, smem_k1c_adj(C), s, P, tm, f);
-  else e = launch_pdl(C.pdl, k1c_adj<256>, grid, blk, smem_k1c_adj(C), s, P, tm, f);
+  const int n = P.C.n;
+  const cudaError_t e = n == 1024 ? launch_k1c_n<1024>(P, tm, nullptr, f, s)
+                        : n == 512 ? launch_k1c_n<512>(P, tm, nullptr, f, s)
+                                   : launch_k1c_n<256>(P, tm, nullptr, f, s);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
 
 // ------------------------------------------------------------------ K5
 // transform g carries time samples t0 + 2g (real part) and t0 + 2g + 1 (imaginary part)
-template <int nf>
+template <int nf, bool VAR>
 __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ gout) {
   extern __shared__ float2 sm[];
   constexpr int G = ring_G<nf>();
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
       if (tt < tt_n) {
         const float2 z = X[(tt >> 1) * rs + pos];
         const size_t i = i0 + (size_t)tt * n_det;
-        gout[i] = epi_fwd(P, i, (tt & 1) ? z.y : z.x);
+        gout[i] = epi_fwd<VAR>(P, i, (tt & 1) ? z.y : z.x);
       }
     }
   }
@@ -299,7 +299,8 @@ cudaError_t configure_ring_kernels(const Consts& C) {
   TAT_RING_SWITCH({
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k3_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k3t_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k5t_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   });
   return e;
@@ -331,7 +332,10 @@ cudaError_t launch_k5(const DevPlan& P, float* g, cudaStream_t s) {
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
-    e = launch_pdl(C.pdl, k5_ring<NF>, dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), dim3(G * NF / 8), sm, s, P, g);
+    if (P.lowk_add)
+      e = launch_pdl(C.pdl, k5_ring<NF, true>, dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), dim3(G * NF / 8), sm, s, P, g);
+    else
+      e = launch_pdl(C.pdl, k5_ring<NF, false>, dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), dim3(G * NF / 8), sm, s, P, g);
   });
   return e != cudaSuccess ? e : cudaGetLastError();
 }

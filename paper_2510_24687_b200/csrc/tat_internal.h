@@ -160,15 +160,18 @@ cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, 
 }
 
 // forward epilogue: value at flat output index i of g
+// VAR = false: the kernel was instantiated for plans without the G25 / G26 variants
+template <bool VAR = true>
 __device__ __forceinline__ float epi_fwd(const DevPlan& P, size_t i, float v) {
-  if (P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n_t * P.C.n_det)];
+  if (VAR && P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n_t * P.C.n_det)];
   v *= P.epi_scale;
   return P.epi_sub ? v - __ldg(&P.epi_sub[i]) : v;
 }
 // adjoint epilogue: store value v of A* g at flat index i of f (pixel ixy = i mod n^2)
+template <bool VAR = true>
 __device__ __forceinline__ void epi_adj_store(const DevPlan& P, float* f, size_t i, int ixy, float v) {
-  if (P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n * P.C.n)];
-  if (P.deapod) v *= P.deapod[ixy % P.C.n] * P.deapod[ixy / P.C.n];
+  if (VAR && P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n * P.C.n)];
+  if (VAR && P.deapod) v *= P.deapod[ixy % P.C.n] * P.deapod[ixy / P.C.n];
   if (P.epi_update) {
     float o = f[i] - P.epi_tau * v;
     if (P.epi_update == 2) o = fmaxf(o, 0.f);
