@@ -54,3 +54,21 @@ def test_dense_parity_and_adjoint(torch_cuda, monkeypatch, n, n_det, n_t, batch,
     lhs = wY * np.sum(Af * gd)
     rhs = wX * np.sum(f.astype(np.float64) * uh)
     assert abs(lhs - rhs) <= 1e-5 * np.sqrt(wY * np.sum(Af * Af)) * np.sqrt(wY * np.sum(gd.astype(np.float64) ** 2))
+
+
+def test_dense_full_size_c3(torch_cuda):
+    """C3 sizes (n = 512, 512 detectors at irregular angles, n_t = 1024, batch 16, the launch
+    configuration the dense timing uses): images 0 and 15 against the oracle in full."""
+    torch = torch_cuda
+    from paper_2510_24687_b200 import Plan
+    n, n_det, n_t, batch = 512, 512, 1024, 16
+    ang = np.sort(np.random.default_rng(1).uniform(0.0, 2 * np.pi, n_det))
+    C = O.derive(n, n_det, n_t, 1.0, 1.0, 2.0, ang)
+    plan = Plan(n, n_det, n_t, batch=batch, angles=ang)
+    f = synth.phantom_batch("C3")
+    gd = np.stack([synth.random_data(n_t, n_det, 500 + b) for b in range(batch)])
+    g = plan.forward(torch.from_numpy(f).cuda()).cpu().numpy()
+    u = plan.adjoint(torch.from_numpy(gd).cuda()).cpu().numpy()
+    for b in (0, batch - 1):
+        _check(g[b], O.forward(f[b].astype(np.float64), C), f"dense C3 A {b}")
+        _check(u[b], O.adjoint(gd[b].astype(np.float64), C), f"dense C3 A* {b}")
