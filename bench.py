@@ -422,6 +422,16 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / pk["hbm_gbs"], "traffic": measured_traffic(name, dom), "kernel": dom,
                 "algorithmic_bytes": mdl["bytes"][dom], "peak_source": pk_kind}
+    # attained fraction of each stage's max(HBM, FP32) floor from the model
+    # bytes / flops at the measured HBM peak and the derived ALU peak
+    floors = {}
+    for st, us in per_stage_us.items():
+        f_us = max(mdl["bytes"][st] / (pk["hbm_gbs"] * 1e9), mdl["flops"][st] / (alu_peak * 1e12)) * 1e6
+        floors[st] = {"floor_us": round(f_us, 2), "frac": round(f_us / us, 3) if us > 0 else None}
+    floor_tot = sum(v["floor_us"] for v in floors.values())
+    stage_floor = {"per_stage": floors, "sum_floor_us": round(floor_tot, 1),
+                   "frac": round(floor_tot / sum(per_stage_us.values()), 3),
+                   "model": "max(model bytes / measured HBM peak, model flops / derived FP32 peak)"}
     eff_hbm = mdl["pair_bytes"] / (ms_per_step * 1e-3) / 1e9     # GB/s, whole batch
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -442,6 +452,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                                    "frac": eff_hbm / pk["hbm_gbs"]},
         "roofline": roof,
         "stage_us": {k: round(v, 2) for k, v in per_stage_us.items()},
+        "stage_floor": stage_floor,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(f_host.nbytes),
                 "d2h_bytes_per_step": int(u_pin[0].numel() * 4),
