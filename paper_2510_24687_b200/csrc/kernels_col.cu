@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_fwd(DevPl
 // Column p: the target values of column p (Rc, ordered by (q0, q1), moved by one bulk copy per
 // column into a double buffer) -> stage B^H (thread q0, only the present q1 are read) ->
 // stage A^H (thread (j, s)) -> residue-group partial sums -> S~1[b][p][y].
-template <int n>
+template <int n, bool CHORD>
 __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPlan P) {
   using G = ColGeo<n>;
   constexpr int R = G::R, J = G::J, NRES = G::NRES, Q0 = G::Q0;
@@ -297,8 +297,12 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPl
     issue(P0, 0);
   }
   __syncthreads();
-  uint32_t m = __ldg(&P.k2c_mask[(size_t)P0 * Q0 + t]);
-  int base = __ldg(&P.k2c_base[(size_t)P0 * Q0 + t]) - (__ldg(&P.k2t_colptr[P0]) & ~1);
+  uint32_t m = 0;
+  int base = 0;
+  if (!CHORD) {
+    m = __ldg(&P.k2c_mask[(size_t)P0 * Q0 + t]);
+    base = __ldg(&P.k2c_base[(size_t)P0 * Q0 + t]) - (__ldg(&P.k2t_colptr[P0]) & ~1);
+  }
   for (int p = P0; p < Pend; ++p) {
     const int it = p - P0, slot = it & 1;
     if (t == 0 && p + 1 < Pend) {
@@ -307,18 +311,28 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPl
     }
     uint32_t m_next = 0;
     int base_next = 0;
-    if (p + 1 < Pend) {
+    if (!CHORD && p + 1 < Pend) {
       m_next = __ldg(&P.k2c_mask[(size_t)(p + 1) * Q0 + t]);
       base_next = __ldg(&P.k2c_base[(size_t)(p + 1) * Q0 + t]) - (__ldg(&P.k2t_colptr[p + 1]) & ~1);
     }
     ac::mbar_wait(&bar[slot], (it >> 1) & 1);
     {   // stage B^H: A~[q0][j] = sum_q1 W_J^{-q1 j} F~[q0 + Q0 q1]
-      const float2* rb = rbuf + slot * RB + base;
       float2 u[J];
+      if (CHORD) {   // targets q = -Qp .. Qp at offset q + Qp of the column
+        const int Qp = __ldg(&P.k2c_chord[p]);
+        const float2* rb = rbuf + slot * RB + (__ldg(&P.k2t_colptr[p]) & 1) + Qp;
 #pragma unroll
-      for (int c = 0; c < J; ++c) {
-        const uint32_t below = m & ((1u << c) - 1u);
-        u[c] = ((m >> c) & 1u) ? rb[__popc(below)] : make_float2(0.f, 0.f);
+        for (int c = 0; c < J; ++c) {
+          const int qm = t + Q0 * c, q = qm < C.N / 2 ? qm : qm - C.N;
+          u[c] = (q >= -Qp && q <= Qp) ? rb[q] : make_float2(0.f, 0.f);
+        }
+      } else {
+        const float2* rb = rbuf + slot * RB + base;
+#pragma unroll
+        for (int c = 0; c < J; ++c) {
+          const uint32_t below = m & ((1u << c) - 1u);
+          u[c] = ((m >> c) & 1u) ? rb[__popc(below)] : make_float2(0.f, 0.f);
+        }
       }
       ce::dftr<J, 1>(u);
 #pragma unroll
@@ -687,7 +701,8 @@ static cudaError_t cfg_col() {
   const int lim = 227 * 1024;
 #define SETC(k) if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   SETC((k2c_fwd<n>));
-  SETC((k2c_adj<n>));
+  SETC((k2c_adj<n, false>));
+  SETC((k2c_adj<n, true>));
   SETC((k1c_fwd<n, false>));
   SETC((k1c_adj<n, false>));
   SETC((k1c_fwd<n, true>));
@@ -719,9 +734,13 @@ cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
   const dim3 grid((C.ncols + C.col_strip - 1) / C.col_strip, C.batch);
   const dim3 blk(col_T(C.n, 8));
-  if (C.n == 1024) e = launch_pdl(C.pdl, k2c_adj<1024>, grid, blk, smem_k2c_adj(C), s, P);
-  else if (C.n == 512) e = launch_pdl(C.pdl, k2c_adj<512>, grid, blk, smem_k2c_adj(C), s, P);
-  else e = launch_pdl(C.pdl, k2c_adj<256>, grid, blk, smem_k2c_adj(C), s, P);
+  const bool ch = P.k2c_chord != nullptr;
+  if (C.n == 1024) e = ch ? launch_pdl(C.pdl, k2c_adj<1024, true>, grid, blk, smem_k2c_adj(C), s, P)
+                          : launch_pdl(C.pdl, k2c_adj<1024, false>, grid, blk, smem_k2c_adj(C), s, P);
+  else if (C.n == 512) e = ch ? launch_pdl(C.pdl, k2c_adj<512, true>, grid, blk, smem_k2c_adj(C), s, P)
+                              : launch_pdl(C.pdl, k2c_adj<512, false>, grid, blk, smem_k2c_adj(C), s, P);
+  else e = ch ? launch_pdl(C.pdl, k2c_adj<256, true>, grid, blk, smem_k2c_adj(C), s, P)
+              : launch_pdl(C.pdl, k2c_adj<256, false>, grid, blk, smem_k2c_adj(C), s, P);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

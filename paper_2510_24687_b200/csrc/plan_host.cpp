@@ -455,12 +455,18 @@ void build_inverse_tables(const Consts& C, const std::vector<int>& node_perm, In
   };
   struct Tg { int key, q; int4 nd; float4 w; };
   std::vector<Tg> col;
+  const double rscale = C.dxi / C.dlam, tscale = nphi / (2.0 * kPi);
+  // pass 0: natural q order (every column is a chord of the disk, |q| <= Q_p: the condition is
+  // symmetric and monotone in |q|); pass 1 (only if some column were not): the (q0, q1) order
+  // of the mask / base path
+  for (int pass = 0; pass < 2; ++pass) {
   I.colptr.assign(C.ncols + 1, 0);
   I.nodes.clear();
   I.w.clear();
   I.tq.clear();
+  I.chord.clear();
   I.max_per_col = 0;
-  const double rscale = C.dxi / C.dlam, tscale = nphi / (2.0 * kPi);
+  bool chords = true;
   for (int p = 0; p < C.ncols; ++p) {
     col.clear();
     for (int q = -N / 2; q < N / 2; ++q) {
@@ -476,7 +482,7 @@ void build_inverse_tables(const Consts& C, const std::vector<int>& node_perm, In
       const double hw = (p == 0) ? 0.5 : 1.0;   // Hermitian half spectrum (K1T doubles p = 0)
       Tg t;
       t.q = ((q % N) + N) % N;
-      t.key = (t.q % Q0) * (N / Q0) + t.q / Q0;
+      t.key = pass == 0 ? q : (t.q % Q0) * (N / Q0) + t.q / Q0;   // pass 0: along the chord
       t.nd = make_int4(code(j0, l0), code(j0 + 1, l0), code(j0, l1), code(j0 + 1, l1));
       t.w = make_float4((float)(hw * (1 - a) * (1 - bb)), (float)(hw * a * (1 - bb)),
                         (float)(hw * (1 - a) * bb), (float)(hw * a * bb));
@@ -490,6 +496,12 @@ void build_inverse_tables(const Consts& C, const std::vector<int>& node_perm, In
     }
     I.colptr[p + 1] = I.colptr[p] + (int)col.size();
     I.max_per_col = std::max(I.max_per_col, (int)col.size());
+    I.chord.push_back(col.empty() ? -1 : -col.front().key);
+    if (!col.empty() && (col.back().key != -col.front().key || (int)col.size() != 2 * col.back().key + 1))
+      chords = false;
+  }
+  if (pass == 0 && chords) break;
+  I.chord.clear();   // pass 1: no chord table (k2c_adj uses mask / base)
   }
   I.mask.clear();
   I.base.clear();

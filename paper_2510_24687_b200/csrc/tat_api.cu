@@ -407,6 +407,11 @@ static tat_status inverse_setup(tat_plan* p) {
     if ((e = upload(p, I.tq, &Q.k2t_tq, tb)) != cudaSuccess) break;
     if ((e = upload(p, I.mask, &Q.k2c_mask, tb)) != cudaSuccess) break;
     if ((e = upload(p, I.base, &Q.k2c_base, tb)) != cudaSuccess) break;
+    if (col_ok(C) && !I.chord.empty()) {
+      if ((e = upload(p, I.chord, &Q.k2c_chord, tb)) != cudaSuccess) break;
+    } else {
+      Q.k2c_chord = nullptr;
+    }
     Q.C.ntargets = (int)I.tq.size();
     Q.C.ntpad = (Q.C.ntargets + 1) & ~1;
     Q.C.k2c_rbuf = (I.max_per_col + 3) & ~1;
@@ -417,7 +422,7 @@ static tat_status inverse_setup(tat_plan* p) {
     Q.Rc = (float2*)d;
     if ((e = alloc_ws(p, (size_t)C.n * C.n, &d)) != cudaSuccess) break;
     p->inv_region = (unsigned char*)d;
-    if ((e = alloc_ws(p, (size_t)C.batch * sizeof(float), &d)) != cudaSuccess) break;
+    if ((e = alloc_ws(p, (size_t)C.batch * kInvParts * sizeof(float), &d)) != cudaSuccess) break;
     p->inv_csum = (float*)d;
   } while (false);
   p->table_bytes += tb;

@@ -130,6 +130,9 @@ struct DevPlan {
   // per-image constants (coef * sum of the call's input image / data), written by k_lowk_sum
   // at the start of each forward / adjoint call and added to every output in the epilogues
   float* lowk_add = nullptr;
+  // inverse (tat_inverse): the Cartesian targets of column p are the whole chord |q| <= Q_p of
+  // the disk, stored in natural q order; k2c_adj then reads them by index (no mask / base)
+  const int* k2c_chord = nullptr;
   // de-apodised bilinear variant (reading G26; tat_plan_set_interpolation): [n] factors
   // 1 / sinc^2(x_i / 2L); K1 scales f[iy][ix] by d[ix] d[iy], K1T's epilogue its output likewise
   const float* deapod = nullptr;
@@ -236,6 +239,7 @@ cudaError_t launch_k5d_tc(const DevPlan& P, float* g, cudaStream_t s);
 cudaError_t launch_k5dt_tc(const DevPlan& P, const float* g, cudaStream_t s);
 cudaError_t configure_dense_kernels(const Consts& C);
 // kernels_inv.cu: inverse-specific stages (Alg. 3 steps 5, 7, 8)
+constexpr int kInvParts = 64;   // k2i_const partial sums per image (fixed order)
 cudaError_t launch_k2i_interp(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k2i_finish(const DevPlan& P, float* f, const unsigned char* region, float* csum,
                               int annulus_count, cudaStream_t s);
@@ -248,6 +252,7 @@ struct InvTables {
   std::vector<int> tq;              // [T] q mod N
   std::vector<uint32_t> mask;       // [ncols][16L] (col_ok only)
   std::vector<int> base;            // [ncols][16L]
+  std::vector<int> chord;           // [ncols] Q_p: column p's targets are q = -Q_p .. Q_p, in order
   int max_per_col = 0;
 };
 void build_inverse_tables(const Consts& C, const std::vector<int>& node_perm, InvTables& I);
