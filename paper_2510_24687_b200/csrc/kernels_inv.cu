@@ -9,10 +9,11 @@
 //   k2i_const  : step 7 -- per image, the sum of v over the annulus r0 < |x| < R as kInvParts
 //                fixed-order partial sums (one CTA each; deterministic).
 //   k2i_project: step 8 -- f = (v + C) on |x| <= r0, 0 elsewhere, C = -sum / count (the
-//                partials summed in a fixed order by every thread).
+//                partials summed in a fixed order once per CTA).
 #include "tat_internal.h"
 
 namespace tat {
+
 
 __device__ __forceinline__ float2 inv_node(const float2* __restrict__ S2, int code) {
   // code >= 0: node value; code < 0: conj of node (-code - 1) (the mirror angle phi + pi)
@@ -30,7 +31,7 @@ __global__ void __launch_bounds__(256) k2i_interp(DevPlan P) {
   const size_t img = (size_t)C.half * C.NL;
   const float2* S2 = P.S2 + C.b0 * img;
   float2* Rc = P.Rc + (size_t)C.b0 * C.ntpad + t;
-#pragma unroll 2
+#pragma unroll 1   // one image at a time: deeper unrolling measured slower (L2 working set)
   for (int b = 0; b < C.batch; ++b, S2 += img, Rc += C.ntpad) {
     float2 acc = __fmul2_rn(make_float2(w.x, w.x), inv_node(S2, nd.x));
     acc = __ffma2_rn(make_float2(w.y, w.y), inv_node(S2, nd.y), acc);
@@ -67,9 +68,14 @@ __global__ void __launch_bounds__(256) k2i_project(DevPlan P, float* __restrict_
   const Consts& C = P.C;
   const int nn = C.n * C.n;
   const int b = C.b0 + blockIdx.y;
-  float sum = 0.f;
-  for (int q = 0; q < kInvParts; ++q) sum += __ldg(&csum[(size_t)b * kInvParts + q]);
-  const float cst = -sum * inv_count;
+  __shared__ float cst_s;
+  if (threadIdx.x == 0) {   // the partials in a fixed order, once per CTA
+    float sum = 0.f;
+    for (int q = 0; q < kInvParts; ++q) sum += __ldg(&csum[(size_t)b * kInvParts + q]);
+    cst_s = -sum * inv_count;
+  }
+  __syncthreads();
+  const float cst = cst_s;
   float* fb = f + (size_t)b * nn;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x)
     fb[i] = (__ldg(&region[i]) == 1) ? fb[i] + cst : 0.f;
