@@ -304,6 +304,15 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # the timed steps replay one CUDA graph of the step's launches (enqueue-only API, PDL edges
+    # kept), so small configurations are not bound by host launch overhead
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
@@ -318,7 +327,10 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     for i in range(args.steps):
         flush.zero_()
         starts[i].record(stream)
-        step()
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
         ends[i].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -446,7 +458,8 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_desc(name), "batch_per_gpu": B,
                    "parallelism": f"replicas x{world} (batch-sharded, no collective)",
-                   "l2": "flushed (256 MB write) between timed steps, outside the step events"},
+                   "l2": "flushed (256 MB write) between timed steps, outside the step events",
+                   "launch": "CUDA graph replay per step" if graph is not None else "eager"},
         "hbm_roofline_effective": {"model_bytes_per_step": mdl["pair_bytes"],
                                    "achieved_gbs": eff_hbm, "peak_gbs": pk["hbm_gbs"],
                                    "frac": eff_hbm / pk["hbm_gbs"]},
@@ -477,6 +490,7 @@ def main():
     ap.add_argument("--impl", default="tat", choices=["tat", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-loop", action="store_true", help="skip the NNLS loop measurement")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a graph")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
