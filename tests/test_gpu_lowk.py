@@ -115,3 +115,19 @@ def test_deapod_parity_and_adjoint(torch_cuda, name, lowk, n_override):
     lhs = wY * np.sum(Af * gd)
     rhs = wX * np.sum(f.astype(np.float64) * uh)
     assert abs(lhs - rhs) <= 1e-5 * np.sqrt(wY * np.sum(Af * Af)) * np.sqrt(wY * np.sum(gd.astype(np.float64) ** 2))
+
+
+def test_variant_rules_validated(torch_cuda):
+    """Unknown rules are rejected with TAT_ERR_INVALID_ARGUMENT and leave the plan unchanged."""
+    from paper_2510_24687_b200 import Plan
+    from paper_2510_24687_b200.tat import TatError
+    geo = _geo("T32", 1)
+    plan = Plan(geo.n, geo.n_det, geo.n_t, geo.R, geo.c, geo.T, 1, geo.angles_array())
+    for bad in (2, -1):
+        with pytest.raises(TatError) as e:
+            plan.set_quadrature(bad)
+        assert e.value.status == 1
+        with pytest.raises(TatError) as e:
+            plan.set_interpolation(bad)
+        assert e.value.status == 1
+    assert plan.quadrature == "trapezoid" and plan.interpolation == "bilinear"
