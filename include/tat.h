@@ -186,6 +186,7 @@ typedef struct {
   double L, T_new, dxi, dlam, omega, dt, h, wJ;
   size_t workspace_bytes, table_bytes;
   int launches_forward, launches_adjoint;
+  int n_targets;    /* Cartesian targets of the transposed bilinear (half spectrum, per image) */
 } tat_plan_info_t;
 
 /* ring_index: optional host int array of n_det receiving the ring position r_d of each
@@ -208,8 +209,9 @@ tat_status tat_plan_host_multiplier(int n, int n_det, int n_t, double R, double 
 /* Optional per-stage device timing (CUDA events recorded between the kernels of each call on
  * the call's stream).  tat_profile_begin arms recording for up to max_calls calls;
  * tat_profile_end synchronises the events and writes the summed milliseconds per stage:
- * stage_ms[0..4] = forward K1..K5, stage_ms[5..9] = adjoint K5T..K1T (10 floats), and the
- * number of forward / adjoint calls recorded.  Not thread-safe with concurrent calls. */
+ * stage_ms[0..4] = forward K1..K5, stage_ms[5..10] = adjoint K5T, K4T, K3T, K2Ta (target
+ * sums), K2Tb (inverse column transforms), K1T (11 floats), and the number of forward /
+ * adjoint calls recorded.  Not thread-safe with concurrent calls. */
 tat_status tat_profile_begin(tat_plan* plan, int max_calls);
 tat_status tat_profile_end(tat_plan* plan, float* stage_ms, int* n_forward, int* n_adjoint);
 

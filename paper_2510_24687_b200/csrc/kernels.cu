@@ -344,7 +344,7 @@ cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float*
   else k3t_angular<<<dim3((C.NL + JT - 1) / JT, B), kThreads, smem_ring(C), s>>>(P);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[3], s);
-  e = launch_k2t(P, s);
+  e = launch_k2t(P, s, ev ? ev[6] : nullptr);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[4], s);
   e = launch_k1t(P, tm, f, s);

@@ -541,10 +541,11 @@ cudaError_t launch_k2tb(const DevPlan& P, cudaStream_t s) {   // K2Tb only (targ
   return cudaGetLastError();
 }
 
-cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s) {
+cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s, cudaEvent_t mid) {
   const Consts& C = P.C;
   cudaError_t e = launch_k2t_sum(P, s);
   if (e != cudaSuccess) return e;
+  if (mid) cudaEventRecord(mid, s);
   if (col_ok(C)) return launch_k2c_adj(P, s);
   const dim3 grid((C.ncols + kStrip - 1) / kStrip, C.batch);
   TAT_DISPATCH_N(k2t_adj<NN><<<grid, fft_threads(C), smem_k2t(C), s>>>(P));

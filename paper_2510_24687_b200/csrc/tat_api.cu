@@ -36,7 +36,7 @@ struct tat_plan {
   int inv_annulus = 0;
   // profiling
   int prof_max = 0, prof_fwd = 0, prof_adj = 0;
-  std::vector<cudaEvent_t> prof_ev;   // (prof_max) sets of 6 events
+  std::vector<cudaEvent_t> prof_ev;   // (prof_max) sets of kProfEv events
   std::vector<char> prof_kind;        // 1 = forward, 0 = adjoint, per used slot
 };
 
@@ -102,6 +102,7 @@ static void fill_info(const Consts& C, tat_plan_info_t* o) {
   o->dt = C.dt; o->h = C.h; o->wJ = C.wJ;
   o->launches_forward = kLaunchesForward;
   o->launches_adjoint = kLaunchesAdjoint;
+  o->n_targets = C.ntargets;
 }
 
 // Host-only: derive the plan constants without touching the device (used by CPU tests).
@@ -251,7 +252,7 @@ static cudaEvent_t* prof_slot(tat_plan* p, bool fwd) {
   if (used >= p->prof_max) return nullptr;
   (fwd ? p->prof_fwd : p->prof_adj)++;
   p->prof_kind.push_back(fwd ? 1 : 0);
-  return &p->prof_ev[(size_t)used * 6];
+  return &p->prof_ev[(size_t)used * kProfEv];
 }
 
 tat_status tat_forward(const tat_plan* plan, const float* f, float* g, cudaStream_t stream) {
@@ -572,7 +573,7 @@ tat_status tat_power_norm(const tat_plan* plan, int iters, unsigned long long se
 tat_status tat_profile_begin(tat_plan* plan, int max_calls) {
   if (!plan || max_calls < 0) return fail(TAT_ERR_INVALID_ARGUMENT, "bad arguments");
   for (cudaEvent_t e : plan->prof_ev) cudaEventDestroy(e);
-  plan->prof_ev.assign((size_t)max_calls * 6, nullptr);
+  plan->prof_ev.assign((size_t)max_calls * kProfEv, nullptr);
   plan->prof_kind.clear();
   for (auto& e : plan->prof_ev) {
     cudaError_t r = cudaEventCreate(&e);
@@ -585,16 +586,20 @@ tat_status tat_profile_begin(tat_plan* plan, int max_calls) {
 
 tat_status tat_profile_end(tat_plan* plan, float* stage_ms, int* n_forward, int* n_adjoint) {
   if (!plan || !stage_ms) return fail(TAT_ERR_INVALID_ARGUMENT, "bad arguments");
-  for (int i = 0; i < 10; ++i) stage_ms[i] = 0.f;
+  for (int i = 0; i < 11; ++i) stage_ms[i] = 0.f;
   int used = plan->prof_fwd + plan->prof_adj;
   for (int u = 0; u < used; ++u) {
-    cudaEvent_t* ev = &plan->prof_ev[(size_t)u * 6];
+    cudaEvent_t* ev = &plan->prof_ev[(size_t)u * kProfEv];
     cudaError_t r = cudaEventSynchronize(ev[5]);
     if (r != cudaSuccess) return cuda_fail(r, "cudaEventSynchronize");
-    bool fwd = plan->prof_kind[u] != 0;
-    for (int s = 0; s < 5; ++s) {
+    const bool fwd = plan->prof_kind[u] != 0;
+    // forward: ev[0..5] bound K1..K5; adjoint: ev[0..3] K5T..K3T, ev[3] -> ev[6] K2Ta,
+    // ev[6] -> ev[4] K2Tb, ev[4] -> ev[5] K1T
+    static const int fa[5] = {0, 1, 2, 3, 4}, fb[5] = {1, 2, 3, 4, 5};
+    static const int aa[6] = {0, 1, 2, 3, 6, 4}, ab[6] = {1, 2, 3, 6, 4, 5};
+    for (int s = 0; s < (fwd ? 5 : 6); ++s) {
       float ms = 0.f;
-      r = cudaEventElapsedTime(&ms, ev[s], ev[s + 1]);
+      r = cudaEventElapsedTime(&ms, ev[fwd ? fa[s] : aa[s]], ev[fwd ? fb[s] : ab[s]]);
       if (r != cudaSuccess) return cuda_fail(r, "cudaEventElapsedTime");
       stage_ms[(fwd ? 0 : 5) + s] += ms;
     }

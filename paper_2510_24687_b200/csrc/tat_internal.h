@@ -186,7 +186,9 @@ __device__ __forceinline__ void epi_adj_store(const DevPlan& P, float* f, size_t
 }
 #endif
 
-// Launchers (kernels.cu).  ev != nullptr: record ev[i] before stage i and ev[5] at the end.
+// Launchers (kernels.cu).  ev != nullptr: record ev[i] before stage i and ev[5] at the end
+// (adjoint: ev[6] between the two K2T kernels).
+constexpr int kProfEv = 7;
 cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float* f, float* g,
                            cudaStream_t s, cudaEvent_t* ev);
 cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float* g, float* f,
@@ -200,7 +202,7 @@ constexpr int kS1BoxY = 4;
 cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out);
 cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
 cudaError_t launch_k2(const DevPlan& P, cudaStream_t s);
-cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s);   // target sums + column IDFT
+cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s, cudaEvent_t mid = nullptr);   // target sums + column IDFT
 cudaError_t launch_k2tb(const DevPlan& P, cudaStream_t s);  // column IDFT of the targets in Rc
 cudaError_t launch_k1t(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s);
 // kernels_ring.cu: K3, K3T, K5, K5T on n_phi-point register FFTs

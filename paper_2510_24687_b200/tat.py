@@ -48,7 +48,8 @@ class PlanInfo(ctypes.Structure):
                 ("dlam", ctypes.c_double), ("omega", ctypes.c_double), ("dt", ctypes.c_double),
                 ("h", ctypes.c_double), ("wJ", ctypes.c_double),
                 ("workspace_bytes", ctypes.c_size_t), ("table_bytes", ctypes.c_size_t),
-                ("launches_forward", ctypes.c_int), ("launches_adjoint", ctypes.c_int)]
+                ("launches_forward", ctypes.c_int), ("launches_adjoint", ctypes.c_int),
+                ("n_targets", ctypes.c_int)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -331,8 +332,9 @@ class Plan:
         _check(self._lib.tat_profile_begin(self._h, max_calls))
 
     def profile_end(self):
-        """(stage_ms[10] summed, n_forward, n_adjoint); stages K1..K5, K5T..K1T."""
-        ms = (ctypes.c_float * 10)()
+        """(stage_ms[11] summed, n_forward, n_adjoint); stages K1..K5, K5T, K4T, K3T, K2Ta,
+        K2Tb, K1T."""
+        ms = (ctypes.c_float * 11)()
         nf, na = ctypes.c_int(), ctypes.c_int()
         _check(self._lib.tat_profile_end(self._h, ms, ctypes.byref(nf), ctypes.byref(na)))
         return list(ms), nf.value, na.value
