@@ -17,6 +17,7 @@
 #include <cuda_fp16.h>
 
 constexpr int n = 512, N = 4096, J = 32, R = 16, Q0 = 128, NCOL = 4;   // 4 columns per group
+constexpr int WPQ = 4, NTHR = 128 * WPQ;   // warps per TMEM lane quarter
 // stage A operand tiles: A_A [128 rows][32 K] fp16, B_A [256 rows][32 K]; stage B: A_B per column
 // [128 rows][64 K], B_B [64 rows][64 K].  No-swizzle K-major cores (8 rows x 16 B); K-adjacent
 // cores LBO apart, row groups SBO apart.  LBO = 144 B (not a multiple of 128 B) so the transposed
@@ -65,8 +66,14 @@ __device__ __forceinline__ void split(float x, __half& hi, __half& lo) {
   hi = __float2half_rn(x);
   lo = __float2half_rn(x - __half2float(hi));
 }
+// the same for a complex value with packed conversions (cvt.rn.f16x2.f32)
+__device__ __forceinline__ void split2(float re, float im, __half2& hi, __half2& lo) {
+  hi = __floats2half2_rn(re, im);
+  const float2 b = __half22float2(hi);
+  lo = __floats2half2_rn(re - b.x, im - b.y);
+}
 
-__global__ void __launch_bounds__(256, 1) tcfft(const float2* __restrict__ x, float2* __restrict__ F, int ncols,
+__global__ void __launch_bounds__(NTHR, 1) tcfft(const float2* __restrict__ x, float2* __restrict__ F, int ncols,
                                                const unsigned char* __restrict__ gB, const float2* __restrict__ tw,
                                                int write_out, float* __restrict__ chk) {
   extern __shared__ __align__(1024) unsigned char sm[];
@@ -77,8 +84,8 @@ __global__ void __launch_bounds__(256, 1) tcfft(const float2* __restrict__ x, fl
   const float2* wtab = tw;   // W_N^m, m < N (32 KB, L1-resident)
   uint64_t* bar = reinterpret_cast<uint64_t*>(AB + NCOL * 2 * SZ_AB);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, quarter = warp & 3, half = warp >> 2;
-  for (uint32_t i = t * 16; i < 2 * SZ_BA + 2 * SZ_BB; i += 256 * 16)
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, quarter = warp & 3, sub = warp >> 2;
+  for (uint32_t i = t * 16; i < 2 * SZ_BA + 2 * SZ_BB; i += NTHR * 16)
     *reinterpret_cast<uint4*>(sm + i) = *reinterpret_cast<const uint4*>(gB + i);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(512));
@@ -95,93 +102,116 @@ __global__ void __launch_bounds__(256, 1) tcfft(const float2* __restrict__ x, fl
   const uint32_t tmem = *tslot, tq = tmem + ((uint32_t)(32 * quarter) << 16);
   uint32_t ph = 0;
   float csum = 0.f;
+  // per-thread twiddle factors (lane = j; this warp's q0 = 16 a + b with a in {2 sub, 2 sub + 1}):
+  // W_N^{q0 (j - n/2)} = P[b] Q[a - 2 sub], P[b] = W_N^{b (j - n/2)}, Q = W_N^{16 a (j - n/2)}
+  float2 Pw[16], Qw[2];
+  {
+    const int jm = lane - n / 2;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) Pw[b] = __ldg(&wtab[(b * jm + 64 * N) & (N - 1)]);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) Qw[c] = __ldg(&wtab[(16 * (2 * sub + c) * jm + 64 * N) & (N - 1)]);
+  }
   constexpr uint32_t IA = idesc_f16(128, 256), IB = idesc_f16(128, 64);
-  for (int g = blockIdx.x; g < ncols / NCOL; g += gridDim.x) {
-    // ---- stage A operand: row (col = quarter, j = lane): x[j + 32 r] (scaled, split); both
-    // warps of a quarter compute the column scale, the first writes the operand
-    const int col = g * NCOL + quarter;
-    const float2* xc = x + (size_t)col * n;
-    float2 v[R];
+  // software pipeline: MMA B(g) and MMA A(g+1) run back to back while the threads prefetch
+  // x(g+2) and then read out F(g); the twiddle phase of g+1 finds A(g+1) done
+  uint64_t* barA = bar;                                   // stage-A MMAs retired
+  uint64_t* barB = bar + 16;                              // stage-B MMAs retired (byte 128)
+  float* red = reinterpret_cast<float*>(bar + 2) + 8;     // [16] per-warp maxima
+  float* isBv = reinterpret_cast<float*>(bar + 2);        // [4] 1 / sB per column
+  uint32_t phA = 0, phB = 0;
+  const int G = ncols / NCOL;
+  auto load_x = [&](int gg, float2 (&v)[4]) {
+    if (gg < G) {
+      const float2* xc = x + (size_t)(gg * NCOL + quarter) * n;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) v[r] = __ldg(&xc[lane + J * (4 * sub + r)]);
+    }
+  };
+  // column scale (reduced over the 4 warps of the quarter) and the stage-A operand of group gg
+  auto put_a = [&](const float2 (&v)[4]) -> float {
     float mx = 0.f;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      v[r] = __ldg(&xc[lane + J * r]);
-      mx = fmaxf(mx, fmaxf(fabsf(v[r].x), fabsf(v[r].y)));
-    }
+    for (int r = 0; r < 4; ++r) mx = fmaxf(mx, fmaxf(fabsf(v[r].x), fabsf(v[r].y)));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(~0u, mx, o));
+    if (lane == 0) red[warp] = mx;
+    asm volatile("bar.sync 1, %0;" ::"n"(NTHR) : "memory");
+    mx = fmaxf(fmaxf(red[quarter], red[quarter + 4]), fmaxf(red[quarter + 8], red[quarter + 12]));
     int ea;
     frexpf(mx > 0.f ? mx : 1.f, &ea);
-    const float sA = ldexpf(1.f, 14 - ea), isA = ldexpf(1.f, ea - 14);   // max -> [2^13, 2^14)
-    if (half == 0) {
-      __half h[2 * R], l[2 * R];
+    const float sA = ldexpf(1.f, 14 - ea);
+    __half2 h[4], l[4];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        split(v[r].x * sA, h[2 * r], l[2 * r]);
-        split(v[r].y * sA, h[2 * r + 1], l[2 * r + 1]);
-      }
+    for (int r = 0; r < 4; ++r) split2(v[r].x * sA, v[r].y * sA, h[r], l[r]);
+    const int row = 32 * quarter + lane;
+    *reinterpret_cast<uint4*>(AA + off_k(row, 8 * sub, SBO_A)) = *reinterpret_cast<uint4*>(h);
+    *reinterpret_cast<uint4*>(AA + SZ_AA + off_k(row, 8 * sub, SBO_A)) = *reinterpret_cast<uint4*>(l);
+    return ldexpf(1.f, ea - 14);   // 1 / sA
+  };
+  auto mma_a = [&]() {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t ah = su32(AA), al = ah + SZ_AA, bh = su32(BA), bl = bh + SZ_BA;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        *reinterpret_cast<uint4*>(AA + off_k(t, 8 * c, SBO_A)) = *reinterpret_cast<uint4*>(&h[8 * c]);
-        *reinterpret_cast<uint4*>(AA + SZ_AA + off_k(t, 8 * c, SBO_A)) = *reinterpret_cast<uint4*>(&l[8 * c]);
-      }
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t o = k * 2 * LBO;
+      mma(tmem, desc(ah + o, SBO_A), desc(bh + o, SBO_A), IA, k > 0);
+      mma(tmem, desc(ah + o, SBO_A), desc(bl + o, SBO_A), IA, true);
+      mma(tmem, desc(al + o, SBO_A), desc(bh + o, SBO_A), IA, true);
     }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(barA)));
+  };
+  auto wait = [&](uint64_t* b, uint32_t& ph) {
+    asm volatile("{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W_%=;\n}\n"
+                 ::"r"(su32(b)), "r"(ph) : "memory");
+    ph ^= 1;
+  };
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(barB)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  int g = blockIdx.x;
+  float2 vn[4];
+  float isA = 1.f;
+  if (g < G) {
+    load_x(g, vn);
+    isA = put_a(vn);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (t == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t ah = su32(AA), al = ah + SZ_AA, bh = su32(BA), bl = bh + SZ_BA;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const uint32_t o = k * 2 * LBO;
-        mma(tmem, desc(ah + o, SBO_A), desc(bh + o, SBO_A), IA, k > 0);
-        mma(tmem, desc(ah + o, SBO_A), desc(bl + o, SBO_A), IA, true);
-        mma(tmem, desc(al + o, SBO_A), desc(bh + o, SBO_A), IA, true);
-      }
-    }
-    commit_wait(bar, ph);   // thread 0 commits, every thread waits
+    if (t == 0) mma_a();
+    load_x(g + gridDim.x, vn);
+  }
+  for (; g < G; g += gridDim.x) {
+    wait(barA, phA);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // ---- twiddle, rescale, transpose into the stage-B operand of column `quarter` (K = 2 j + c);
-    // warp half h handles q0 in [64 h, 64 h + 64); the column scale is reduced over both halves
+    // ---- twiddle, rescale, transpose into the stage-B operand of column `quarter`
     {
       const int j = lane;
-      float ymax = 0.f;
-      float2 y[Q0 / 2];
-#pragma unroll
-      for (int cb = 0; cb < 4; ++cb) {
-        float d[32];
-        ld32(tq + (4 * half + cb) * 32, d);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int q0 = (4 * half + cb) * 16 + e;
-          const float2 w = __ldg(&wtab[(q0 * (j - n / 2) + 64 * N) & (N - 1)]);   // W_N^{q0 (j - n/2)}
-          const float re = d[2 * e] * isA, im = d[2 * e + 1] * isA;
-          y[q0 - 64 * half] = make_float2(re * w.x - im * w.y, re * w.y + im * w.x);
-          ymax = fmaxf(ymax, fmaxf(fabsf(re), fabsf(im)));   // |y| = |d| (unit twiddle)
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ymax = fmaxf(ymax, __shfl_xor_sync(~0u, ymax, o));
-      float* ym = reinterpret_cast<float*>(bar + 2) + 8;
-      if (lane == 0) ym[warp] = ymax;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      ymax = fmaxf(ym[quarter], ym[quarter + 4]);
-      int eb;
-      frexpf(ymax > 0.f ? ymax : 1.f, &eb);
-      const float sB = ldexpf(1.f, 14 - eb);
+      const float sBr = 1.f / 16.f;   // D is in units of sA: x sA / 16 keeps |Y| in fp16's range
       unsigned char* ab = AB + quarter * 2 * SZ_AB;
 #pragma unroll
-      for (int i = 0; i < Q0 / 2; ++i) {
-        const int q0 = 64 * half + i;
-        __half h0, l0, h1, l1;
-        split(y[i].x * sB, h0, l0);
-        split(y[i].y * sB, h1, l1);
-        const uint32_t o = off_k(q0, 2 * j, SBO_B);
-        *reinterpret_cast<__half2*>(ab + o) = __halves2half2(h0, h1);
-        *reinterpret_cast<__half2*>(ab + SZ_AB + o) = __halves2half2(l0, l1);
+      for (int cb = 0; cb < 2; ++cb) {
+        float d[32];
+        ld32(tq + (2 * sub + cb) * 32, d);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int q0 = (2 * sub + cb) * 16 + e;
+          const float2 w = make_float2(Pw[e].x * Qw[cb].x - Pw[e].y * Qw[cb].y, Pw[e].x * Qw[cb].y + Pw[e].y * Qw[cb].x);
+          const float re = d[2 * e] * sBr, im = d[2 * e + 1] * sBr;
+          __half2 hi, lo;
+          split2(re * w.x - im * w.y, re * w.y + im * w.x, hi, lo);
+          const uint32_t o = off_k(q0, 2 * j, SBO_B);
+          *reinterpret_cast<__half2*>(ab + o) = hi;
+          *reinterpret_cast<__half2*>(ab + SZ_AB + o) = lo;
+        }
       }
-      if (lane == 0 && half == 0) reinterpret_cast<float*>(bar + 2)[quarter] = ldexpf(1.f, eb - 14);   // 1 / sB
+      if (lane == 0 && sub == 0) isBv[quarter] = 16.f * isA;   // 1 / sB
     }
+    // ---- stage-A operand of the next group (AA is free: A(g) retired)
+    const bool more = g + (int)gridDim.x < G;
+    float isA_next = 1.f;
+    if (more) isA_next = put_a(vn);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -198,16 +228,19 @@ __global__ void __launch_bounds__(256, 1) tcfft(const float2* __restrict__ x, fl
           mma(dd, desc(al + o, SBO_B), desc(bh + o, SBO_B), IB, true);
         }
       }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(barB)));
+      if (more) mma_a();   // A(g+1): its TMEM columns were read out above
     }
-    commit_wait(bar, ph);
+    if (more) load_x(g + 2 * (int)gridDim.x, vn);
+    wait(barB, phB);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // ---- output: lane q0 = 32 warp + lane of every column, q1 = 0..31
-    const float* isBv = reinterpret_cast<const float*>(bar + 2);
-    for (int c = 0; c < NCOL; ++c) {
+    // ---- output: lane q0 = 32 quarter + lane; warp `sub` reads column sub, q1 = 0..31
+    {
+      const int c = sub;
       const float isB = isBv[c];
       const int q0 = 32 * quarter + lane, colc = g * NCOL + c;
-      {
-        const int cb = half;
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
         float d[32];
         ld32(tq + 256 + 64 * c + 32 * cb, d);
 #pragma unroll
@@ -219,11 +252,11 @@ __global__ void __launch_bounds__(256, 1) tcfft(const float2* __restrict__ x, fl
         }
       }
     }
+    isA = isA_next;
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();   // AA / AB / TMEM reused by the next group
-    asm volatile("tcgen05.fence::after_thread_sync;");
+    __syncthreads();   // AB / TMEM-B / isBv reused by the next group
   }
-  if (chk) chk[blockIdx.x * 256 + t] = csum;
+  if (chk) chk[blockIdx.x * NTHR + t] = csum;
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
@@ -282,14 +315,14 @@ int main(int argc, char** argv) {
   cudaMalloc(&dF, (size_t)ncols * N * 8);
   cudaMalloc(&dtw, htw.size() * 8);
   cudaMalloc(&dB, hB.size());
-  cudaMalloc(&dchk, 148 * 256 * 4);
+  cudaMalloc(&dchk, 148 * NTHR * 4);
   cudaMemcpy(dx, hx.data(), hx.size() * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dtw, htw.data(), htw.size() * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, hB.data(), hB.size(), cudaMemcpyHostToDevice);
-  const size_t smem = 2 * SZ_BA + 2 * SZ_BB + 2 * SZ_AA + NCOL * 2 * SZ_AB + 128;
+  const size_t smem = 2 * SZ_BA + 2 * SZ_BB + 2 * SZ_AA + NCOL * 2 * SZ_AB + 512;
   cudaFuncSetAttribute(tcfft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   printf("smem %zu B\n", smem);
-  tcfft<<<148, 256, smem>>>(dx, dF, ncols, dB, dtw, 1, nullptr);
+  tcfft<<<148, NTHR, smem>>>(dx, dF, ncols, dB, dtw, 1, nullptr);
   cudaError_t e = cudaDeviceSynchronize();
   printf("run: %s\n", cudaGetErrorString(e));
   if (e != cudaSuccess) return 1;
@@ -319,10 +352,10 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int i = 0; i < 3; ++i) tcfft<<<148, 256, smem>>>(dx, dF, ncols, dB, dtw, 0, dchk);
+  for (int i = 0; i < 3; ++i) tcfft<<<148, NTHR, smem>>>(dx, dF, ncols, dB, dtw, 0, dchk);
   cudaEventRecord(e0);
   const int reps = 10;
-  for (int i = 0; i < reps; ++i) tcfft<<<148, 256, smem>>>(dx, dF, ncols, dB, dtw, 0, dchk);
+  for (int i = 0; i < reps; ++i) tcfft<<<148, NTHR, smem>>>(dx, dF, ncols, dB, dtw, 0, dchk);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
