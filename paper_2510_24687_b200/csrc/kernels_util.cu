@@ -52,46 +52,56 @@ cudaError_t launch_dot_partial(const float* a, const float* b, size_t count, flo
   return cudaGetLastError();
 }
 
-// Reading G25 (low-harmonic quadrature variant): out[b] = coef * sum of image b, accumulated in
-// float64 by one 1024-thread CTA per image (16-byte loads when the image is 16-byte aligned).
-__global__ void __launch_bounds__(1024) k_lowk_sum(const float* __restrict__ x, size_t per, int b0, double coef,
-                                                   const float* __restrict__ dw, int n, float* __restrict__ out) {
-  __shared__ double red[32];
+// Reading G25 (low-harmonic quadrature variant): out[b] = coef * sum of image b (times the G26
+// factors d[ix] d[iy] when dw != nullptr), as kLowkParts fixed-range partial sums per image in
+// float64; the CTA that finishes last (per-image counter) adds the partials in a fixed order and
+// resets the counter, so the result is deterministic.
+constexpr int kLowkParts = 32;
+__global__ void __launch_bounds__(256) k_lowk_sum(const float* __restrict__ x, size_t per, int b0, double coef,
+                                                  const float* __restrict__ dw, int n, float* __restrict__ out,
+                                                  double* __restrict__ part, unsigned int* __restrict__ cnt) {
+  __shared__ double red[8];
+  __shared__ bool last;
   pdl_trigger();
-  const int b = b0 + blockIdx.x;
+  const int b = b0 + blockIdx.y, q = blockIdx.x;
   const float* p = x + (size_t)b * per;
   double acc = 0.0;
-  if (dw) {   // image sum of D f (reading G26)
-    for (int iy = threadIdx.x >> 5; iy < n; iy += blockDim.x >> 5) {
+  if (dw) {   // rows [n q / P, n (q + 1) / P) of D f
+    const int y0 = n * q / kLowkParts, y1 = n * (q + 1) / kLowkParts;
+    for (int iy = y0 + (threadIdx.x >> 5); iy < y1; iy += blockDim.x >> 5) {
       double row = 0.0;
       for (int ix = threadIdx.x & 31; ix < n; ix += 32) row += (double)__ldg(p + (size_t)iy * n + ix) * dw[ix];
       acc += row * dw[iy];
     }
-  } else if ((per & 3) == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-    const float4* q = reinterpret_cast<const float4*>(p);
-    for (size_t i = threadIdx.x; i < per / 4; i += blockDim.x) {
-      const float4 v = __ldg(q + i);
-      acc += ((double)v.x + (double)v.y) + ((double)v.z + (double)v.w);
-    }
   } else {
-    for (size_t i = threadIdx.x; i < per; i += blockDim.x) acc += (double)__ldg(p + i);
+    const size_t i0 = per * q / kLowkParts, i1 = per * (q + 1) / kLowkParts;
+    for (size_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) acc += (double)__ldg(p + i);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    acc = red[threadIdx.x];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (threadIdx.x == 0) out[b] = (float)(coef * acc);
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    part[(size_t)b * kLowkParts + q] = s;
+    __threadfence();
+    last = atomicAdd(&cnt[b], 1u) == kLowkParts - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (int k = 0; k < kLowkParts; ++k) s += *((volatile double*)&part[(size_t)b * kLowkParts + k]);
+    out[b] = (float)(coef * s);
+    cnt[b] = 0;
   }
 }
 
 cudaError_t launch_lowk_sum(const DevPlan& P, const float* x, size_t per_image, double coef, bool image,
                             cudaStream_t s) {
-  k_lowk_sum<<<P.C.batch, 1024, 0, s>>>(x, per_image, P.C.b0, coef, image ? P.deapod : nullptr, P.C.n,
-                                        P.lowk_add);
+  k_lowk_sum<<<dim3(kLowkParts, P.C.batch), 256, 0, s>>>(x, per_image, P.C.b0, coef, image ? P.deapod : nullptr,
+                                                         P.C.n, P.lowk_add, P.lowk_part, P.lowk_cnt);
   return cudaGetLastError();
 }
 

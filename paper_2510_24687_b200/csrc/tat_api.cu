@@ -25,6 +25,8 @@ struct tat_plan {
   float* pw_img = nullptr;      // power iteration: second image buffer [B][n][n]
   float* pw_part = nullptr;     // kUtilBlocks partial dot products
   float* lowk_buf = nullptr;    // [B] G25 per-image constants (tat_plan_set_quadrature)
+  double* lowk_part = nullptr;  // [B][32] their partial sums
+  unsigned int* lowk_cnt = nullptr;
   const float* deapod_buf = nullptr;   // [n] G26 factors (tat_plan_set_interpolation)
   // inverse (built on first use)
   std::vector<int> node_perm;   // host copy: (j, l') -> adjoint S2 position
@@ -345,12 +347,18 @@ tat_status tat_plan_set_quadrature(tat_plan* plan, int rule) {
     return TAT_OK;
   }
   if (!plan->lowk_buf) {
+    const size_t B = (size_t)plan->P.C.batch;
     void* d = nullptr;
-    cudaError_t e = alloc_ws(plan, (size_t)plan->P.C.batch * sizeof(float), &d);
+    cudaError_t e = alloc_ws(plan, B * (32 * sizeof(double) + sizeof(float) + sizeof(unsigned int)) + 64, &d);
+    if (e == cudaSuccess) e = cudaMemset(d, 0, B * (32 * sizeof(double) + sizeof(float) + sizeof(unsigned int)) + 64);
     if (e != cudaSuccess) return cuda_fail(e, "tat_plan_set_quadrature alloc");
-    plan->lowk_buf = (float*)d;
+    plan->lowk_part = (double*)d;
+    plan->lowk_buf = (float*)(plan->lowk_part + 32 * B);
+    plan->lowk_cnt = (unsigned int*)(plan->lowk_buf + B);
   }
   plan->P.lowk_add = plan->lowk_buf;
+  plan->P.lowk_part = plan->lowk_part;
+  plan->P.lowk_cnt = plan->lowk_cnt;
   return TAT_OK;
 }
 

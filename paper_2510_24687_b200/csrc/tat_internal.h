@@ -130,6 +130,8 @@ struct DevPlan {
   // per-image constants (coef * sum of the call's input image / data), written by k_lowk_sum
   // at the start of each forward / adjoint call and added to every output in the epilogues
   float* lowk_add = nullptr;
+  double* lowk_part = nullptr;        // [batch][32] partial sums (k_lowk_sum)
+  unsigned int* lowk_cnt = nullptr;   // [batch] finished-part counters (kept at 0 between calls)
   // inverse (tat_inverse): the Cartesian targets of column p are the whole chord |q| <= Q_p of
   // the disk, stored in natural q order; k2c_adj then reads them by index (no mask / base)
   const int* k2c_chord = nullptr;
