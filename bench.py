@@ -52,52 +52,43 @@ def peaks():
 
 # ----------------------------------------------------------------------------- models
 def model(info: dict) -> dict:
-    """Algorithmic bytes and flops per launch (whole batch), DESIGN.md "Roofline model".
-    Bytes: each intermediate written once and read once at its stored size, inputs/outputs
-    once, plan tables once per launch.  Flops: 5 m log2 m per m-point complex FFT, 6 per
-    complex twiddle, 14 per bilinear node (3 complex lerps), 2 per real multiply."""
+    """SURVEY §8(d) "Algorithmic bytes" and flops per launch (whole batch), DESIGN.md §7.
+    Bytes: every transposed intermediate (S1..S4) written once and read once at its minimal
+    size (complex64, Hermitian-reduced), inputs / outputs once, plan tables once per call:
+      per image per A (= per A*): 4n^2 + 4 n_t n_det + 16 [n (N/2+1) + 2 N_lam (K+1) + n_t (K+1)],
+      per call: 16 N_lam (K+1) + 4 n_det.
+    Split over the stages as the survey does (K1 = f + S1, K2 = S1 + S2 + tables, K3 = S2 + S3,
+    K4 = S3 + S4, K5 = S4 + g + ring map; the adjoint stages mirror them).
+    Flops: 5 m log2 m per m-point complex FFT (K2: N-point per column, SURVEY §8(d)'s 8.1 GFLOP
+    at C3), the same convention for every stage."""
     n, N, B = info["n"], info["N"], info["batch"]
-    L = N // n
     ncols = N // 2 + 1
     NL = info["J"] + 1
     Kp = info["K"] + 1
-    half = info["n_ring"] // 2
     nphi = info["n_ring"]
     n_t, n_det = info["n_t"], info["n_det"]
     M2 = 2 * info["M"]
-    c8 = 8
     f_b, g_b = 4 * n * n, 4 * n_t * n_det
-    S1, S2, S3, S4 = c8 * n * ncols, c8 * half * NL, c8 * Kp * NL, c8 * Kp * n_t
-    nodes = half * NL
-    Rc = c8 * info.get("n_targets", 0)       # transposed-bilinear target sums per image
+    S1, S2, S3, S4 = 8 * n * ncols, 8 * NL * Kp, 8 * NL * Kp, 8 * n_t * Kp
+    tables = 16 * NL * Kp
     lg = math.log2
     fft = lambda m: 5 * m * lg(m)
-    by = {
-        "K1": B * (f_b + S1), "K2": B * (S1 + S2) + 16 * nodes, "K3": B * (S2 + S3) + 4 * Kp * NL,
-        "K4": B * (S3 + S4), "K5": B * (S4 + g_b) + 4 * n_det,
-        "K5T": B * (g_b + S4) + 4 * n_det, "K4T": B * (S4 + S3) + 4 * Kp * NL,
-        "K3T": B * (S3 + S2), "K2Ta": B * (S2 + Rc) + 16 * info.get("n_targets", 0),
-        "K2Tb": B * (Rc + S1), "K1T": B * (S1 + f_b),
-    }
-    fl = {
-        "K1": B * (n / 2) * L * (fft(n) + 6 * n),
-        "K2": B * ncols * L * (fft(n) + 6 * n) + B * nodes * 14,
-        "K3": B * NL * (fft(nphi) + 6 * Kp),
-        "K4": B * Kp * fft(M2),
-        "K5": B * n_t * fft(nphi),
-    }
-    fl.update({"K5T": fl["K5"], "K4T": fl["K4"] + B * Kp * NL * 6, "K3T": fl["K3"],
-               "K2Ta": B * nodes * 14, "K2Tb": B * ncols * L * (fft(n) + 6 * n), "K1T": fl["K1"]})
-    # the headline's model bytes (SURVEY §8(d)) count the method's intermediates only: the
-    # adjoint column stage as S2 + S1 (+ its node records), not this implementation's Rc round
-    # trip between K2Ta and K2Tb (which the per-kernel rooflines above do include)
-    pair_bytes = (sum(v for k, v in by.items() if k not in ("K2Ta", "K2Tb"))
-                  + B * (S2 + S1) + 12 * 4 * nodes)
-    return {"bytes": by, "flops": fl, "pair_bytes": pair_bytes}
+    fwd = {"K1": B * (f_b + S1), "K2": B * (S1 + S2) + tables, "K3": B * (S2 + S3),
+           "K4": B * (S3 + S4), "K5": B * (S4 + g_b) + 4 * n_det}
+    adj = {"K5T": fwd["K5"], "K4T": fwd["K4"], "K3T": fwd["K3"], "K2T": fwd["K2"], "K1T": fwd["K1"]}
+    by = {**fwd, **adj}
+    fl = {"K1": B * n * fft(N) / 2,            # n/2 complex row-pair transforms of length N
+          "K2": B * ncols * fft(N),
+          "K3": B * NL * fft(nphi),
+          "K4": B * Kp * fft(M2),
+          "K5": B * n_t * fft(nphi) / 2}         # two real time samples per complex transform
+    fl.update({"K5T": fl["K5"], "K4T": fl["K4"], "K3T": fl["K3"], "K2T": fl["K2"], "K1T": fl["K1"]})
+    per_op = B * (f_b + g_b + 16 * (n * ncols + 2 * NL * Kp + n_t * Kp)) + tables + 4 * n_det
+    return {"bytes": by, "flops": fl, "pair_bytes": 2 * per_op, "op_bytes": per_op}
 
 
 BOUND = {"K1": "hbm", "K2": "alu", "K3": "hbm", "K4": "alu", "K5": "hbm",
-         "K5T": "hbm", "K4T": "alu", "K3T": "hbm", "K2Ta": "hbm", "K2Tb": "alu", "K1T": "hbm"}
+         "K5T": "hbm", "K4T": "alu", "K3T": "hbm", "K2T": "alu", "K1T": "hbm"}
 
 
 def measured_traffic(name: str, stage: str):
@@ -284,6 +275,126 @@ def landweber(plan, f, f_host, geo, name, dev, stream, iters: int = 50, reps: in
             "image_pairs_per_s": B * iters / (ms / 1000.0), "final_rel_residual": rel_res}
 
 
+def step_graph(plan, f, g, u):
+    """A CUDA graph of one step (A then A* over the batch) on the current stream."""
+    import torch
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        plan.forward(f, out=g)
+        plan.adjoint(g, out=u)
+    return graph
+
+
+def time_replays(graph, flush, stream, reps: int) -> list:
+    """Per-replay device times (ms) with CUDA events, L2 flushed before each (outside)."""
+    import torch
+    st = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
+    for i in range(reps):
+        flush.zero_()
+        st[i].record(stream)
+        graph.replay()
+        en[i].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in zip(st, en)]
+
+
+def other_configs(names, flush, stream, pk) -> dict:
+    """SURVEY §8(d) per-config numbers: µs per batch A + A* pair (graph replay, median of 20),
+    image-pairs/s and the effective HBM fraction by the §8(d) model bytes."""
+    import torch
+    from paper_2510_24687_b200 import Plan
+    out = {}
+    for name in names:
+        geo = synth.geometry(name)
+        plan = Plan(geo.n, geo.n_det, geo.n_t, geo.R, geo.c, geo.T, geo.batch, geo.angles_array())
+        f = torch.from_numpy(synth.phantom_batch(name)).cuda()
+        g = torch.empty((geo.batch, geo.n_t, geo.n_det), device="cuda")
+        u = torch.empty((geo.batch, geo.n, geo.n), device="cuda")
+        for _ in range(3):
+            plan.forward(f, out=g)
+            plan.adjoint(g, out=u)
+        graph = step_graph(plan, f, g, u)
+        graph.replay()
+        torch.cuda.synchronize()
+        ms = statistics.median(time_replays(graph, flush, stream, 20))
+        mdl = model(plan.info)
+        out[name] = {"us_per_pair": round(1000 * ms, 2),
+                     "image_pairs_per_s": round(geo.batch / (ms / 1000.0), 1),
+                     "hbm_frac": round(mdl["pair_bytes"] / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
+                     "batch": geo.batch}
+        del graph, plan
+    return out
+
+
+def lpd_step_bench(name: str, steps: int, warmup: int, flush, stream, K: int = 5) -> dict:
+    """LPD-shaped training step (§4.2; §8(f) f3): K
+    unrolled primal-dual iterations q <- Gamma(q, A f, y), f <- Lambda(f, A* q) (eq:LPD_dual,
+    eq:LPD_primal) with the CNNs replaced by elementwise maps with learnable scalars (no
+    networks), f0 = q0 = 0, loss ||f_K - f_true||^2, torch.autograd backward through
+    Plan.A / Plan.Astar (backward of A = A^T, of A* = omega A: libtat kernels), then an SGD
+    update.  y = A f_true + 5 % noise.  Eager (autograd), CUDA events per step."""
+    import torch
+    from paper_2510_24687_b200 import Plan
+    geo = synth.geometry(name)
+    B = geo.batch
+    plan = Plan(geo.n, geo.n_det, geo.n_t, geo.R, geo.c, geo.T, B, geo.angles_array())
+    f_true = torch.from_numpy(synth.phantom_batch(name)).cuda()
+    y = plan.forward(f_true)
+    noise = torch.from_numpy(np.stack([synth.random_data(geo.n_t, geo.n_det, 4100 + b)
+                                       for b in range(B)])).cuda()
+    y = y + 0.05 * y.abs().amax(dim=(1, 2), keepdim=True) * noise
+    lam = 1.0 / plan.power_norm(10, seed=4000)
+    a = torch.tensor([1.0, 0.0], device="cuda", requires_grad=True)          # Gamma
+    b = torch.tensor([lam, 0.0], device="cuda", requires_grad=True)          # Lambda
+    opt = torch.optim.SGD([a, b], lr=1e-6)
+    calls = {"forward": 0, "adjoint": 0, "transpose": 0, "forward_scaled": 0}
+    for nm in calls:
+        fn = getattr(plan, nm)
+
+        def wrap(*args, _fn=fn, _nm=nm, **kw):
+            calls[_nm] += 1
+            return _fn(*args, **kw)
+        setattr(plan, nm, wrap)
+
+    def train_step():
+        f = torch.zeros_like(f_true)
+        q = torch.zeros_like(y)
+        for _ in range(K):
+            q = q + a[0] * (plan.A(f) - y) + a[1] * q                       # Gamma stand-in
+            f = torch.relu(f - b[0] * plan.Astar(q) + b[1] * f)              # Lambda stand-in
+        loss = ((f - f_true) ** 2).mean()
+        opt.zero_grad(set_to_none=True)
+        loss.backward()
+        opt.step()
+        return loss
+
+    for _ in range(warmup):
+        train_step()
+    torch.cuda.synchronize()
+    for k in calls:
+        calls[k] = 0
+    st = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        st[i].record(stream)
+        loss = train_step()
+        en[i].record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.median([x.elapsed_time(z) for x, z in zip(st, en)])
+    per = {k: v // steps for k, v in calls.items()}
+    n_a = per["forward"] + per["forward_scaled"]
+    n_as = per["adjoint"] + per["transpose"]
+    return {"workload": f"{name}: LPD-shaped training step, K = {K} unrolled iterations, batch {B}, "
+                        "5% noise, elementwise CNN stand-ins, autograd through Plan.A / Plan.Astar, SGD",
+            "ms_per_step": ms, "steps_per_s": 1000.0 / ms,
+            "operator_evals_per_step": {"A (forward + omega A in backward)": n_a,
+                                        "A* (adjoint + A^T in backward)": n_as},
+            "image_operator_pairs_per_s": B * 0.5 * (n_a + n_as) / (ms / 1000.0),
+            "final_loss": float(loss.item())}
+
+
 def run_gpu(args, rank: int, world: int, local_rank: int):
     import torch
     import torch.distributed as dist
@@ -314,9 +425,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     # kept), so small configurations are not bound by host launch overhead
     graph = None
     if not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step()
+        graph = step_graph(plan, f, g, u)
         graph.replay()
         torch.cuda.synchronize()
     if world > 1:
@@ -355,46 +464,24 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     ms_per_step = total_ms / args.steps
     value = units / (total_ms / 1000.0)
 
-    # ---- end to end: every step copies its batch from pinned host memory (H2D), runs A and A*
-    # and reads the result back (D2H), through the public API; copies and compute run on three
-    # streams with two buffer sets, so step i's H2D / D2H overlap the compute of its neighbours
+    # ---- end to end through the C ABI with HOST buffers: every step tat_pair_host copies its
+    # batch from pinned host memory (H2D), runs A and A*, copies A* g back (D2H); the plan
+    # pipelines the copies of neighbouring steps on its own streams (include/tat.h)
     f_pin = torch.from_numpy(f_host).pin_memory()
     u_pin = [torch.empty((B, geo.n, geo.n), dtype=torch.float32).pin_memory() for _ in range(2)]
-    f_dev = [torch.empty_like(f) for _ in range(2)]
-    u_dev = [torch.empty_like(f) for _ in range(2)]
-    s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    ev = lambda: torch.cuda.Event()
-    in_done, cmp_done, out_done = [ev(), ev()], [ev(), ev()], [ev(), ev()]
-
-    def e2e_step(i):
-        k = i & 1
-        with torch.cuda.stream(s_in):
-            s_in.wait_event(cmp_done[k])          # f_dev[k] free (compute of step i-2 done)
-            f_dev[k].copy_(f_pin, non_blocking=True)
-            in_done[k].record(s_in)
-        s_cmp.wait_event(in_done[k])
-        s_cmp.wait_event(out_done[k])             # u_dev[k] free (D2H of step i-2 done)
-        plan.forward(f_dev[k], out=g, stream=s_cmp)
-        plan.adjoint(g, out=u_dev[k], stream=s_cmp)
-        cmp_done[k].record(s_cmp)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(cmp_done[k])
-            u_pin[k].copy_(u_dev[k], non_blocking=True)
-            out_done[k].record(s_out)
-
-    for e in in_done + cmp_done + out_done:
-        e.record(stream)
+    fp_np, up_np = f_pin.numpy(), [t.numpy() for t in u_pin]
     for i in range(4):
-        e2e_step(i)
+        plan.pair_host(fp_np, up_np[i & 1], stream=stream)
+    plan.join_host(stream)
     torch.cuda.synchronize()
+    e2e_steps = max(3, args.steps)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(3, args.steps)
-    e0.record(s_in)
+    e0.record(stream)
     for i in range(e2e_steps):
-        e2e_step(i)
-    s_out.wait_event(cmp_done[(e2e_steps - 1) & 1])
-    e1.record(s_out)
+        plan.pair_host(fp_np, up_np[i & 1], stream=stream)
+    plan.join_host(stream)
+    e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms, e2e_units = reduce_timing(e0.elapsed_time(e1), B * e2e_steps, world, dev)
     e2e_value = e2e_units / (e2e_ms / 1000.0)
@@ -417,24 +504,31 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         except Exception as exc:   # geometry outside the inverse's support
             inv = {"unavailable": str(exc)}
 
+    pk, pk_kind = peaks()
+    extras = lpd = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras = other_configs([c for c in ("C1", "C2", "C4", "C5") if c != name], flush, stream, pk)
+        lpd = lpd_step_bench("C4", 5, 3, flush, stream)
+
     if rank != 0:
         return 0
 
-    pk, pk_kind = peaks()
     mdl = model(info)
-    per_stage_us = {s: 1000.0 * stage_ms[i] / max(1, (nf if i < 5 else na))
-                    for i, s in enumerate(STAGES)}
+    raw = {s: 1000.0 * stage_ms[i] / max(1, (nf if i < 5 else na)) for i, s in enumerate(STAGES)}
+    per_stage_us = {k: v for k, v in raw.items() if k not in ("K2Ta", "K2Tb")}
+    per_stage_us["K2T"] = raw["K2Ta"] + raw["K2Tb"]     # the adjoint column stage (A*-4)
     dom = max(per_stage_us, key=per_stage_us.get)
     dur_s = per_stage_us[dom] * 1e-6
-    clk = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
     alu_peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12    # TFLOP/s
     if BOUND[dom] == "alu":
         ach = mdl["flops"][dom] / dur_s / 1e12
         roof = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
                 "frac": ach / alu_peak, "traffic": measured_traffic(name, dom),
                 "kernel": dom, "algorithmic_flops": mdl["flops"][dom],
+                "flops_model": "SURVEY §8(d): 5 N log2 N per N-point column transform",
                 "hbm_achieved_gbs": mdl["bytes"][dom] / dur_s / 1e9,
-                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (DESIGN.md)"}
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz; "
+                               "profiles/r2_ubench_fp32.txt measures it"}
     else:
         ach = mdl["bytes"][dom] / dur_s / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -449,15 +543,11 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     floor_tot = sum(v["floor_us"] for v in floors.values())
     stage_floor = {"per_stage": floors, "sum_floor_us": round(floor_tot, 1),
                    "frac": round(floor_tot / sum(per_stage_us.values()), 3),
-                   "model": "max(model bytes / measured HBM peak, model flops / derived FP32 peak)"}
+                   "model": "max(§8(d) model bytes / measured HBM peak, model flops / derived FP32 peak)"}
     eff_hbm = mdl["pair_bytes"] / (ms_per_step * 1e-3) / 1e9     # GB/s, whole batch
     cpu = None
     if world == 1 and not args.no_cpu:
-        pairs, t_work, setup = oracle_sample(name, float(os.environ.get("TAT_ORACLE_BUDGET_S", "10")),
-                                             min_pairs=1, max_pairs=64)
-        cpu = {"value": pairs / t_work, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
-               "sample": f"{pairs} image pair(s) (A then A*) of {name} in float64 direct sums; "
-                         f"table setup {setup:.1f}s excluded"}
+        cpu = cpu_baseline_leg(name, plan, f, g, u, geo)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -467,6 +557,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                    "l2": "flushed (256 MB write) between timed steps, outside the step events",
                    "launch": "CUDA graph replay per step" if graph is not None else "eager"},
         "hbm_roofline_effective": {"model_bytes_per_step": mdl["pair_bytes"],
+                                   "model": "SURVEY §8(d) algorithmic bytes (2 x per-operator)",
                                    "achieved_gbs": eff_hbm, "peak_gbs": pk["hbm_gbs"],
                                    "frac": eff_hbm / pk["hbm_gbs"]},
         "roofline": roof,
@@ -475,16 +566,51 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(f_host.nbytes),
                 "d2h_bytes_per_step": int(u_pin[0].numel() * 4),
-                "pipelined": "H2D / compute / D2H on three streams, two buffer sets"},
+                "path": "tat_pair_host (C ABI, pinned host buffers, copies pipelined on the "
+                        "plan's streams), device-timed over the whole run"},
         "gpu_launches": (info["launches_forward"] + info["launches_adjoint"]) * args.steps,
         "clocks": clocks,
         "landweber": lw,
         "inverse": inv,
+        "other_configs": extras,
+        "lpd_step": lpd,
         "paper_context": "A alone: 0.0055 s at 257^2, 360x513, batch 1 on an Nvidia A2000 "
                          "(PAPER.md L822-825); not this workload",
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_baseline_leg(name, plan, f, g, u, geo) -> dict:
+    """The float64 oracle as it stands, timed on the host cores on a bounded sample of the
+    workload (SURVEY §8(d) "Oracle timing"); the sampled images' oracle outputs are also
+    compared with the GPU's outputs for the same images (rel-L2, the parity bar 1e-4)."""
+    from oracle import tat_oracle as O
+    import torch
+    budget = float(os.environ.get("TAT_ORACLE_BUDGET_S", "10"))
+    C = O.derive_geom(geo)
+    t0 = time.perf_counter()
+    O.forward(np.zeros((geo.n, geo.n)), C)          # untimed warm-up (table caches)
+    setup = time.perf_counter() - t0
+    plan.forward(f, out=g)
+    plan.adjoint(g, out=u)
+    torch.cuda.synchronize()
+    fh, gh, uh = f.cpu().numpy(), g.cpu().numpy(), u.cpu().numpy()
+    done, t_work, worst_a, worst_as = 0, 0.0, 0.0, 0.0
+    while done < 64 and (done < 1 or t_work < budget):
+        b = done % geo.batch
+        t1 = time.perf_counter()
+        ga = O.forward(fh[b].astype(np.float64), C)
+        ua = O.adjoint(gh[b].astype(np.float64), C)
+        t_work += time.perf_counter() - t1
+        worst_a = max(worst_a, float(np.linalg.norm(gh[b] - ga) / np.linalg.norm(ga)))
+        worst_as = max(worst_as, float(np.linalg.norm(uh[b] - ua) / np.linalg.norm(ua)))
+        done += 1
+    return {"value": done / t_work, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+            "sample": f"{done} image pair(s) (A then A*) of {name} in float64 direct sums; "
+                      f"table setup {setup:.1f}s excluded",
+            "parity_on_sample": {"A_rel_l2_max": worst_a, "Astar_rel_l2_max": worst_as,
+                                 "bar": 1e-4}}
 
 
 def main():
@@ -497,6 +623,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-loop", action="store_true", help="skip the NNLS loop measurement")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a graph")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the other-config and LPD-step measurements")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -34,6 +34,18 @@
  * nothing.  The thread-local message of the last failure is tat_last_error().
  * NaN/Inf in f or g propagate (no scan pass).
  *
+ * Alignment: every DEVICE buffer passed to an entry point (f, g, g_obs, r, roi, ...) must be
+ * 16-byte aligned (the kernels move it with bulk copies, TMA and 16-byte vector accesses);
+ * an unaligned pointer is rejected with TAT_ERR_INVALID_ARGUMENT before any launch.  Host
+ * buffers of the *_host variants have no alignment requirement.
+ *
+ * CUDA graphs: every entry point except tat_plan_create, tat_power_norm, tat_nnls_converge
+ * and a tat_inverse with a new r0 is enqueue-only and may be captured.  A launch copies the
+ * plan's operator state (tables, quadrature / interpolation rule) by value into its kernel
+ * parameters, so a graph captured before a tat_plan_set_* call that changed the operator keeps
+ * applying the OLD operator: recapture after such a call (tat_plan_info_t.generation counts
+ * them; a graph is current while the generation it was captured at is unchanged).
+ *
  * Kernels of a call are launched with programmatic dependent launch (each kernel's table loads
  * overlap its predecessor's tail); the environment variable TAT_PDL=0, read at plan creation,
  * disables it (debugging).
@@ -90,6 +102,20 @@ tat_status tat_forward_host(const tat_plan* plan, const float* f_host, float* g_
                             cudaStream_t stream);
 tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_host,
                             cudaStream_t stream);
+
+/* Pipelined host-buffer pair (the end-to-end path of bench.py): g = A f, u = A* g for host
+ * buffers f_host [batch][n][n], u_host [batch][n][n] and optionally g_host [batch][n_t][n_det]
+ * (NULL: g stays on the device).  The plan owns two device staging sets and two copy streams:
+ * the H2D copy of call i runs on the plan's input stream, the operators on `stream`, the D2H
+ * copies on the plan's output stream, so call i's copies overlap the compute of calls i-1 and
+ * i+1 (pinned host memory is required for the overlap; pageable memory works, serialised).
+ * Call i's host buffers may be reused once it has completed; tat_host_join(plan, s) makes
+ * stream s wait for every copy enqueued so far (synchronise s afterwards to read the results).
+ * The first call after a join (or ever) is also ordered after the work already on `stream`.
+ * Not capturable (uses plan-internal streams).  Errors as tat_forward. */
+tat_status tat_pair_host(const tat_plan* plan, const float* f_host, float* g_host, float* u_host,
+                         cudaStream_t stream);
+tat_status tat_host_join(const tat_plan* plan, cudaStream_t stream);
 
 /* ---- Inverse: A^{-1} g by the approximate universal backprojection of
  * PAPER.md §3.3 Algorithm 3 (L703-784): analysis of g on the ring, the sine transform and the
@@ -171,6 +197,23 @@ tat_status tat_nnls(const tat_plan* plan, const float* g_obs, float* f, float* r
 tat_status tat_power_norm(const tat_plan* plan, int iters, unsigned long long seed,
                           double* lambda_max, cudaStream_t stream);
 
+/* tat_nnls_converge: the same iteration with the paper's stopping criterion (§4.3
+ * L968-971: "the L2 norm of an update to the current approximation is smaller than 0.3% of the
+ * L2 norm of the very first (non-zero) approximation"; DESIGN reading G28), per image:
+ *   the first iterate k0 >= 1 with ||f^k0|| > 0 sets the scale s_b = ||f^k0||_2 (no test on it);
+ *   image b stops after the first CHECKED iteration k > k0 with ||f^k - f^(k-1)||_2 < rel_tol s_b
+ *   (the paper's rel_tol = 3e-3); its iterate is then frozen while the other images go on.
+ * Iterations are checked while some image has no scale yet and then every `check_every`-th
+ * (k % check_every == 0; 1 = every iteration, the paper's rule exactly).  Each check is one
+ * deterministic device reduction (fixed-order float64 partials) read by the host.
+ *   iters_out  host [batch]: iterations applied to image b (= the stopping k), or -max_iters if
+ *              the rule was not met within max_iters.
+ * SYNCHRONOUS (host loop; synchronises `stream` at every check).  max_iters, check_every >= 1,
+ * rel_tol > 0; other arguments as tat_nnls. */
+tat_status tat_nnls_converge(const tat_plan* plan, const float* g_obs, float* f, float* r_work,
+                             float lambda, int max_iters, int check_every, double rel_tol, int nonneg,
+                             const float* roi, int* iters_out, cudaStream_t stream);
+
 /* NULL-safe.  The caller must ensure no work using the plan is in flight. */
 void tat_plan_destroy(tat_plan* plan);
 
@@ -187,6 +230,7 @@ typedef struct {
   size_t workspace_bytes, table_bytes;
   int launches_forward, launches_adjoint;
   int n_targets;    /* Cartesian targets of the transposed bilinear (half spectrum, per image) */
+  unsigned generation; /* operator changes by tat_plan_set_* since creation (graph currency) */
 } tat_plan_info_t;
 
 /* ring_index: optional host int array of n_det receiving the ring position r_d of each

@@ -493,6 +493,32 @@ def nnls(g_obs: np.ndarray, f0: np.ndarray, C: Constants, lam: float, iters: int
     return f
 
 
+def nnls_converge(g_obs: np.ndarray, f0: np.ndarray, C: Constants, lam: float, max_iters: int,
+                  rel_tol: float = 3e-3, check_every: int = 1, nonneg: bool = True,
+                  roi: np.ndarray | None = None) -> tuple[np.ndarray, int]:
+    """The NNLS iteration above with the paper's stopping criterion (§4.3:
+    "the L2 norm of an update to the current approximation is smaller than 0.3% of the L2 norm
+    of the very first (non-zero) approximation"), reading G28: the first iterate f^k0 (k0 >= 1)
+    with ||f^k0|| > 0 fixes s = ||f^k0||; the iteration stops after the first checked k > k0
+    with ||f^k - f^(k-1)|| < rel_tol s.  Iterations are checked until s is known, then every
+    check_every-th (k % check_every == 0).  Returns (f, k), or (f, -max_iters) if the rule
+    was not met."""
+    f = np.array(f0, dtype=np.float64)
+    scale = 0.0
+    for k in range(1, max_iters + 1):
+        prev = f
+        f = f - lam * adjoint(forward(f, C) - g_obs, C)              # L841-843
+        if nonneg:
+            f = np.maximum(f, 0.0)                                     # L845
+        if roi is not None:
+            f = f * roi                                                # L848-850
+        if scale == 0.0:
+            scale = float(np.linalg.norm(f))
+        elif k % check_every == 0 and np.linalg.norm(f - prev) < rel_tol * scale:
+            return f, k
+    return f, -max_iters
+
+
 def power_norm(C: Constants, v0: np.ndarray, iters: int) -> float:
     """Largest eigenvalue of A*A (self-adjoint in X; eqn:innerProducts P:L217-222) by power
     iteration from v0: the last Rayleigh quotient <v, A*A v> / <v, v>.  The NNLS step must

@@ -39,8 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = _nvcc()
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    objs, procs = [], []
+    for src in SOURCES:   # compile the translation units concurrently
         obj = os.path.join(objdir, src + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
@@ -48,8 +48,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
         else:
             cmd[1:1] = ["-x", "c++"]
-        subprocess.run(cmd, check=True)
+        procs.append((src, subprocess.Popen(cmd)))
         objs.append(obj)
+    bad = [src for src, p in procs if p.wait() != 0]
+    if bad:
+        raise RuntimeError(f"nvcc failed for {bad}")
     tmp = LIB + ".tmp"
     subprocess.run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], check=True)
     os.replace(tmp, LIB)

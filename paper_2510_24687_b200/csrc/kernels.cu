@@ -276,12 +276,13 @@ cudaError_t configure_kernels(const DevPlan& P) {
   if (e == cudaSuccess) e = configure_ring_kernels(C);
   if (e == cudaSuccess) e = configure_dct_kernels(C);
   if (e == cudaSuccess) e = configure_dense_kernels(C);
-  SETSM(k3_angular_mult, smem_ring(C));
-  SETSM(k4_dct, smem_dct(C));
-  SETSM(k5_synth_restrict, smem_ring(C));
-  SETSM(k5t_analysis, smem_ring(C));
-  SETSM(k4t_dct, smem_dct(C));
-  SETSM(k3t_angular, smem_ring(C));
+  if (smem_ring(C) > (size_t)kSmemLimit || smem_dct(C) > (size_t)kSmemLimit) return cudaErrorInvalidConfiguration;
+  SETSM(k3_angular_mult, kSmemLimit);
+  SETSM(k4_dct, kSmemLimit);
+  SETSM(k5_synth_restrict, kSmemLimit);
+  SETSM(k5t_analysis, kSmemLimit);
+  SETSM(k4t_dct, kSmemLimit);
+  SETSM(k3t_angular, kSmemLimit);
 
 #undef SETSM
   return e;

@@ -138,7 +138,8 @@ size_t smem_dct_fast(const Consts& C) { return (size_t)4 * rstride(dct_fast_nf(C
 cudaError_t configure_dct_kernels(const Consts& C) {
   const int nf = dct_fast_nf(C);
   if (!nf) return cudaSuccess;
-  const int sm = (int)smem_dct_fast(C);
+  if (smem_dct_fast(C) > (size_t)kSmemLimit) return cudaErrorInvalidConfiguration;
+  const int sm = kSmemLimit;
   cudaError_t e = cudaSuccess;
   TAT_DCT_SWITCH(nf, {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k4_dct_fast<NF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);

@@ -294,7 +294,8 @@ size_t smem_ring_fast(const Consts& C) {
 
 cudaError_t configure_ring_kernels(const Consts& C) {
   if (!ring_fast_ok(C)) return cudaSuccess;
-  const int sm = (int)smem_ring_fast(C);
+  if (smem_ring_fast(C) > (size_t)kSmemLimit) return cudaErrorInvalidConfiguration;
+  const int sm = kSmemLimit;
   cudaError_t e = cudaSuccess;
   TAT_RING_SWITCH({
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k3_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);

@@ -39,6 +39,45 @@ __global__ void __launch_bounds__(256) k_dot_partial(const float* a, const float
   if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
 }
 
+// Per-image squared norms of the NNLS update f - fp and of the iterate f (the 0.3 % stopping
+// rule, §4.3): block (k, b) sums a fixed contiguous range of image b with a
+// fixed per-thread order and a fixed float64 tree, so the result is bitwise reproducible.
+__global__ void __launch_bounds__(256) k_diff_norms(const float* __restrict__ f, const float* __restrict__ fp,
+                                                    size_t per, double* part) {
+  __shared__ double red[2][256];
+  const int b = blockIdx.y, k = blockIdx.x;
+  const size_t chunk = (per + kNormParts - 1) / kNormParts;
+  const size_t i0 = (size_t)k * chunk, i1 = i0 + chunk < per ? i0 + chunk : per;
+  const float* x = f + (size_t)b * per;
+  const float* y = fp + (size_t)b * per;
+  float sd = 0.f, sf = 0.f;
+  for (size_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const float a = __ldg(&x[i]), d = a - __ldg(&y[i]);
+    sd = fmaf(d, d, sd);
+    sf = fmaf(a, a, sf);
+  }
+  red[0][threadIdx.x] = sd;
+  red[1][threadIdx.x] = sf;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + w];
+      red[1][threadIdx.x] += red[1][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[((size_t)b * kNormParts + k) * 2] = red[0][0];
+    part[((size_t)b * kNormParts + k) * 2 + 1] = red[1][0];
+  }
+}
+
+cudaError_t launch_diff_norms(const float* f, const float* fp, int batch, size_t per_image, double* part,
+                              cudaStream_t s) {
+  k_diff_norms<<<dim3(kNormParts, batch), 256, 0, s>>>(f, fp, per_image, part);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill_random(float* v, size_t count, unsigned long long seed, cudaStream_t s) {
   k_fill_random<<<kUtilBlocks, 256, 0, s>>>(v, count, seed);
   return cudaGetLastError();

@@ -14,33 +14,51 @@
 
 using namespace tat;
 
+// The operator entry points take `const tat_plan*` (tat.h): the operator a plan applies is fixed
+// between tat_plan_set_* calls.  State those calls create lazily (host-variant staging, power-
+// iteration and inverse buffers, profiling slots) is not part of the operator and is `mutable`.
 struct tat_plan {
   DevPlan P;
   CUtensorMap tm_s1;
   std::vector<int> ring;
-  std::vector<void*> allocs;
-  size_t workspace_bytes = 0, table_bytes = 0;
-  float* stage_in = nullptr;    // host-variant staging: [B][n][n]
-  float* stage_out = nullptr;   // [B][n_t][n_det]
-  float* pw_img = nullptr;      // power iteration: second image buffer [B][n][n]
-  float* pw_part = nullptr;     // kUtilBlocks partial dot products
+  mutable std::vector<void*> allocs;
+  mutable size_t workspace_bytes = 0, table_bytes = 0;
+  unsigned generation = 0;      // bumped by every tat_plan_set_* call that changes the operator
+  mutable float* stage_in = nullptr;    // host-variant staging: [B][n][n]
+  mutable float* stage_out = nullptr;   // [B][n_t][n_det]
+  mutable float* pw_img = nullptr;      // power iteration: second image buffer [B][n][n]
+  mutable float* pw_part = nullptr;     // kUtilBlocks partial dot products
+  // tat_nnls_converge (stopping rule): previous iterate, per-image norm partials, active flags
+  mutable float* nn_prev = nullptr;
+  mutable double* nn_part = nullptr;
+  mutable int* nn_active = nullptr;
+  // tat_pair_host pipeline: two staging sets, copy streams, per-set events
+  mutable bool hp_ready = false, hp_joined = true;
+  mutable unsigned long long hp_calls = 0;
+  mutable cudaStream_t hp_in = nullptr, hp_out = nullptr;
+  mutable cudaEvent_t hp_entry = nullptr, hp_in_done[2] = {}, hp_cmp_done[2] = {}, hp_out_done[2] = {};
+  mutable float *hp_f[2] = {}, *hp_g[2] = {}, *hp_u[2] = {};
   float* lowk_buf = nullptr;    // [B] G25 per-image constants (tat_plan_set_quadrature)
   double* lowk_part = nullptr;  // [B][32] their partial sums
   unsigned int* lowk_cnt = nullptr;
   const float* deapod_buf = nullptr;   // [n] G26 factors (tat_plan_set_interpolation)
   // inverse (built on first use)
   std::vector<int> node_perm;   // host copy: (j, l') -> adjoint S2 position
-  bool inv_ready = false;
-  DevPlan Pinv;                 // P with the inverse tables swapped in
-  double inv_r0 = -1.0;
-  unsigned char* inv_region = nullptr;
-  float* inv_csum = nullptr;
-  int inv_annulus = 0;
+  mutable bool inv_ready = false;
+  mutable DevPlan Pinv;                 // P with the inverse tables swapped in
+  mutable double inv_r0 = -1.0;
+  mutable unsigned char* inv_region = nullptr;
+  mutable float* inv_csum = nullptr;
+  mutable int inv_annulus = 0;
   // profiling
-  int prof_max = 0, prof_fwd = 0, prof_adj = 0;
-  std::vector<cudaEvent_t> prof_ev;   // (prof_max) sets of kProfEv events
-  std::vector<char> prof_kind;        // 1 = forward, 0 = adjoint, per used slot
+  mutable int prof_max = 0, prof_fwd = 0, prof_adj = 0;
+  mutable std::vector<cudaEvent_t> prof_ev;   // (prof_max) sets of kProfEv events
+  mutable std::vector<char> prof_kind;        // 1 = forward, 0 = adjoint, per used slot
 };
+
+// Device buffers handed to the kernels must be 16-byte aligned (bulk copies, TMA, float4 and
+// 16-byte cp.async accesses); an unaligned view is rejected before any launch.
+static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 static thread_local std::string g_last_error;
 
@@ -54,7 +72,7 @@ static tat_status cuda_fail(cudaError_t e, const char* where) {
 }
 
 template <class T>
-static cudaError_t upload(tat_plan* p, const std::vector<T>& h, const T** dst, size_t& bytes) {
+static cudaError_t upload(const tat_plan* p, const std::vector<T>& h, const T** dst, size_t& bytes) {
   void* d = nullptr;
   size_t nb = h.size() * sizeof(T);
   if (nb == 0) nb = sizeof(T);
@@ -67,13 +85,26 @@ static cudaError_t upload(tat_plan* p, const std::vector<T>& h, const T** dst, s
   return e;
 }
 
-static cudaError_t alloc_ws(tat_plan* p, size_t nb, void** dst) {
+static cudaError_t alloc_ws(const tat_plan* p, size_t nb, void** dst) {
   cudaError_t e = cudaMalloc(dst, nb);
   if (e == cudaSuccess) { p->allocs.push_back(*dst); p->workspace_bytes += nb; }
   return e;
 }
 
-static void free_all(tat_plan* p) {
+static void free_all(const tat_plan* p) {
+  if (p->hp_ready) {
+    cudaStreamSynchronize(p->hp_in);
+    cudaStreamSynchronize(p->hp_out);
+    for (int k = 0; k < 2; ++k) {
+      cudaEventDestroy(p->hp_in_done[k]);
+      cudaEventDestroy(p->hp_cmp_done[k]);
+      cudaEventDestroy(p->hp_out_done[k]);
+    }
+    cudaEventDestroy(p->hp_entry);
+    cudaStreamDestroy(p->hp_in);
+    cudaStreamDestroy(p->hp_out);
+    p->hp_ready = false;
+  }
   for (void* a : p->allocs) cudaFree(a);
   p->allocs.clear();
   for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
@@ -242,13 +273,14 @@ tat_status tat_plan_info(const tat_plan* plan, tat_plan_info_t* out, int* ring_i
   if (!plan || !out) return fail(TAT_ERR_INVALID_ARGUMENT, "plan or out is NULL");
   fill_info(plan->P.C, out);
   out->workspace_bytes = plan->workspace_bytes;
+  out->generation = plan->generation;
   out->table_bytes = plan->table_bytes;
   if (ring_index)
     for (int d = 0; d < plan->P.C.n_det; ++d) ring_index[d] = plan->ring[d];
   return TAT_OK;
 }
 
-static cudaEvent_t* prof_slot(tat_plan* p, bool fwd) {
+static cudaEvent_t* prof_slot(const tat_plan* p, bool fwd) {
   if (p->prof_max <= 0) return nullptr;
   int used = p->prof_fwd + p->prof_adj;
   if (used >= p->prof_max) return nullptr;
@@ -259,8 +291,8 @@ static cudaEvent_t* prof_slot(tat_plan* p, bool fwd) {
 
 tat_status tat_forward(const tat_plan* plan, const float* f, float* g, cudaStream_t stream) {
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
-  tat_plan* p = const_cast<tat_plan*>(plan);
-  cudaEvent_t* ev = prof_slot(p, true);
+  if (!al16(f) || !al16(g)) return fail(TAT_ERR_INVALID_ARGUMENT, "f and g must be 16-byte aligned");
+  cudaEvent_t* ev = prof_slot(plan, true);
   cudaError_t e = launch_forward(plan->P, plan->tm_s1, f, g, stream, ev);
   if (e != cudaSuccess) return cuda_fail(e, "tat_forward launch");
   return TAT_OK;
@@ -268,14 +300,14 @@ tat_status tat_forward(const tat_plan* plan, const float* f, float* g, cudaStrea
 
 tat_status tat_adjoint(const tat_plan* plan, const float* g, float* f, cudaStream_t stream) {
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
-  tat_plan* p = const_cast<tat_plan*>(plan);
-  cudaEvent_t* ev = prof_slot(p, false);
+  if (!al16(f) || !al16(g)) return fail(TAT_ERR_INVALID_ARGUMENT, "f and g must be 16-byte aligned");
+  cudaEvent_t* ev = prof_slot(plan, false);
   cudaError_t e = launch_adjoint(plan->P, plan->tm_s1, g, f, stream, ev);
   if (e != cudaSuccess) return cuda_fail(e, "tat_adjoint launch");
   return TAT_OK;
 }
 
-static tat_status ensure_staging(tat_plan* p) {
+static tat_status ensure_staging(const tat_plan* p) {
   if (p->stage_in) return TAT_OK;
   const Consts& C = p->P.C;
   void *a = nullptr, *b = nullptr;
@@ -295,7 +327,7 @@ static tat_status ensure_staging(tat_plan* p) {
 tat_status tat_forward_host(const tat_plan* plan, const float* f_host, float* g_host,
                             cudaStream_t stream) {
   if (!plan || !f_host || !g_host) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
-  tat_plan* p = const_cast<tat_plan*>(plan);
+  const tat_plan* p = plan;
   tat_status st = ensure_staging(p);
   if (st != TAT_OK) return st;
   const Consts& C = p->P.C;
@@ -313,7 +345,7 @@ tat_status tat_forward_host(const tat_plan* plan, const float* f_host, float* g_
 tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_host,
                             cudaStream_t stream) {
   if (!plan || !f_host || !g_host) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
-  tat_plan* p = const_cast<tat_plan*>(plan);
+  const tat_plan* p = plan;
   tat_status st = ensure_staging(p);
   if (st != TAT_OK) return st;
   const Consts& C = p->P.C;
@@ -328,9 +360,83 @@ tat_status tat_adjoint_host(const tat_plan* plan, const float* g_host, float* f_
   return TAT_OK;
 }
 
+// ------------------------------------------------------------------ pipelined host-buffer pair
+static tat_status ensure_pair(const tat_plan* p) {
+  if (p->hp_ready) return TAT_OK;
+  const Consts& C = p->P.C;
+  const size_t nimg = (size_t)C.batch * C.n * C.n * sizeof(float);
+  const size_t ndat = (size_t)C.batch * C.n_t * C.n_det * sizeof(float);
+  cudaError_t e = cudaSuccess;
+  void* d = nullptr;
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    if ((e = alloc_ws(p, nimg, &d)) == cudaSuccess) p->hp_f[k] = (float*)d; else break;
+    if ((e = alloc_ws(p, ndat, &d)) == cudaSuccess) p->hp_g[k] = (float*)d; else break;
+    if ((e = alloc_ws(p, nimg, &d)) == cudaSuccess) p->hp_u[k] = (float*)d; else break;
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->hp_in, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->hp_out, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->hp_entry, cudaEventDisableTiming);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&p->hp_in_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->hp_cmp_done[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->hp_out_done[k], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "tat_pair_host setup");
+  p->hp_ready = true;
+  return TAT_OK;
+}
+
+tat_status tat_pair_host(const tat_plan* plan, const float* f_host, float* g_host, float* u_host,
+                         cudaStream_t stream) {
+  if (!plan || !f_host || !u_host) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  tat_status st = ensure_pair(plan);
+  if (st != TAT_OK) return st;
+  const tat_plan* p = plan;
+  const Consts& C = p->P.C;
+  const size_t nimg = (size_t)C.batch * C.n * C.n * sizeof(float);
+  const size_t ndat = (size_t)C.batch * C.n_t * C.n_det * sizeof(float);
+  const int k = (int)(p->hp_calls & 1);
+  cudaError_t e = cudaSuccess;
+  if (p->hp_joined) {   // first call after a join: ordered after the work already on `stream`
+    e = cudaEventRecord(p->hp_entry, stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->hp_in, p->hp_entry, 0);
+  }
+  // set k is free once the compute of call i-2 has read hp_f[k] (and its D2H, below, is done)
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->hp_in, p->hp_cmp_done[k], 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(p->hp_f[k], f_host, nimg, cudaMemcpyHostToDevice, p->hp_in);
+  if (e == cudaSuccess) e = cudaEventRecord(p->hp_in_done[k], p->hp_in);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, p->hp_in_done[k], 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, p->hp_out_done[k], 0);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_pair_host H2D");
+  st = tat_forward(plan, p->hp_f[k], p->hp_g[k], stream);
+  if (st != TAT_OK) return st;
+  st = tat_adjoint(plan, p->hp_g[k], p->hp_u[k], stream);
+  if (st != TAT_OK) return st;
+  e = cudaEventRecord(p->hp_cmp_done[k], stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->hp_out, p->hp_cmp_done[k], 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(u_host, p->hp_u[k], nimg, cudaMemcpyDeviceToHost, p->hp_out);
+  if (e == cudaSuccess && g_host) e = cudaMemcpyAsync(g_host, p->hp_g[k], ndat, cudaMemcpyDeviceToHost, p->hp_out);
+  if (e == cudaSuccess) e = cudaEventRecord(p->hp_out_done[k], p->hp_out);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_pair_host D2H");
+  p->hp_calls++;
+  p->hp_joined = false;
+  return TAT_OK;
+}
+
+tat_status tat_host_join(const tat_plan* plan, cudaStream_t stream) {
+  if (!plan) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (!plan->hp_ready || plan->hp_calls == 0) return TAT_OK;
+  const int k = (int)((plan->hp_calls - 1) & 1);   // the copy-out stream is in order
+  cudaError_t e = cudaStreamWaitEvent(stream, plan->hp_out_done[k], 0);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_host_join");
+  plan->hp_joined = true;
+  return TAT_OK;
+}
+
 // ------------------------------------------------------------------ autograd support
 tat_status tat_transpose(const tat_plan* plan, const float* g, float* f, cudaStream_t stream) {
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  if (!al16(f) || !al16(g)) return fail(TAT_ERR_INVALID_ARGUMENT, "f and g must be 16-byte aligned");
   DevPlan Q = plan->P;
   Q.C.omega = 1.0;   // omega enters only through the K4T multiplier: A^T = A* / omega
   cudaError_t e = launch_adjoint(Q, plan->tm_s1, g, f, stream, nullptr);
@@ -343,9 +449,11 @@ tat_status tat_plan_set_quadrature(tat_plan* plan, int rule) {
   if (rule != TAT_QUAD_TRAPEZOID && rule != TAT_QUAD_LOWK)
     return fail(TAT_ERR_INVALID_ARGUMENT, "unknown quadrature rule");
   if (rule == TAT_QUAD_TRAPEZOID) {
+    if (plan->P.lowk_add) plan->generation++;
     plan->P.lowk_add = nullptr;
     return TAT_OK;
   }
+  if (!plan->P.lowk_add) plan->generation++;
   if (!plan->lowk_buf) {
     const size_t B = (size_t)plan->P.C.batch;
     void* d = nullptr;
@@ -367,9 +475,11 @@ tat_status tat_plan_set_interpolation(tat_plan* plan, int rule) {
   if (rule != TAT_INTERP_BILINEAR && rule != TAT_INTERP_DEAPOD)
     return fail(TAT_ERR_INVALID_ARGUMENT, "unknown interpolation rule");
   if (rule == TAT_INTERP_BILINEAR) {
+    if (plan->P.deapod) plan->generation++;
     plan->P.deapod = nullptr;
     return TAT_OK;
   }
+  if (!plan->P.deapod) plan->generation++;
   if (!plan->deapod_buf) {
     const Consts& C = plan->P.C;
     std::vector<float> w(C.n);
@@ -391,6 +501,7 @@ tat_status tat_plan_set_interpolation(tat_plan* plan, int rule) {
 tat_status tat_forward_scaled(const tat_plan* plan, const float* f, float* g, float alpha,
                               cudaStream_t stream) {
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  if (!al16(f) || !al16(g)) return fail(TAT_ERR_INVALID_ARGUMENT, "f and g must be 16-byte aligned");
   if (!std::isfinite(alpha)) return fail(TAT_ERR_INVALID_ARGUMENT, "alpha is not finite");
   DevPlan Q = plan->P;
   Q.epi_scale = alpha;
@@ -400,7 +511,7 @@ tat_status tat_forward_scaled(const tat_plan* plan, const float* f, float* g, fl
 }
 
 // ------------------------------------------------------------------ inverse (Algorithm 3)
-static tat_status inverse_setup(tat_plan* p) {
+static tat_status inverse_setup(const tat_plan* p) {
   if (p->inv_ready) return TAT_OK;
   const Consts& C = p->P.C;
   InvTables I;
@@ -448,6 +559,7 @@ static tat_status inverse_setup(tat_plan* p) {
 tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0,
                        cudaStream_t stream) {
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  if (!al16(f) || !al16(g)) return fail(TAT_ERR_INVALID_ARGUMENT, "f and g must be 16-byte aligned");
   const Consts& C = plan->P.C;
   if (!(r0 > 0.0 && r0 < C.R)) return fail(TAT_ERR_INVALID_ARGUMENT, "r0 must lie in (0, R)");
   if (C.R != 1.0 || C.c != 1.0)
@@ -456,7 +568,7 @@ tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0
     return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: needs detectors on a canonical ring");
   if (!dct4_ok(C) && !dct_fast_r(C))
     return fail(TAT_ERR_UNSUPPORTED_GEOMETRY, "inverse: no sine-transform kernel for this 2M");
-  tat_plan* p = const_cast<tat_plan*>(plan);
+  const tat_plan* p = plan;
   tat_status st = inverse_setup(p);
   if (st != TAT_OK) return st;
   cudaError_t e = cudaSuccess;
@@ -471,7 +583,10 @@ tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0
         else if (r < C.R) { v = 2; ++cnt; }
         reg[(size_t)iy * C.n + ix] = v;
       }
-    e = cudaMemcpy(p->inv_region, reg.data(), reg.size(), cudaMemcpyHostToDevice);
+    // ordered on `stream`: earlier inverse calls still reading the old mask finish first; the
+    // synchronisation keeps the host vector alive until the (pageable) copy has been staged
+    e = cudaMemcpyAsync(p->inv_region, reg.data(), reg.size(), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return cuda_fail(e, "inverse region upload");
     p->inv_r0 = r0;
     p->inv_annulus = cnt;
@@ -488,6 +603,7 @@ tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0
 tat_status tat_residual(const tat_plan* plan, const float* f, const float* g_obs, float* r,
                         cudaStream_t stream) {
   if (!plan || !f || !g_obs || !r) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  if (!al16(f) || !al16(g_obs) || !al16(r)) return fail(TAT_ERR_INVALID_ARGUMENT, "buffers must be 16-byte aligned");
   DevPlan Q = plan->P;
   Q.epi_sub = g_obs;
   cudaError_t e = launch_forward(Q, plan->tm_s1, f, r, stream, nullptr);
@@ -498,6 +614,7 @@ tat_status tat_residual(const tat_plan* plan, const float* f, const float* g_obs
 tat_status tat_adjoint_step(const tat_plan* plan, const float* r, float* f, float lambda,
                             int nonneg, const float* roi, cudaStream_t stream) {
   if (!plan || !f || !r) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  if (!al16(f) || !al16(r) || !al16(roi)) return fail(TAT_ERR_INVALID_ARGUMENT, "buffers must be 16-byte aligned");
   if (!std::isfinite(lambda)) return fail(TAT_ERR_INVALID_ARGUMENT, "lambda is not finite");
   DevPlan Q = plan->P;
   Q.epi_update = nonneg ? 2 : 1;
@@ -522,7 +639,85 @@ tat_status tat_nnls(const tat_plan* plan, const float* g_obs, float* f, float* r
   return TAT_OK;
 }
 
-static cudaError_t dot_host(tat_plan* p, const float* a, const float* b, size_t count,
+tat_status tat_nnls_converge(const tat_plan* plan, const float* g_obs, float* f, float* r_work,
+                             float lambda, int max_iters, int check_every, double rel_tol, int nonneg,
+                             const float* roi, int* iters_out, cudaStream_t stream) {
+  if (!plan || !g_obs || !f || !r_work || !iters_out)
+    return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
+  if (!al16(f) || !al16(g_obs) || !al16(r_work) || !al16(roi))
+    return fail(TAT_ERR_INVALID_ARGUMENT, "buffers must be 16-byte aligned");
+  if (max_iters < 1 || check_every < 1 || !(rel_tol > 0.0) || !std::isfinite(lambda))
+    return fail(TAT_ERR_INVALID_ARGUMENT, "max_iters, check_every must be >= 1, rel_tol > 0, lambda finite");
+  const tat_plan* p = plan;
+  const Consts& C = p->P.C;
+  const int B = C.batch;
+  const size_t per = (size_t)C.n * C.n;
+  cudaError_t e = cudaSuccess;
+  void* d = nullptr;
+  if (!p->nn_prev) {
+    if ((e = alloc_ws(p, (size_t)B * per * sizeof(float), &d)) == cudaSuccess) p->nn_prev = (float*)d;
+    if (e == cudaSuccess && (e = alloc_ws(p, (size_t)B * kNormParts * 2 * sizeof(double), &d)) == cudaSuccess)
+      p->nn_part = (double*)d;
+    if (e == cudaSuccess && (e = alloc_ws(p, (size_t)B * sizeof(int), &d)) == cudaSuccess) p->nn_active = (int*)d;
+    if (e != cudaSuccess) {
+      p->nn_prev = nullptr;
+      return cuda_fail(e, "tat_nnls_converge buffers");
+    }
+  }
+  std::vector<int> active(B, 1), iters(B, -max_iters);
+  std::vector<double> first(B, 0.0), part((size_t)B * kNormParts * 2);
+  e = cudaMemcpyAsync(p->nn_active, active.data(), B * sizeof(int), cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  DevPlan R = p->P;          // r = A f - g_obs
+  R.epi_sub = g_obs;
+  DevPlan U = p->P;          // f <- P(f - lambda A* r) for the active images
+  U.epi_update = nonneg ? 2 : 1;
+  U.epi_tau = lambda;
+  U.epi_roi = roi;
+  U.epi_active = p->nn_active;
+  int live = B;
+  for (int k = 1; k <= max_iters && live > 0 && e == cudaSuccess; ++k) {
+    bool unset = false;
+    for (int b = 0; b < B; ++b) unset |= active[b] && first[b] == 0.0;
+    const bool chk = unset || k % check_every == 0;
+    if (chk) e = cudaMemcpyAsync(p->nn_prev, f, (size_t)B * per * sizeof(float), cudaMemcpyDeviceToDevice, stream);
+    if (e == cudaSuccess) e = launch_forward(R, p->tm_s1, f, r_work, stream, nullptr);
+    if (e == cudaSuccess) e = launch_adjoint(U, p->tm_s1, r_work, f, stream, nullptr);
+    if (e != cudaSuccess || !chk) continue;
+    e = launch_diff_norms(f, p->nn_prev, B, per, p->nn_part, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(part.data(), p->nn_part, part.size() * sizeof(double),
+                                              cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) break;
+    bool changed = false;
+    for (int b = 0; b < B; ++b) {
+      if (!active[b]) continue;
+      double dd = 0.0, ff = 0.0;
+      for (int q = 0; q < kNormParts; ++q) {   // fixed order
+        dd += part[((size_t)b * kNormParts + q) * 2];
+        ff += part[((size_t)b * kNormParts + q) * 2 + 1];
+      }
+      if (first[b] == 0.0) {   // the first non-zero approximation sets the scale (no test on it)
+        if (ff > 0.0) first[b] = std::sqrt(ff);
+      } else if (std::sqrt(dd) < rel_tol * first[b]) {
+        active[b] = 0;
+        iters[b] = k;
+        --live;
+        changed = true;
+      }
+    }
+    if (changed && live > 0) {
+      e = cudaMemcpyAsync(p->nn_active, active.data(), B * sizeof(int), cudaMemcpyHostToDevice, stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    }
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "tat_nnls_converge");
+  for (int b = 0; b < B; ++b) iters_out[b] = iters[b];
+  return TAT_OK;
+}
+
+static cudaError_t dot_host(const tat_plan* p, const float* a, const float* b, size_t count,
                             cudaStream_t s, double* out) {
   cudaError_t e = launch_dot_partial(a, b, count, p->pw_part, s);
   float part[kUtilBlocks];
@@ -537,7 +732,7 @@ static cudaError_t dot_host(tat_plan* p, const float* a, const float* b, size_t 
 tat_status tat_power_norm(const tat_plan* plan, int iters, unsigned long long seed,
                           double* lambda_max, cudaStream_t stream) {
   if (!plan || !lambda_max || iters < 1) return fail(TAT_ERR_INVALID_ARGUMENT, "bad arguments");
-  tat_plan* p = const_cast<tat_plan*>(plan);
+  const tat_plan* p = plan;
   tat_status st = ensure_staging(p);
   if (st != TAT_OK) return st;
   const Consts& C = p->P.C;

@@ -126,6 +126,9 @@ struct DevPlan {
   float epi_scale = 1.f;   // forward: stores epi_scale * (A f) (- epi_sub)
   float epi_tau = 0.f;
   int epi_update = 0;
+  // tat_nnls_converge: per-image flags [batch]; an image whose flag is 0 keeps its iterate (the
+  // update epilogue stores nothing for it).  nullptr: every image is updated.
+  const int* epi_active = nullptr;
   // low-harmonic quadrature variant (reading G25; tat_plan_set_quadrature): when set, [batch]
   // per-image constants (coef * sum of the call's input image / data), written by k_lowk_sum
   // at the start of each forward / adjoint call and added to every output in the epilogues
@@ -178,6 +181,7 @@ __device__ __forceinline__ void epi_adj_store(const DevPlan& P, float* f, size_t
   if (VAR && P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n * P.C.n)];
   if (VAR && P.deapod) v *= P.deapod[ixy % P.C.n] * P.deapod[ixy / P.C.n];
   if (P.epi_update) {
+    if (P.epi_active && !__ldg(&P.epi_active[i / ((size_t)P.C.n * P.C.n)])) return;
     float o = f[i] - P.epi_tau * v;
     if (P.epi_update == 2) o = fmaxf(o, 0.f);
     if (P.epi_roi) o *= __ldg(&P.epi_roi[ixy]);
@@ -191,6 +195,10 @@ __device__ __forceinline__ void epi_adj_store(const DevPlan& P, float* f, size_t
 // Launchers (kernels.cu).  ev != nullptr: record ev[i] before stage i and ev[5] at the end
 // (adjoint: ev[6] between the two K2T kernels).
 constexpr int kProfEv = 7;
+// Every kernel's dynamic shared-memory attribute is set to this device-wide limit (never to a
+// per-plan size): the attribute is process-global, so a later plan with smaller tables must not
+// lower the limit an earlier plan's launches rely on.  Launch sizes are checked against it.
+constexpr int kSmemLimit = 227 * 1024;
 cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float* f, float* g,
                            cudaStream_t s, cudaEvent_t* ev);
 cudaError_t launch_adjoint(const DevPlan& P, const CUtensorMap& tm, const float* g, float* f,
@@ -268,6 +276,11 @@ constexpr int kUtilBlocks = 296;
 cudaError_t launch_fill_random(float* v, size_t count, unsigned long long seed, cudaStream_t s);
 cudaError_t launch_scale(float* v, size_t count, float f, cudaStream_t s);
 cudaError_t launch_dot_partial(const float* a, const float* b, size_t count, float* partial, cudaStream_t s);
+// tat_nnls_converge: per image b, kNormParts fixed-range partials of (sum (f - fp)^2, sum f^2)
+// in float64 at part[(b * kNormParts + k) * 2 + {0, 1}] (summed on the host in a fixed order)
+constexpr int kNormParts = 32;
+cudaError_t launch_diff_norms(const float* f, const float* fp, int batch, size_t per_image, double* part,
+                              cudaStream_t s);
 // G25: P.lowk_add[b] = coef * sum of image b of x (per_image floats each), b = b0 .. b0 + batch - 1
 // (forward: weighted by the G26 factors when P.deapod is set)
 cudaError_t launch_lowk_sum(const DevPlan& P, const float* x, size_t per_image, double coef, bool image,

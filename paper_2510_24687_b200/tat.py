@@ -27,7 +27,7 @@ EXPORTS = ("tat_plan_create", "tat_forward", "tat_adjoint", "tat_forward_host",
            "tat_transpose", "tat_forward_scaled", "tat_inverse",
            "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm",
            "tat_plan_set_quadrature", "tat_plan_set_interpolation", "tat_status_string",
-           "tat_last_error")
+           "tat_last_error", "tat_pair_host", "tat_host_join", "tat_nnls_converge")
 
 QUAD_TRAPEZOID, QUAD_LOWK = 0, 1        # tat_plan_set_quadrature rules (DESIGN reading G25)
 INTERP_BILINEAR, INTERP_DEAPOD = 0, 1   # tat_plan_set_interpolation rules (reading G26)
@@ -49,7 +49,7 @@ class PlanInfo(ctypes.Structure):
                 ("h", ctypes.c_double), ("wJ", ctypes.c_double),
                 ("workspace_bytes", ctypes.c_size_t), ("table_bytes", ctypes.c_size_t),
                 ("launches_forward", ctypes.c_int), ("launches_adjoint", ctypes.c_int),
-                ("n_targets", ctypes.c_int)]
+                ("n_targets", ctypes.c_int), ("generation", ctypes.c_uint)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -92,6 +92,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.tat_adjoint_step.argtypes = [vp, vp, vp, f32, i, vp, vp]
     lib.tat_nnls.argtypes = [vp, vp, vp, vp, f32, i, i, vp, vp]
     lib.tat_power_norm.argtypes = [vp, i, ctypes.c_ulonglong, dp, vp]
+    lib.tat_pair_host.argtypes = [vp, vp, vp, vp, vp]
+    lib.tat_host_join.argtypes = [vp, vp]
+    lib.tat_nnls_converge.argtypes = [vp, vp, vp, vp, f32, i, i, d, i, vp, ip, vp]
     lib.tat_status_string.argtypes = [i]
     lib.tat_status_string.restype = ctypes.c_char_p
     lib.tat_last_error.argtypes = []
@@ -101,7 +104,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "tat_plan_host_multiplier", "tat_profile_begin", "tat_profile_end",
                  "tat_transpose", "tat_forward_scaled", "tat_inverse",
                  "tat_residual", "tat_adjoint_step", "tat_nnls", "tat_power_norm",
-                 "tat_plan_set_quadrature", "tat_plan_set_interpolation"):
+                 "tat_plan_set_quadrature", "tat_plan_set_interpolation", "tat_pair_host",
+                 "tat_host_join", "tat_nnls_converge"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -187,6 +191,8 @@ class Plan:
         if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
                 and tuple(t.shape) == shape):
             raise ValueError(f"{name} must be a contiguous float32 CUDA tensor of shape {shape}")
+        if t.data_ptr() % 16:
+            raise ValueError(f"{name} must be 16-byte aligned (include/tat.h)")
 
     def forward(self, f, out=None, stream=None):
         """g = A f on the current (or given) torch stream; no host synchronisation."""
@@ -307,6 +313,41 @@ class Plan:
                                   float(lam), int(iters), int(nonneg), self._roi(roi),
                                   self._stream(stream)))
         return f
+
+    def nnls_converge(self, g_obs, f, lam: float, max_iters: int, rel_tol: float = 3e-3,
+                      check_every: int = 1, nonneg: bool = True, roi=None, r_work=None, stream=None):
+        """NNLS with the paper's stopping rule (synchronous).  Returns the
+        per-image iteration counts (negative: not converged within max_iters)."""
+        import torch
+        self._chk(g_obs, (self.batch, self.n_t, self.n_det), "g_obs")
+        self._chk(f, (self.batch, self.n, self.n), "f")
+        r = r_work if r_work is not None else torch.empty_like(g_obs)
+        self._chk(r, (self.batch, self.n_t, self.n_det), "r_work")
+        it = np.zeros(self.batch, dtype=np.int32)
+        _check(self._lib.tat_nnls_converge(self._h, ctypes.c_void_p(g_obs.data_ptr()),
+                                           ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(r.data_ptr()),
+                                           float(lam), int(max_iters), int(check_every), float(rel_tol),
+                                           int(nonneg), self._roi(roi),
+                                           it.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                           self._stream(stream)))
+        return it
+
+    def pair_host(self, f_host: np.ndarray, u_host: np.ndarray, g_host=None, stream=None):
+        """Pipelined g = A f, u = A* g from / to host buffers (tat_pair_host); enqueue-only,
+        results valid after join_host(stream) and a synchronisation of that stream."""
+        assert f_host.dtype == np.float32 and f_host.flags.c_contiguous and f_host.shape == (self.batch, self.n, self.n)
+        assert u_host.dtype == np.float32 and u_host.flags.c_contiguous and u_host.shape == (self.batch, self.n, self.n)
+        gp = None
+        if g_host is not None:
+            assert g_host.dtype == np.float32 and g_host.flags.c_contiguous
+            assert g_host.shape == (self.batch, self.n_t, self.n_det)
+            gp = g_host.ctypes.data
+        _check(self._lib.tat_pair_host(self._h, ctypes.c_void_p(f_host.ctypes.data), ctypes.c_void_p(gp),
+                                       ctypes.c_void_p(u_host.ctypes.data), self._stream(stream)))
+
+    def join_host(self, stream=None):
+        """Make the stream wait for every copy tat_pair_host has enqueued (tat_host_join)."""
+        _check(self._lib.tat_host_join(self._h, self._stream(stream)))
 
     def power_norm(self, iters: int = 20, seed: int = 0, stream=None) -> float:
         """Largest eigenvalue of A*A by power iteration (synchronous setup call)."""

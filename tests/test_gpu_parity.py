@@ -108,22 +108,56 @@ def test_parity_other_grids(torch_cuda, n, n_t, T):
     _check(_run(torch_cuda, plan, g=gr)[0], O.adjoint(gr[0].astype(np.float64), C), "A*")
 
 
+def _adjoint_identity(torch, plan, geo, C, f, g):
+    """<A f, g>_Y = <f, A* g>_X per image (eqn:innerProducts P:L217-222, discretised as G18),
+    GPU outputs, inner products in float64 on the host; bound ADJ_TOL ||A f||_Y ||g||_Y."""
+    wY = C.dt * 2 * np.pi * C.R / C.n_ring
+    wX = C.h * C.h
+    Af = _run(torch, plan, f=f).astype(np.float64)
+    Asg = _run(torch, plan, g=g).astype(np.float64)
+    worst = 0.0
+    for b in range(f.shape[0]):
+        lhs = wY * np.sum(Af[b] * g[b].astype(np.float64))
+        rhs = wX * np.sum(f[b].astype(np.float64) * Asg[b])
+        bound = np.sqrt(wY * np.sum(Af[b] * Af[b])) * np.sqrt(wY * np.sum(g[b].astype(np.float64) ** 2))
+        worst = max(worst, abs(lhs - rhs) / bound)
+        assert abs(lhs - rhs) <= ADJ_TOL * bound, (b, lhs, rhs, bound)
+    return worst
+
+
 @pytest.mark.parametrize("name", ["T32", "C1", "C2"])
 def test_adjoint_identity_gpu(torch_cuda, name):
     geo = synth.geometry(name)
     plan = _plan(geo, batch=1)
     C = O.derive_geom(geo)
-    wY = C.dt * 2 * np.pi * C.R / C.n_ring
-    wX = C.h * C.h
     for s in range(5):
         f = synth.random_image(geo.n, 300 + s)[None]
         g = synth.random_data(geo.n_t, geo.n_det, 400 + s)[None]
-        Af = _run(torch_cuda, plan, f=f).astype(np.float64)
-        Asg = _run(torch_cuda, plan, g=g).astype(np.float64)
-        lhs = wY * np.sum(Af * g)
-        rhs = wX * np.sum(f * Asg)
-        bound = ADJ_TOL * np.sqrt(wY * np.sum(Af * Af)) * np.sqrt(wY * np.sum(g.astype(np.float64) ** 2))
-        assert abs(lhs - rhs) <= bound, (lhs, rhs, bound)
+        _adjoint_identity(torch_cuda, plan, geo, C, f, g)
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_adjoint_identity_gpu_full_batch(torch_cuda, name):
+    """The north star's 1e-5 adjoint test on the two-stage column engines (n = 512: C3,
+    n = 256: C4, n = 1024: C5) at each configuration's own batch, a distinct random (f, g)
+    per image, in the launch configuration bench.py times."""
+    geo = synth.geometry(name)
+    plan = _plan(geo)
+    C = O.derive_geom(geo)
+    f = np.stack([synth.random_image(geo.n, 600 + b) for b in range(geo.batch)])
+    g = np.stack([synth.random_data(geo.n_t, geo.n_det, 700 + b) for b in range(geo.batch)])
+    _adjoint_identity(torch_cuda, plan, geo, C, f, g)
+
+
+def test_adjoint_identity_phantoms_c3(torch_cuda):
+    """Same identity with g = A f of the C3 phantoms (structured, not white) against
+    phantoms of the next seeds: the pairing bench.py's A then A* step produces."""
+    geo = synth.geometry("C3")
+    plan = _plan(geo)
+    C = O.derive_geom(geo)
+    f = synth.phantom_batch("C3")
+    g = _run(torch_cuda, plan, f=np.stack([synth.phantom("C3", 16 + b) for b in range(16)]))
+    _adjoint_identity(torch_cuda, plan, geo, C, f, g)
 
 
 def test_delta_and_rotation_gpu(torch_cuda):
@@ -167,24 +201,100 @@ def test_zero_input_gives_zero(torch_cuda):
     assert np.all(_run(torch_cuda, plan, g=zg) == 0)
 
 
-@pytest.mark.parametrize("name,images", [("C3", [0, 7, 15]), ("C4", [0, 33, 63]), ("C5", [0, 3])])
+@pytest.mark.parametrize("name,images", [("C3", list(range(16))), ("C4", list(range(0, 64, 4))),
+                                         ("C5", list(range(4)))])
 def test_parity_full_size(torch_cuda, name, images):
     """Full BASELINE sizes in the launch configuration bench.py times (whole batch on the GPU),
-    checked image by image against the oracle on sampled images."""
+    checked image by image against the oracle: every image of C3 and C5, 16 of C4's 64."""
     geo = synth.geometry(name)
     C = O.derive_geom(geo)
     plan = _plan(geo)
     f = synth.phantom_batch(name)
     g_gpu = _run(torch_cuda, plan, f=f)
-    gs = []
     for b in images:
-        ref = O.forward(f[b].astype(np.float64), C)
-        _check(g_gpu[b], ref, f"{name} A image {b}")
-        gs.append(ref)
+        _check(g_gpu[b], O.forward(f[b].astype(np.float64), C), f"{name} A image {b}")
     u_gpu = _run(torch_cuda, plan, g=g_gpu)
     for b in images:
         ref = O.adjoint(g_gpu[b].astype(np.float64), C)
         _check(u_gpu[b], ref, f"{name} A* image {b}")
+
+
+def test_graph_replay_matches_eager_c3(torch_cuda):
+    """bench.py times a CUDA-graph replay of the step (A then A*): the replayed results equal
+    the eager launches bit for bit, and image 5 matches the oracle."""
+    torch = torch_cuda
+    geo = synth.geometry("C3")
+    plan = _plan(geo)
+    f = torch.from_numpy(synth.phantom_batch("C3")).cuda()
+    g = torch.empty((geo.batch, geo.n_t, geo.n_det), device="cuda")
+    u = torch.empty((geo.batch, geo.n, geo.n), device="cuda")
+    plan.forward(f, out=g)
+    plan.adjoint(g, out=u)
+    torch.cuda.synchronize()
+    g_eager, u_eager = g.clone(), u.clone()
+    g.zero_()
+    u.zero_()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        plan.forward(f, out=g)
+        plan.adjoint(g, out=u)
+    g.zero_()
+    u.zero_()
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(g, g_eager) and torch.equal(u, u_eager)
+    C = O.derive_geom(geo)
+    _check(g[5].cpu().numpy(), O.forward(f[5].cpu().numpy().astype(np.float64), C), "graph A 5")
+    _check(u[5].cpu().numpy(), O.adjoint(g[5].cpu().numpy().astype(np.float64), C), "graph A* 5")
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_host_buffer_abi(torch_cuda, name):
+    """tat_forward_host / tat_adjoint_host (H2D + operator + D2H on the stream): the same
+    kernels as the device entry points, so the results are equal bit for bit; checked against
+    the oracle on one image."""
+    torch = torch_cuda
+    geo = synth.geometry(name)
+    plan = _plan(geo)
+    f = synth.phantom_batch(name)
+    g_h = np.empty((geo.batch, geo.n_t, geo.n_det), np.float32)
+    plan.forward_host(f, g_h)
+    torch.cuda.synchronize()
+    u_h = np.empty((geo.batch, geo.n, geo.n), np.float32)
+    plan.adjoint_host(g_h, u_h)
+    torch.cuda.synchronize()
+    g_d = _run(torch, plan, f=f)
+    u_d = _run(torch, plan, g=g_h)
+    assert np.array_equal(g_h, g_d) and np.array_equal(u_h, u_d)
+    C = O.derive_geom(geo)
+    _check(g_h[-1], O.forward(f[-1].astype(np.float64), C), f"{name} host A")
+    _check(u_h[-1], O.adjoint(g_h[-1].astype(np.float64), C), f"{name} host A*")
+
+
+@pytest.mark.parametrize("n,n_det,n_ring,dense", [(32, 16, 16, False), (32, 8, 8, False),
+                                                  (32, 12, 16, False), (32, 6, None, True),
+                                                  (32, 14, None, True)])
+def test_small_rings_generic_kernels(torch_cuda, n, n_det, n_ring, dense):
+    """n_ring < 32 runs the generic ring kernels (kernels.cu k3_angular_mult, k5_synth_restrict,
+    k5t_analysis, k3t_angular): canonical rings of 8 and 16 positions (full and partial) and
+    dense-mode geometries whose polar grid has n_phi = 8 or 16, with batch 2."""
+    if dense:
+        ang = np.sort(np.random.default_rng(n_det).uniform(0.0, 2 * np.pi, n_det))
+    else:
+        ang = np.asarray(synth.ring_angles(n_det, n_ring, 3))
+    geo = synth.Geometry(n, n_det, 2 * n, batch=2, angles=tuple(ang))
+    C = O.derive(n, n_det, 2 * n, 1.0, 1.0, 2.0, ang)
+    assert bool(C.dense) == dense and C.n_ring < 32
+    plan = _plan(geo)
+    f = np.stack([synth.phantom("C1", b, n=n) for b in range(2)])
+    g_gpu = _run(torch_cuda, plan, f=f)
+    gr = np.stack([synth.random_data(2 * n, n_det, 90 + b) for b in range(2)])
+    u_gpu = _run(torch_cuda, plan, g=gr)
+    for b in range(2):
+        _check(g_gpu[b], O.forward(f[b].astype(np.float64), C), f"small ring A {b}")
+        _check(u_gpu[b], O.adjoint(gr[b].astype(np.float64), C), f"small ring A* {b}")
+    _adjoint_identity(torch_cuda, plan, geo, C, f, gr)
 
 
 def test_parity_mixed_engines_and_arc_at_n256(torch_cuda):

@@ -126,8 +126,17 @@ def test_check2_brute_force_kwave_n32():
         g = O.forward(f, C)
         gb = _brute_force(f, C)
         nrm = np.linalg.norm(gb)
-        assert np.linalg.norm(g - gb) / nrm <= 2.5e-2                       # raw (n=32 is coarse)
-        gk = _brute_force(Kw * f, C) - (C.dlam ** 2 / 12) * (C.h ** 2 / (2 * np.pi)) * f.sum()
+        # reading G27: at n = 32 the raw error is dominated by the G9 trapezoid
+        # offset -(dlam^2/12)(h^2/2pi) sum f, a t-independent constant fixed by the definition;
+        # its size e_off is predicted here, not fitted.  Hard gates: the survey's 1.5e-2 on the
+        # raw error with only that analytic constant removed, and the raw error itself within
+        # e_off + 1.5e-2 (measured: 1.2e-3 .. 2.1e-3 and 1.57e-2 .. 2.15e-2 over seeds 7-16).
+        off = (C.dlam ** 2 / 12) * (C.h ** 2 / (2 * np.pi)) * f.sum()
+        e_off = abs(off) * np.sqrt(g.size) / nrm
+        raw = np.linalg.norm(g - gb) / nrm
+        assert np.linalg.norm(g - (gb - off)) / nrm <= 1.5e-2             # raw, G9 offset removed
+        assert raw <= e_off + 1.5e-2                                       # raw, derived bound
+        gk = _brute_force(Kw * f, C) - off
         assert np.linalg.norm(g - gk) / nrm <= 1.5e-3                       # calibrated
 
 

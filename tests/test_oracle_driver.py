@@ -84,3 +84,35 @@ def test_monotone_descent_and_projection_invariants(t32):
         assert res <= prev * (1 + 1e-12)
         assert f.min() >= 0.0 and np.all(f[roi == 0] == 0.0)
         prev = res
+
+
+def test_stopping_rule_against_eigendecomposition(t32, dense_t32):
+    """nnls_converge (reading G28) pinned by an independent route: for the
+    unconstrained iteration from f0 = 0 the update is f^k - f^(k-1) = (I - lam M)^(k-1) lam b,
+    M = A*A = omega A^T A, b = A* g (dense T32 operator), evaluated through numpy.linalg.eigh of
+    M; the first k >= 2 whose update norm is below 0.3 % of ||f^1|| = ||lam b|| is the stop."""
+    C = t32
+    A = dense_t32
+    M = C.omega * A.T @ A
+    w, V = np.linalg.eigh(0.5 * (M + M.T))
+    lam = 1.0 / w.max()
+    g = synth.random_data(C.n_t, C.n_det, 31).astype(np.float64)
+    b = C.omega * A.T @ g.ravel()
+    c = V.T @ (lam * b)
+    s = np.linalg.norm(lam * b)
+    k_ref = next(k for k in range(2, 5000)
+                 if np.linalg.norm((1.0 - lam * w) ** (k - 1) * c) < 3e-3 * s)
+    f, k = O.nnls_converge(g, np.zeros((C.n, C.n)), C, lam, 5000, nonneg=False)
+    assert k == k_ref
+    x = np.clip(lam * w, 0.0, None)
+    f_ref = V @ (lam * np.where(x > 0, -np.expm1(k * np.log1p(-x)) / np.where(x > 0, x, 1), k) * (V.T @ b))
+    # (k float64 iterations vs the spectral closed form; the near-null modes amplify rounding)
+    assert np.linalg.norm(f.ravel() - f_ref) <= 1e-6 * np.linalg.norm(f_ref)
+    # checked every m-th iteration: the update norms are non-increasing (|1 - lam w| <= 1), so
+    # the stop is the first multiple of m at or after k_ref
+    for m in (3, 7):
+        _, km = O.nnls_converge(g, np.zeros((C.n, C.n)), C, lam, 5000, check_every=m, nonneg=False)
+        assert km == -(-k_ref // m) * m
+    # not converged within the cap: negative count
+    _, kc = O.nnls_converge(g, np.zeros((C.n, C.n)), C, lam, k_ref - 1, nonneg=False)
+    assert kc == -(k_ref - 1)
