@@ -519,7 +519,10 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     per_stage_us["K2T"] = raw["K2Ta"] + raw["K2Tb"]     # the adjoint column stage (A*-4)
     dom = max(per_stage_us, key=per_stage_us.get)
     dur_s = per_stage_us[dom] * 1e-6
-    alu_peak = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12    # TFLOP/s
+    # FP32 FFMA peak MEASURED on this pool's B200 (tools/ubench_fp32.cu, profiles/
+    # r2_ubench_fp32.txt: 3.553e13 lane-ops/s = 71.1 TFLOP/s at 1965 MHz; 95 % of the 74.4
+    # TFLOP/s that 148 SM x 128 lanes x 2 x 1965 MHz gives), scaled to the run's max clock
+    alu_peak = 2 * 3.553e13 / 1e12 * pk.get("sm_max_mhz", 1965.0) / 1965.0    # TFLOP/s
     if BOUND[dom] == "alu":
         ach = mdl["flops"][dom] / dur_s / 1e12
         roof = {"bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
@@ -527,8 +530,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                 "kernel": dom, "algorithmic_flops": mdl["flops"][dom],
                 "flops_model": "SURVEY §8(d): 5 N log2 N per N-point column transform",
                 "hbm_achieved_gbs": mdl["bytes"][dom] / dur_s / 1e9,
-                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz; "
-                               "profiles/r2_ubench_fp32.txt measures it"}
+                "peak_source": "measured FFMA rate (tools/ubench_fp32.cu, profiles/r2_ubench_fp32.txt)"}
     else:
         ach = mdl["bytes"][dom] / dur_s / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -543,7 +545,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     floor_tot = sum(v["floor_us"] for v in floors.values())
     stage_floor = {"per_stage": floors, "sum_floor_us": round(floor_tot, 1),
                    "frac": round(floor_tot / sum(per_stage_us.values()), 3),
-                   "model": "max(§8(d) model bytes / measured HBM peak, model flops / derived FP32 peak)"}
+                   "model": "max(§8(d) model bytes / measured HBM peak, model flops / measured FP32 peak)"}
     eff_hbm = mdl["pair_bytes"] / (ms_per_step * 1e-3) / 1e9     # GB/s, whole batch
     cpu = None
     if world == 1 and not args.no_cpu:

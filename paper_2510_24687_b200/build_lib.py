@@ -33,17 +33,20 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every translation unit and link libtat.so (or `out`, with extra -D `defines`:
+    tuning variants, e.g. python -m paper_2510_24687_b200.build_lib --out /tmp/v.so -DX=1)."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
     nvcc = _nvcc()
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build") if out is None else out + ".objs"
     os.makedirs(objdir, exist_ok=True)
     objs, procs = [], []
     for src in SOURCES:   # compile the translation units concurrently
         obj = os.path.join(objdir, src + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
+               *defines, "-I", INCLUDE, "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
         else:
@@ -53,11 +56,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     bad = [src for src, p in procs if p.wait() != 0]
     if bad:
         raise RuntimeError(f"nvcc failed for {bad}")
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     subprocess.run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                defines=[a for a in sys.argv[1:] if a.startswith("-D")], out=out))

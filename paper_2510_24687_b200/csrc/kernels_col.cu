@@ -355,6 +355,459 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPl
   }
 }
 
+// ================================================================== adjoint, fused (K2T)
+// The whole adjoint column stage A*-4 in one kernel (Alg. 2 steps 5-6, with
+// step 5's interpolation replaced by the exact transpose of A-2's bilinear gather, reading G4):
+// one CTA per (column p, group of images).  The column's target records (which nodes of the
+// window, with which bilinear weights, sum into each Cartesian target (p, q); 12 bytes each)
+// are staged in shared memory once and reused for every image; per image, the node window
+// (the nodes with p0 in {p-1, p}: one contiguous range of the adjoint S2) arrives by a bulk
+// copy double-buffered one image ahead.  Phase 1 forms the target sums in a fixed order
+// (deterministic, no atomics) into a compact array that aliases the column buffer; then stage
+// B^H (only the present q1 are read), stage A^H and the residue sums as in k2c_adj.  Columns
+// whose records or window exceed the shared-memory caps (the origin columns) read them from
+// global memory instead.
+template <int n>
+__global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adjf(DevPlan P) {
+  using G = ColGeo<n>;
+  constexpr int R = G::R, J = G::J, NRES = G::NRES, Q0 = G::Q0, T = G::T, NW = T / 32;
+  extern __shared__ __align__(128) float2 sm[];
+  const Consts& C = P.C;
+  const int t = threadIdx.x, j = t % J, sg = t / J, lane = t & 31, warp = t >> 5;
+  // CTA -> work item: the slow columns (origin region: over the shared-memory caps) first, one
+  // image per CTA, so they run concurrently with everything else and are not the kernel's tail;
+  // then the other columns, k2f_ipc images per CTA
+  const int ngrp = (C.batch + C.k2f_ipc - 1) / C.k2f_ipc;
+  const int nsl = C.k2f_nslow * C.batch;
+  const bool slow = (int)blockIdx.x < nsl;
+  int p, bA, bB;
+  if (slow) {
+    p = __ldg(&P.k2f_cols[blockIdx.x / C.batch]);
+    bA = C.b0 + blockIdx.x % C.batch;
+    bB = bA + 1;
+  } else {
+    const int id = blockIdx.x - nsl;
+    p = __ldg(&P.k2f_cols[C.k2f_nslow + id / ngrp]);
+    bA = C.b0 + (id % ngrp) * C.k2f_ipc;
+    bB = min(bA + C.k2f_ipc, C.b0 + C.batch);
+  }
+  float2* Wb = sm;                                                     // column buffer / targets
+  uint32_t* recs = reinterpret_cast<uint32_t*>(sm + G::WS);            // [rcap][3]
+  float2* win = sm + G::WS + (3 * C.k2f_rcap + 1) / 2;                 // 2 x [wcap]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(win + 2 * C.k2f_wcap);
+  float2 A[NRES][R];
+  PowR<G::R, kFactPow> pw;
+  col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
+  const int r0 = __ldg(&P.k2f_recptr[p]), nrec = __ldg(&P.k2f_recptr[p + 1]) - r0;
+  const int t0 = __ldg(&P.k2t_colptr[p]), ntg = __ldg(&P.k2t_colptr[p + 1]) - t0;
+  const int w0 = __ldg(&P.k2_colptr[p > 0 ? p - 1 : 0]), nwin = __ldg(&P.k2_colptr[p + 1]) - w0;
+  const uint32_t m = __ldg(&P.k2c_mask[(size_t)p * Q0 + t]);
+  const int base = __ldg(&P.k2c_base[(size_t)p * Q0 + t]) - t0;
+  const size_t img = (size_t)C.half * C.NL;
+  const uint32_t* rp = slow ? P.k2f_rec + (size_t)3 * r0 : recs;
+  // targets with more than two entries: their descriptors (index in column, first entry, count)
+  // and entry lists are column constants, staged after the records once per CTA (fast columns)
+  const int o0 = __ldg(&P.k2f_ovptr[p]), nov = __ldg(&P.k2f_ovptr[p + 1]) - o0;
+  const int e0 = nov > 0 ? __ldg(&P.k2f_ovt[o0]).y : 0;
+  const int ne = nov > 0 ? __ldg(&P.k2f_ovt[o0 + nov - 1]).y + __ldg(&P.k2f_ovt[o0 + nov - 1]).z - e0 : 0;
+  int4* ovt_s = reinterpret_cast<int4*>(recs + 3 * nrec);                // nrec: multiple of 4
+  int2* ove_s = reinterpret_cast<int2*>(ovt_s + nov);
+  const int4* ovt = slow ? P.k2f_ovt + o0 : ovt_s;
+  const int2* ove = slow ? P.k2f_ov + e0 : ove_s;
+  if (!slow) {
+    for (int i = t; i < nov; i += T) ovt_s[i] = __ldg(&P.k2f_ovt[o0 + i]);
+    for (int i = t; i < ne; i += T) ove_s[i] = __ldg(&P.k2f_ov[e0 + i]);
+  }
+  auto issue = [&](int b, int slot) {   // thread 0: node window of image b -> win[slot]
+    const size_t s0 = ((size_t)b * img + w0) & ~(size_t)1;
+    const size_t s1 = ((size_t)b * img + w0 + nwin + 1) & ~(size_t)1;
+    ac::mbar_expect_tx(&bar[slot], (uint32_t)(s1 - s0) * 8);
+    ac::bulk_g2s(win + slot * C.k2f_wcap, P.S2 + s0, (uint32_t)(s1 - s0) * 8, &bar[slot]);
+  };
+  if (t == 0) {   // the records are plan tables: staged before the predecessor has finished
+    ac::mbar_init(&bar[0], 1);
+    ac::mbar_init(&bar[1], 1);
+    ac::mbar_init(&bar[2], 1);
+    ac::fence_mbar_init();
+    if (!slow && nrec > 0) {
+      ac::mbar_expect_tx(&bar[2], (uint32_t)nrec * 12);
+      ac::bulk_g2s(recs, P.k2f_rec + (size_t)3 * r0, (uint32_t)nrec * 12, &bar[2]);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (t == 0 && !slow) issue(bA, 0);
+  __syncthreads();
+  if (!slow && nrec > 0) ac::mbar_wait(&bar[2], 0);
+  for (int b = bA; b < bB; ++b) {
+    const int it = b - bA, slot = it & 1;
+    if (t == 0 && !slow && b + 1 < bB) {
+      ac::fence_proxy_async();
+      issue(b + 1, slot ^ 1);
+    }
+    const float2* wv;
+    if (!slow) {
+      ac::mbar_wait(&bar[slot], (it >> 1) & 1);
+      wv = win + slot * C.k2f_wcap + (int)(((size_t)b * img + w0) & 1);
+    } else {
+      wv = P.S2 + (size_t)b * img + w0;
+    }
+    // phase 1: target sums (fixed order: entry 0, then entry 1), KU targets per thread per
+    // pass with every load issued before the arithmetic (the slow columns read global memory)
+    constexpr int KU = 4;
+    for (int q = t; q < ntg; q += KU * T) {
+      uint32_t i01[KU], wa[KU], wb[KU];
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int qq = q + k * T;
+        const bool ok = qq < ntg;
+        i01[k] = ok ? rp[3 * qq] : 0u;
+        wa[k] = ok ? rp[3 * qq + 1] : 0u;
+        wb[k] = ok ? rp[3 * qq + 2] : 0u;
+      }
+      float2 v0[KU], v1[KU];
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const bool ov = (i01[k] >> 16) == 0xFFFFu;
+        v0[k] = ov ? make_float2(0.f, 0.f) : wv[i01[k] & 0xFFFFu];
+        v1[k] = ov ? make_float2(0.f, 0.f) : wv[i01[k] >> 16];
+      }
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int qq = q + k * T;
+        if (qq >= ntg) break;
+        if ((i01[k] >> 16) == 0xFFFFu) continue;   // more than two entries: second pass
+        const float w0f = __uint_as_float(wa[k]), w1f = __uint_as_float(wb[k]);
+        float2 acc = __fmul2_rn(make_float2(w0f, w0f), v0[k]);
+        Wb[qq] = __ffma2_rn(make_float2(w1f, w1f), v1[k], acc);
+      }
+    }
+    // second pass: targets with more than two entries (1.5 % at C3; up to ~280 entries near the
+    // origin), one warp each: lane l sums the entries e = l (mod 32) in order, then a fixed
+    // xor-butterfly combines the lanes (deterministic)
+    auto butterfly_store = [&](float2 acc, int dst) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+      }
+      if (lane == 0) Wb[dst] = acc;
+    };
+    for (int o = warp; o < nov; o += NW) {
+      const int4 d = ovt[o];
+      float2 acc = make_float2(0.f, 0.f);
+      for (int e = lane; e < d.z; e += 32) {
+        const int2 en = ove[d.y - e0 + e];
+        const float w = __int_as_float(en.y);
+        acc = __ffma2_rn(make_float2(w, w), wv[en.x], acc);
+      }
+      butterfly_store(acc, d.x);
+    }
+    __syncthreads();
+    {   // stage B^H: A~[q0][j] = sum_q1 W_J^{-q1 j} F~[q0 + Q0 q1]
+      float2 u[J];
+      const float2* rb = Wb + base;
+#pragma unroll
+      for (int c = 0; c < J; ++c) {
+        const uint32_t below = m & ((1u << c) - 1u);
+        u[c] = ((m >> c) & 1u) ? rb[__popc(below)] : make_float2(0.f, 0.f);
+      }
+      __syncthreads();   // the target sums alias the column buffer
+      ce::dftr<J, 1>(u);
+#pragma unroll
+      for (int c = 0; c < J; ++c) Wb[G::widx(t, c)] = u[c];
+    }
+    __syncthreads();
+    float2 acc[R];
+    stage_a_adj<G>(Wb, A, pw, j, sg, acc);
+    residue_reduce<G>(Wb, acc, j, sg);
+    float2* out = P.S1 + ((size_t)b * C.ncols + p) * n;
+    for (int y = t; y < n; y += T) out[y] = residue_sum<G>(Wb, y);
+    __syncthreads();   // Wb free; win[slot] consumed
+  }
+}
+
+// ================================================================== K2Ta, multi-image
+// The transposed bilinear alone (target sums -> Rc, read by k2c_adj), with k2c_adjf's tables and
+// work split: one CTA per (column, group of images), the column's records and overflow lists
+// staged in shared memory once, one node window per image double-buffered by bulk copies; the
+// slow (origin) columns run one image per CTA at the head of the grid from global memory.
+// Fixed-order sums, the > 2-entry targets by one warp each (lane-strided, xor butterfly).
+constexpr int kSumfT = 256;
+__global__ void __launch_bounds__(kSumfT) k2t_sumf(DevPlan P) {
+  constexpr int T = kSumfT, NW = T / 32;
+  extern __shared__ __align__(128) float2 sm[];
+  const Consts& C = P.C;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int ngrp = (C.batch + C.k2f_ipc - 1) / C.k2f_ipc;
+  const int nsl = C.k2f_nslow * C.batch;
+  const bool slow = (int)blockIdx.x < nsl;
+  int p, bA, bB;
+  if (slow) {
+    p = __ldg(&P.k2f_cols[blockIdx.x / C.batch]);
+    bA = C.b0 + blockIdx.x % C.batch;
+    bB = bA + 1;
+  } else {
+    const int id = blockIdx.x - nsl;
+    p = __ldg(&P.k2f_cols[C.k2f_nslow + id / ngrp]);
+    bA = C.b0 + (id % ngrp) * C.k2f_ipc;
+    bB = min(bA + C.k2f_ipc, C.b0 + C.batch);
+  }
+  uint32_t* recs = reinterpret_cast<uint32_t*>(sm);                    // [rcap][3]
+  float2* win = sm + (3 * C.k2f_rcap + 1) / 2;                         // 2 x [wcap]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(win + 2 * C.k2f_wcap);
+  const int r0 = __ldg(&P.k2f_recptr[p]), nrec = __ldg(&P.k2f_recptr[p + 1]) - r0;
+  const int t0 = __ldg(&P.k2t_colptr[p]), ntg = __ldg(&P.k2t_colptr[p + 1]) - t0;
+  const int w0 = __ldg(&P.k2_colptr[p > 0 ? p - 1 : 0]), nwin = __ldg(&P.k2_colptr[p + 1]) - w0;
+  const size_t img = (size_t)C.half * C.NL;
+  const uint32_t* rp = slow ? P.k2f_rec + (size_t)3 * r0 : recs;
+  const int o0 = __ldg(&P.k2f_ovptr[p]), nov = __ldg(&P.k2f_ovptr[p + 1]) - o0;
+  const int e0 = nov > 0 ? __ldg(&P.k2f_ovt[o0]).y : 0;
+  const int ne = nov > 0 ? __ldg(&P.k2f_ovt[o0 + nov - 1]).y + __ldg(&P.k2f_ovt[o0 + nov - 1]).z - e0 : 0;
+  int4* ovt_s = reinterpret_cast<int4*>(recs + 3 * nrec);
+  int2* ove_s = reinterpret_cast<int2*>(ovt_s + nov);
+  const int4* ovt = slow ? P.k2f_ovt + o0 : ovt_s;
+  const int2* ove = slow ? P.k2f_ov + e0 : ove_s;
+  if (!slow) {
+    for (int i = t; i < nov; i += T) ovt_s[i] = __ldg(&P.k2f_ovt[o0 + i]);
+    for (int i = t; i < ne; i += T) ove_s[i] = __ldg(&P.k2f_ov[e0 + i]);
+  }
+  auto issue = [&](int b, int slot) {
+    const size_t s0 = ((size_t)b * img + w0) & ~(size_t)1;
+    const size_t s1 = ((size_t)b * img + w0 + nwin + 1) & ~(size_t)1;
+    ac::mbar_expect_tx(&bar[slot], (uint32_t)(s1 - s0) * 8);
+    ac::bulk_g2s(win + slot * C.k2f_wcap, P.S2 + s0, (uint32_t)(s1 - s0) * 8, &bar[slot]);
+  };
+  if (t == 0) {
+    ac::mbar_init(&bar[0], 1);
+    ac::mbar_init(&bar[1], 1);
+    ac::mbar_init(&bar[2], 1);
+    ac::fence_mbar_init();
+    if (!slow && nrec > 0) {
+      ac::mbar_expect_tx(&bar[2], (uint32_t)nrec * 12);
+      ac::bulk_g2s(recs, P.k2f_rec + (size_t)3 * r0, (uint32_t)nrec * 12, &bar[2]);
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (t == 0 && !slow) issue(bA, 0);
+  __syncthreads();
+  if (!slow && nrec > 0) ac::mbar_wait(&bar[2], 0);
+  for (int b = bA; b < bB; ++b) {
+    const int it = b - bA, slot = it & 1;
+    if (t == 0 && !slow && b + 1 < bB) {
+      ac::fence_proxy_async();
+      issue(b + 1, slot ^ 1);
+    }
+    const float2* wv;
+    if (!slow) {
+      ac::mbar_wait(&bar[slot], (it >> 1) & 1);
+      wv = win + slot * C.k2f_wcap + (int)(((size_t)b * img + w0) & 1);
+    } else {
+      wv = P.S2 + (size_t)b * img + w0;
+    }
+    float2* Rc = P.Rc + (size_t)b * C.ntpad + t0;
+    constexpr int KU = 4;
+    for (int q = t; q < ntg; q += KU * T) {
+      uint32_t i01[KU], wa[KU], wb[KU];
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int qq = q + k * T;
+        const bool ok = qq < ntg;
+        i01[k] = ok ? rp[3 * qq] : 0u;
+        wa[k] = ok ? rp[3 * qq + 1] : 0u;
+        wb[k] = ok ? rp[3 * qq + 2] : 0u;
+      }
+      float2 v0[KU], v1[KU];
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const bool ov = (i01[k] >> 16) == 0xFFFFu;
+        v0[k] = ov ? make_float2(0.f, 0.f) : wv[i01[k] & 0xFFFFu];
+        v1[k] = ov ? make_float2(0.f, 0.f) : wv[i01[k] >> 16];
+      }
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int qq = q + k * T;
+        if (qq >= ntg) break;
+        if ((i01[k] >> 16) == 0xFFFFu) continue;
+        const float w0f = __uint_as_float(wa[k]), w1f = __uint_as_float(wb[k]);
+        const float2 acc = __fmul2_rn(make_float2(w0f, w0f), v0[k]);
+        Rc[qq] = __ffma2_rn(make_float2(w1f, w1f), v1[k], acc);
+      }
+    }
+    for (int o = warp; o < nov; o += NW) {
+      const int4 d = ovt[o];
+      float2 acc = make_float2(0.f, 0.f);
+      for (int e = lane; e < d.z; e += 32) {
+        const int2 en = ove[d.y - e0 + e];
+        const float w = __int_as_float(en.y);
+        acc = __ffma2_rn(make_float2(w, w), wv[en.x], acc);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+      }
+      if (lane == 0) Rc[d.x] = acc;
+    }
+    __syncthreads();   // win[slot] consumed
+  }
+}
+
+// ================================================================== K2Ta, streaming strips
+// The transposed bilinear (D2^T, reading G12) as a streaming kernel: one CTA per (strip of
+// columns, image).  The strip's union node window (one contiguous range of the adjoint S2)
+// arrives by ONE bulk copy while every thread's target records (12 bytes, coalesced, L2-
+// resident across images) are loaded into registers, so each CTA has ~60 KB in flight; then the
+// fixed-order sums are stored contiguously to Rc.  Targets with more than two entries are
+// summed by one warp each (lane-strided, fixed xor butterfly).  Deterministic, no atomics.
+// One CTA per (strip, group of k2s_ipc images): the strip's records (KR per thread) and its
+// first overflow targets (KO per warp, one entry per lane) are image-independent and loaded into
+// registers ONCE; per image only the window arrives (bulk copy, double-buffered one image ahead)
+// and the sums are stored, so the per-image critical path is one bulk copy.
+constexpr int kStripT = 256, kStripKR = 10;
+__global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
+  constexpr int T = kStripT, KR = kStripKR, NW = T / 32;
+  extern __shared__ __align__(128) float2 win[];
+  const Consts& C = P.C;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  // heavy strips (origin region: long overflow lists read from global memory) first, one image
+  // per CTA; then the others, k2s_ipc images per CTA
+  const int ngrp = (C.batch + C.k2s_ipc - 1) / C.k2s_ipc;
+  const int nhv = C.k2s_nheavy * C.batch;
+  int s, bA, bB;
+  if ((int)blockIdx.x < nhv) {
+    s = blockIdx.x / C.batch;
+    bA = C.b0 + blockIdx.x % C.batch;
+    bB = bA + 1;
+  } else {
+    const int id = blockIdx.x - nhv;
+    s = C.k2s_nheavy + id / ngrp;
+    bA = C.b0 + (id % ngrp) * C.k2s_ipc;
+    bB = min(bA + C.k2s_ipc, C.b0 + C.batch);
+  }
+  const int4 st = __ldg(&P.k2s_strip[s]);   // (window start, nodes, first target, targets)
+  const int ntg = st.w;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(win + 2 * C.k2s_wcap + kStripOvBytes / 8);
+  const size_t img = (size_t)C.half * C.NL;
+  const uint32_t* rp = P.k2s_rec + (size_t)3 * st.z;
+  uint32_t i01[KR], wa[KR], wb[KR];
+#pragma unroll
+  for (int k = 0; k < KR; ++k) {
+    const int qq = t + k * T;
+    const bool ok = qq < ntg;
+    i01[k] = ok ? __ldg(&rp[3 * qq]) : 0xFFFF0000u;   // (an absent record reads as "overflow")
+    wa[k] = ok ? __ldg(&rp[3 * qq + 1]) : 0u;
+    wb[k] = ok ? __ldg(&rp[3 * qq + 2]) : 0u;
+  }
+  // overflow lists (targets with > 2 entries): light strips stage descriptors and entries in
+  // shared memory once (image-independent); heavy strips (origin region) read global memory
+  const int2 ovr = __ldg(&P.k2s_ovr[s]);
+  const int nov = ovr.y - ovr.x;
+  const bool heavy = s < C.k2s_nheavy;
+  const int e0 = nov > 0 ? __ldg(&P.k2s_ovt[ovr.x]).y : 0;
+  const int ne = nov > 0 ? __ldg(&P.k2s_ovt[ovr.y - 1]).y + __ldg(&P.k2s_ovt[ovr.y - 1]).z - e0 : 0;
+  int4* ovt_s = reinterpret_cast<int4*>(win + 2 * C.k2s_wcap);
+  int2* ove_s = reinterpret_cast<int2*>(ovt_s + nov);
+  const int4* ovt = heavy ? P.k2s_ovt + ovr.x : ovt_s;
+  const int2* ove = heavy ? P.k2s_ov + e0 : ove_s;
+  if (!heavy) {
+    for (int i = t; i < nov; i += T) ovt_s[i] = __ldg(&P.k2s_ovt[ovr.x + i]);
+    for (int i = t; i < ne; i += T) ove_s[i] = __ldg(&P.k2s_ov[e0 + i]);
+  }
+  auto issue = [&](int b, int slot) {
+    const size_t src = (size_t)b * img + st.x;
+    const size_t s0 = src & ~(size_t)1, s1 = (src + st.y + 1) & ~(size_t)1;
+    ac::mbar_expect_tx(&bar[slot], (uint32_t)(s1 - s0) * 8);
+    ac::bulk_g2s(win + slot * C.k2s_wcap, P.S2 + s0, (uint32_t)(s1 - s0) * 8, &bar[slot]);
+  };
+  if (t == 0) {
+    ac::mbar_init(&bar[0], 1);
+    ac::mbar_init(&bar[1], 1);
+    ac::fence_mbar_init();
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (t == 0) issue(bA, 0);
+  __syncthreads();
+  for (int b = bA; b < bB; ++b) {
+    const int it = b - bA, slot = it & 1;
+    if (t == 0 && b + 1 < bB) {
+      ac::fence_proxy_async();
+      issue(b + 1, slot ^ 1);
+    }
+    ac::mbar_wait(&bar[slot], (it >> 1) & 1);
+    const float2* wv = win + slot * C.k2s_wcap + (int)(((size_t)b * img + st.x) & 1);
+    float2* Rc = P.Rc + (size_t)b * C.ntpad + st.z;
+#pragma unroll
+    for (int k = 0; k < KR; ++k) {
+      if ((i01[k] >> 16) == 0xFFFFu) continue;    // absent, or more than two entries
+      const float w0f = __uint_as_float(wa[k]), w1f = __uint_as_float(wb[k]);
+      const float2 acc = __fmul2_rn(make_float2(w0f, w0f), wv[i01[k] & 0xFFFFu]);
+      Rc[t + k * T] = __ffma2_rn(make_float2(w1f, w1f), wv[i01[k] >> 16], acc);
+    }
+    for (int q = t + KR * T; q < ntg; q += T) {   // strips with more than KR T targets
+      const uint32_t a = __ldg(&rp[3 * q]);
+      if ((a >> 16) == 0xFFFFu) continue;
+      const float w0f = __uint_as_float(__ldg(&rp[3 * q + 1])), w1f = __uint_as_float(__ldg(&rp[3 * q + 2]));
+      const float2 acc = __fmul2_rn(make_float2(w0f, w0f), wv[a & 0xFFFFu]);
+      Rc[q] = __ffma2_rn(make_float2(w1f, w1f), wv[a >> 16], acc);
+    }
+    // targets with more than two entries (deterministic fixed-order sums)
+    if (!heavy) {   // light strips: one thread per target, its entries in order, all in smem
+      for (int o = t; o < nov; o += T) {
+        const int4 d = ovt_s[o];
+        const int2* en = ove_s + (d.y - e0);
+        float w = __int_as_float(en[0].y);
+        float2 acc = __fmul2_rn(make_float2(w, w), wv[en[0].x]);
+        for (int e = 1; e < d.z; ++e) {
+          w = __int_as_float(en[e].y);
+          acc = __ffma2_rn(make_float2(w, w), wv[en[e].x], acc);
+        }
+        Rc[d.x] = acc;
+      }
+    } else {        // heavy strips (lists up to ~280): one warp per target, lane l sums the
+                    // entries l (mod 32) in order, a fixed xor butterfly combines the lanes
+      for (int o = warp; o < nov; o += NW) {
+        const int4 d = __ldg(&ovt[o]);
+        float2 acc = make_float2(0.f, 0.f);
+        for (int e = lane; e < d.z; e += 32) {
+          const int2 en = __ldg(&ove[d.y - e0 + e]);
+          const float w = __int_as_float(en.y);
+          acc = __ffma2_rn(make_float2(w, w), wv[en.x], acc);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+        }
+        if (lane == 0) Rc[d.x] = acc;
+      }
+    }
+    __syncthreads();   // win[slot] consumed
+  }
+}
+
+size_t smem_k2t_strip(const Consts& C) { return (size_t)2 * C.k2s_wcap * 8 + kStripOvBytes + 16; }
+
+cudaError_t launch_k2t_strip(const DevPlan& P, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid(C.k2s_nheavy * C.batch + (C.k2s_n - C.k2s_nheavy) * ((C.batch + C.k2s_ipc - 1) / C.k2s_ipc));
+  const cudaError_t e = launch_pdl(C.pdl, k2t_strip, grid, dim3(kStripT), smem_k2t_strip(C), s, P);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+size_t smem_k2t_sumf(const Consts& C) {
+  return (size_t)C.k2f_rcap * 12 + (size_t)2 * C.k2f_wcap * 8 + 64;
+}
+
+cudaError_t launch_k2t_sumf(const DevPlan& P, cudaStream_t s) {
+  const Consts& C = P.C;
+  const dim3 grid(C.k2f_nslow * C.batch + (C.ncols - C.k2f_nslow) * ((C.batch + C.k2f_ipc - 1) / C.k2f_ipc));
+  const cudaError_t e = launch_pdl(C.pdl, k2t_sumf, grid, dim3(kSumfT), smem_k2t_sumf(C), s, P);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 // ================================================================== K1 forward (row pairs)
 // z = f_y + i f_{y+1}; Z[p] = sum_x z[x] W_N^{p (x - n/2)} (Alg. 1 steps 1-2, the zero-extended
 // row DFT); S1[b][p][y] = (Z[p] + conj Z[-p]) / 2, S1[b][p][y+1] = (Z[p] - conj Z[-p]) / (2i)
@@ -695,6 +1148,11 @@ size_t smem_k2c_adj(const Consts& C) {
   return (size_t)Q0 * (J + 1) * 8 + (size_t)2 * C.k2c_rbuf * 8 + 64;
 }
 
+size_t smem_k2c_adjf(const Consts& C) {
+  const int Q0 = col_R(C.n) * 8, J = C.n / col_R(C.n);
+  return (size_t)Q0 * (J + 1) * 8 + (size_t)C.k2f_rcap * 12 + (size_t)2 * C.k2f_wcap * 8 + 64;
+}
+
 size_t smem_k1c(const Consts& C) {
   return (size_t)2 * (col_R(C.n) * 8) * (C.n / col_R(C.n) + 1) * 8 + (size_t)std::max(2 * kK1BoxP * 4, 2 * C.n) * 8 + 64;
 }
@@ -710,6 +1168,9 @@ static cudaError_t cfg_col() {
   SETC((k2c_fwd<n>));
   SETC((k2c_adj<n, false>));
   SETC((k2c_adj<n, true>));
+  SETC((k2c_adjf<n>));
+  SETC(k2t_sumf);
+  SETC(k2t_strip);
   SETC((k1c_fwd<n, false>));
   SETC((k1c_adj<n, false>));
   SETC((k1c_fwd<n, true>));
@@ -748,6 +1209,18 @@ cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
                               : launch_pdl(C.pdl, k2c_adj<512, false>, grid, blk, smem_k2c_adj(C), s, P);
   else e = ch ? launch_pdl(C.pdl, k2c_adj<256, true>, grid, blk, smem_k2c_adj(C), s, P)
               : launch_pdl(C.pdl, k2c_adj<256, false>, grid, blk, smem_k2c_adj(C), s, P);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_k2c_adjf(const DevPlan& P, cudaStream_t s) {
+  const Consts& C = P.C;
+  cudaError_t e = cudaSuccess;
+  const dim3 grid(C.k2f_nslow * C.batch + (C.ncols - C.k2f_nslow) * ((C.batch + C.k2f_ipc - 1) / C.k2f_ipc));
+  const dim3 blk(col_T(C.n, 8));
+  const size_t sm = smem_k2c_adjf(C);
+  if (C.n == 1024) e = launch_pdl(C.pdl, k2c_adjf<1024>, grid, blk, sm, s, P);
+  else if (C.n == 512) e = launch_pdl(C.pdl, k2c_adjf<512>, grid, blk, sm, s, P);
+  else e = launch_pdl(C.pdl, k2c_adjf<256>, grid, blk, sm, s, P);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

@@ -543,7 +543,12 @@ cudaError_t launch_k2tb(const DevPlan& P, cudaStream_t s) {   // K2Tb only (targ
 
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s, cudaEvent_t mid) {
   const Consts& C = P.C;
-  cudaError_t e = launch_k2t_sum(P, s);
+  if (C.k2f == 1) {   // fused: target sums inside the column kernel (no Rc round trip)
+    if (mid) cudaEventRecord(mid, s);
+    return launch_k2c_adjf(P, s);
+  }
+  cudaError_t e = C.k2f == 3 ? launch_k2t_strip(P, s)
+                  : C.k2f == 2 ? launch_k2t_sumf(P, s) : launch_k2t_sum(P, s);
   if (e != cudaSuccess) return e;
   if (mid) cudaEventRecord(mid, s);
   if (col_ok(C)) return launch_k2c_adj(P, s);

@@ -423,6 +423,113 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
         H.k2c_base[(size_t)p * Q0 + q0] = t;
       }
     }
+    // fused adjoint column stage (k2c_adjf): the same target records with node references
+    // relative to the column's node window (nodes with p0 in {p-1, p}, one contiguous range of
+    // the adjoint S2), 12 bytes each {i0 | i1 << 16, w0, w1}; a target with more than two
+    // entries has i1 = 0xFFFF, w0 = first index into k2f_ov, w1 = entry count (bit patterns).
+    // Each column's block starts at a multiple of 4 records (48 bytes: 16-B bulk copies).
+    H.k2f_recptr.assign(C.ncols + 1, 0);
+    H.k2f_rec.clear();
+    H.k2f_ov.clear();
+    H.k2f_ovt.clear();
+    H.k2f_ovptr.assign(1, 0);
+    bool fits = true;
+    for (int p = 0; p < C.ncols; ++p) {
+      const int wlo = H.k2_colptr[p > 0 ? p - 1 : 0], whi = H.k2_colptr[p + 1];
+      if (whi - wlo >= 0xFFFF) fits = false;
+      H.k2f_recptr[p] = (int)(H.k2f_rec.size() / 3);
+      for (int t = H.k2t_colptr[p]; t < H.k2t_colptr[p + 1]; ++t) {
+        const int e0 = H.k2t_tstart[t], e1 = H.k2t_tstart[t + 1];
+        auto rel = [&](int src) {
+          if (src < wlo || src >= whi) fits = false;
+          return (uint32_t)(src - wlo);
+        };
+        if (e1 - e0 <= 2) {
+          const int2 a = H.k2t_ent[e0];
+          const int2 c = (e1 - e0 == 2) ? H.k2t_ent[e0 + 1] : make_int2(a.x, 0);
+          H.k2f_rec.push_back(rel(a.x) | (rel(c.x) << 16));
+          H.k2f_rec.push_back((uint32_t)a.y);
+          H.k2f_rec.push_back((uint32_t)c.y);
+        } else {   // summed by one warp in the kernel's second pass (k2f_ovt)
+          H.k2f_ovt.push_back(make_int4(t - H.k2t_colptr[p], (int)H.k2f_ov.size(), e1 - e0, 0));
+          H.k2f_rec.push_back(0xFFFF0000u);
+          H.k2f_rec.push_back((uint32_t)H.k2f_ov.size());
+          H.k2f_rec.push_back((uint32_t)(e1 - e0));
+          for (int e = e0; e < e1; ++e) H.k2f_ov.push_back(make_int2((int)rel(H.k2t_ent[e].x), H.k2t_ent[e].y));
+        }
+      }
+      H.k2f_ovptr.push_back((int)H.k2f_ovt.size());
+      while ((H.k2f_rec.size() / 3) % 4) {   // pad the column block to 4 records
+        H.k2f_rec.push_back(0u);
+        H.k2f_rec.push_back(0u);
+        H.k2f_rec.push_back(0u);
+      }
+    }
+    H.k2f_recptr[C.ncols] = (int)(H.k2f_rec.size() / 3);
+    if (!fits) H.k2f_recptr.clear();   // window too large for 16-bit offsets: no fused stage
+
+    // k2t_strip (the transposed bilinear as a streaming kernel): columns grouped into strips
+    // whose union node window (p0 in [P0-1, P1-1]) and target count stay under kStripNodes /
+    // kStripTargets; records {i0 | i1 << 16, w0, w1} relative to the strip's window; targets with
+    // more than two entries: i1 = 0xFFFF, w0 = index into k2s_ovt (summed by one warp each)
+    H.k2s_strip.clear();
+    H.k2s_rec.clear();
+    H.k2s_ovt.clear();
+    H.k2s_ov.clear();
+    H.k2s_ovptr.assign(1, 0);
+    bool sfits = true;
+    for (int P0 = 0; P0 < C.ncols;) {
+      const int wlo = H.k2_colptr[P0 > 0 ? P0 - 1 : 0];
+      int P1 = P0 + 1;
+      while (P1 < C.ncols && H.k2_colptr[P1 + 1] - wlo <= kStripNodes &&
+             H.k2t_colptr[P1 + 1] - H.k2t_colptr[P0] <= kStripTargets)
+        ++P1;
+      const int whi = H.k2_colptr[P1];
+      if (whi - wlo >= 0xFFFF) sfits = false;   // 16-bit window offsets
+      const int ta = H.k2t_colptr[P0], tb2 = H.k2t_colptr[P1];
+      H.k2s_strip.push_back(make_int4(wlo, whi - wlo, ta, tb2 - ta));
+      for (int t = ta; t < tb2; ++t) {
+        const int e0 = H.k2t_tstart[t], e1 = H.k2t_tstart[t + 1];
+        auto rel = [&](int src) { return (uint32_t)(src - wlo); };
+        if (e1 - e0 <= 2) {
+          const int2 a = H.k2t_ent[e0];
+          const int2 c = (e1 - e0 == 2) ? H.k2t_ent[e0 + 1] : make_int2(a.x, 0);
+          H.k2s_rec.push_back(rel(a.x) | (rel(c.x) << 16));
+          H.k2s_rec.push_back((uint32_t)a.y);
+          H.k2s_rec.push_back((uint32_t)c.y);
+        } else {
+          H.k2s_rec.push_back(0xFFFF0000u);
+          H.k2s_rec.push_back((uint32_t)H.k2s_ovt.size());
+          H.k2s_rec.push_back((uint32_t)(e1 - e0));
+          H.k2s_ovt.push_back(make_int4(t - ta, (int)H.k2s_ov.size(), e1 - e0, 0));
+          for (int e = e0; e < e1; ++e) H.k2s_ov.push_back(make_int2((int)rel(H.k2t_ent[e].x), H.k2t_ent[e].y));
+        }
+      }
+      H.k2s_ovptr.push_back((int)H.k2s_ovt.size());
+      P0 = P1;
+    }
+    if (!sfits) H.k2s_strip.clear();
+    // heavy strips (more overflow targets than the warps keep in registers, or lists longer
+    // than 32 entries: the origin region) first, so that they run one image per CTA at the
+    // head of the grid; every strip carries its own overflow range (k2s_ovr)
+    {
+      std::vector<int> heavy, light;
+      const int ns = (int)H.k2s_strip.size();
+      for (int s = 0; s < ns; ++s) {
+        size_t bytes = 0;   // overflow descriptors + entries, staged in shared memory
+        for (int o = H.k2s_ovptr[s]; o < H.k2s_ovptr[s + 1]; ++o) bytes += 16 + 8 * (size_t)H.k2s_ovt[o].z;
+        (bytes > (size_t)kStripOvBytes ? heavy : light).push_back(s);
+      }
+      std::vector<int4> st;
+      H.k2s_ovr.clear();
+      for (int pass = 0; pass < 2; ++pass)
+        for (int s : pass ? light : heavy) {
+          st.push_back(H.k2s_strip[s]);
+          H.k2s_ovr.push_back(make_int2(H.k2s_ovptr[s], H.k2s_ovptr[s + 1]));
+        }
+      H.k2s_strip.swap(st);
+      H.k2s_nheavy = (int)heavy.size();
+    }
   }
 }
 

@@ -134,7 +134,7 @@ static void fill_info(const Consts& C, tat_plan_info_t* o) {
   o->L = C.Lbox; o->T_new = C.T_new; o->dxi = C.dxi; o->dlam = C.dlam; o->omega = C.omega;
   o->dt = C.dt; o->h = C.h; o->wJ = C.wJ;
   o->launches_forward = kLaunchesForward;
-  o->launches_adjoint = kLaunchesAdjoint;
+  o->launches_adjoint = kLaunchesAdjoint - (C.k2f == 1 ? 1 : 0);   // fused K2T: one kernel
   o->n_targets = C.ntargets;
 }
 
@@ -249,6 +249,83 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     }
     if ((e = alloc_ws(p, B * (size_t)P.C.ntpad * sizeof(float2) + 16, &d)) != cudaSuccess) break;
     P.Rc = (float2*)d;
+    // fused adjoint column stage (k2c_adjf): shared-memory caps for a column's records and one
+    // image's node window, the largest over the columns p >= 2 (the origin columns 0 and 1 are
+    // 2-3x larger and read global memory), shrunk until 3 CTAs fit per SM (n <= 512)
+    // adjoint column stage variant (Consts::k2f); TAT_K2F=0/1/2 overrides (debugging, tuning)
+    const char* k2f_env = getenv("TAT_K2F");
+    const int k2f_mode = k2f_env ? atoi(k2f_env) : 3;
+    if (col_ok(P.C) && !H.k2s_strip.empty() && k2f_mode == 3) {   // k2t_strip + k2c_adj
+      int wmax = 2;
+      for (const int4& s4 : H.k2s_strip) wmax = std::max(wmax, s4.y + 2);
+      P.C.k2s_n = (int)H.k2s_strip.size();
+      P.C.k2s_wcap = (wmax + 1) & ~1;
+      const char* sipc = getenv("TAT_K2S_IPC");   // tuning switch: images per CTA
+      P.C.k2s_ipc = std::max(1, std::min(C.batch, sipc ? atoi(sipc) : 8));
+      if (getenv("TAT_VERBOSE"))
+        fprintf(stderr, "tat: K2T mode 3 strips %d window cap %d smem %zu\n", P.C.k2s_n, P.C.k2s_wcap,
+                smem_k2t_strip(P.C));
+      if (smem_k2t_strip(P.C) <= (size_t)kSmemLimit) {
+        if ((e = upload(p, H.k2s_strip, &P.k2s_strip, tb)) != cudaSuccess) break;
+        if ((e = upload(p, H.k2s_rec, &P.k2s_rec, tb)) != cudaSuccess) break;
+        if ((e = upload(p, H.k2s_ovt, &P.k2s_ovt, tb)) != cudaSuccess) break;
+        if ((e = upload(p, H.k2s_ov, &P.k2s_ov, tb)) != cudaSuccess) break;
+        if ((e = upload(p, H.k2s_ovr, &P.k2s_ovr, tb)) != cudaSuccess) break;
+        P.C.k2s_nheavy = H.k2s_nheavy;
+        P.C.k2f = 3;
+      }
+    }
+    if (col_ok(P.C) && !H.k2f_recptr.empty() && (k2f_mode == 1 || k2f_mode == 2)) {
+      const int Q0 = col_R(C.n) * 8, Jc = C.n / col_R(C.n);
+      int rcap = 4, wcap = 2, tmax = 0;
+      for (int q = 0; q < C.ncols; ++q) {
+        tmax = std::max(tmax, H.k2t_colptr[q + 1] - H.k2t_colptr[q]);
+        if (q < 2) continue;
+        int nb = 12 * (H.k2f_recptr[q + 1] - H.k2f_recptr[q]);   // records + overflow lists
+        for (int o = H.k2f_ovptr[q]; o < H.k2f_ovptr[q + 1]; ++o) nb += 16 + 8 * H.k2f_ovt[o].z;
+        rcap = std::max(rcap, (nb + 11) / 12);
+        wcap = std::max(wcap, H.k2_colptr[q + 1] - H.k2_colptr[q - 1] + 2);
+      }
+      if (k2f_mode == 2 || tmax <= Q0 * (Jc + 1)) {   // fused: the target sums alias the column buffer
+        P.C.k2f_rcap = (rcap + 3) & ~3;
+        P.C.k2f_wcap = (wcap + 1) & ~1;
+        // fused: 3 CTAs of 128 threads per SM (n <= 512); k2t_sumf: 4 CTAs of 256 threads
+        const size_t budget = k2f_mode == 2 ? (size_t)55 * 1024
+                              : C.n >= 1024 ? (size_t)kSmemLimit : (size_t)74 * 1024;
+        auto need = [&]() { return k2f_mode == 2 ? smem_k2t_sumf(P.C) : smem_k2c_adjf(P.C); };
+        while (need() > budget && P.C.k2f_rcap > 4) {
+          P.C.k2f_rcap = std::max(4, (P.C.k2f_rcap * 15 / 16) & ~3);
+          P.C.k2f_wcap = std::max(2, (P.C.k2f_wcap * 15 / 16) & ~1);
+        }
+        const char* ipc = getenv("TAT_K2F_IPC");   // tuning switch: images per CTA
+        P.C.k2f_ipc = std::max(1, std::min(C.batch, ipc ? atoi(ipc) : 8));
+        // slow columns (records + overflow lists over the record cap, or the window over its
+        // cap: the origin region) run one image per CTA at the head of the grid, reading global
+        // memory; the others k2f_ipc images per CTA with the column constants staged once
+        std::vector<int> cols, slow;
+        for (int q = 0; q < C.ncols; ++q) {
+          size_t bytes = (size_t)12 * (H.k2f_recptr[q + 1] - H.k2f_recptr[q]);
+          for (int o = H.k2f_ovptr[q]; o < H.k2f_ovptr[q + 1]; ++o) bytes += 16 + 8 * (size_t)H.k2f_ovt[o].z;
+          const bool sl = bytes > (size_t)12 * P.C.k2f_rcap ||
+                          H.k2_colptr[q + 1] - H.k2_colptr[q > 0 ? q - 1 : 0] + 2 > P.C.k2f_wcap;
+          (sl ? slow : cols).push_back(q);
+        }
+        P.C.k2f_nslow = (int)slow.size();
+        if (getenv("TAT_VERBOSE"))
+          fprintf(stderr, "tat: K2T mode %d rcap %d wcap %d smem %zu ipc %d slow columns %d of %d\n",
+                  k2f_mode, P.C.k2f_rcap, P.C.k2f_wcap, need(), P.C.k2f_ipc, P.C.k2f_nslow, C.ncols);
+        cols.insert(cols.begin(), slow.begin(), slow.end());
+        if (need() <= (size_t)kSmemLimit) {
+          if ((e = upload(p, cols, &P.k2f_cols, tb)) != cudaSuccess) break;
+          if ((e = upload(p, H.k2f_rec, &P.k2f_rec, tb)) != cudaSuccess) break;
+          if ((e = upload(p, H.k2f_recptr, &P.k2f_recptr, tb)) != cudaSuccess) break;
+          if ((e = upload(p, H.k2f_ov, &P.k2f_ov, tb)) != cudaSuccess) break;
+          if ((e = upload(p, H.k2f_ovt, &P.k2f_ovt, tb)) != cudaSuccess) break;
+          if ((e = upload(p, H.k2f_ovptr, &P.k2f_ovptr, tb)) != cudaSuccess) break;
+          P.C.k2f = k2f_mode == 1 ? 1 : 2;
+        }
+      }
+    }
     e = configure_kernels(P);
     if (e == cudaSuccess) e = make_s1_tensor_map(P, &p->tm_s1);
   } while (false);

@@ -39,7 +39,18 @@ struct Consts {
   int ntpad = 0;    // per-image stride of Rc (ntargets rounded up to even: 16-B bulk copies)
   int k2c_rbuf = 0; // k2c_adj: entries per column target buffer (max targets per column + 2)
   int k2t_win = 0;  // k2t_sum: max nodes with p0 in {p-1, p} over columns p
-};  // plain data: passed by value to kernels inside DevPlan
+  int k2f = 0;      // adjoint column stage: 0 k2t_sum + k2c_adj; 1 fused k2c_adjf;
+                    // 2 k2t_sumf (multi-image target sums on k2c_adjf's tables) + k2c_adj
+  int k2f_rcap = 0; // k2c_adjf: shared-memory capacity for a column's records (multiple of 4)
+  int k2f_wcap = 0; // ... and for one image's node window (even); larger columns read global
+  int k2f_ipc = 0;  // ... images per CTA (the records of a column are staged once per CTA)
+  int k2f_nslow = 0; // ... columns run from global memory, one image per CTA (k2f_cols head)
+  int k2s_n = 0;     // k2t_strip: number of strips; k2s_wcap: largest strip window (nodes, even)
+  int k2s_wcap = 0;
+  int k2s_ipc = 0;   // k2t_strip: images per CTA (the strip's records stay in registers)
+  int k2s_nheavy = 0; // k2t_strip: leading heavy strips, one image per CTA
+};
+
 
 // Host-side tables (float64 built, float32/int stored), uploaded by tat_plan_create.
 struct HostTables {
@@ -72,7 +83,25 @@ struct HostTables {
   // and the index of the first such target (targets of a column are ordered by (q0, q1))
   std::vector<uint32_t> k2c_mask;   // [ncols][16L] (only when col_ok)
   std::vector<int> k2c_base;        // [ncols][16L]
+  // k2c_adjf (fused adjoint column stage): window-relative target records, 3 words each
+  std::vector<uint32_t> k2f_rec;    // {i0 | i1 << 16, w0 bits, w1 bits}, column blocks padded to 4
+  std::vector<int> k2f_recptr;      // [ncols + 1] first record of each column (empty: not fused)
+  std::vector<int2> k2f_ov;         // overflow entries (window offset, w bits)
+  std::vector<int4> k2f_ovt;        // targets with > 2 entries: (index in column, first entry, count, 0)
+  std::vector<int> k2f_ovptr;       // [ncols + 1] into k2f_ovt
+  // k2t_strip (streaming transposed bilinear): column strips (window start, window nodes,
+  // first target, targets), strip-relative records as k2f_rec, overflow lists per strip
+  std::vector<int4> k2s_strip;      // empty: not available
+  std::vector<uint32_t> k2s_rec;
+  std::vector<int4> k2s_ovt;        // (target in strip, first entry, count, 0)
+  std::vector<int2> k2s_ov;
+  std::vector<int> k2s_ovptr;       // [strips + 1] into k2s_ovt (host only, in build order)
+  std::vector<int2> k2s_ovr;        // [strips] overflow range of each strip (device order)
+  int k2s_nheavy = 0;               // heavy strips, placed first (one image per CTA)
 };
+constexpr int kStripNodes = 4096;   // k2t_strip: node-window budget of a strip (a single column may exceed it)
+constexpr int kStripTargets = 2560; // ... and its target budget
+constexpr int kStripOvBytes = 8192; // ... shared memory for a light strip's overflow lists
 
 // returns "" on success, else an error message; code receives 1 (invalid) or 2 (unsupported)
 std::string derive_consts(int n, int n_det, int n_t, double R, double c, double T, int batch,
@@ -103,6 +132,17 @@ struct DevPlan {
   const int* ring = nullptr;
   const uint32_t* k2c_mask = nullptr;
   const int* k2c_base = nullptr;
+  const uint32_t* k2f_rec = nullptr;  // fused adjoint column stage tables (HostTables)
+  const int* k2f_recptr = nullptr;
+  const int2* k2f_ov = nullptr;
+  const int4* k2f_ovt = nullptr;
+  const int* k2f_ovptr = nullptr;
+  const int* k2f_cols = nullptr;      // [ncols] column order of the grid: slow columns first
+  const int4* k2s_strip = nullptr;    // k2t_strip tables (HostTables)
+  const uint32_t* k2s_rec = nullptr;
+  const int4* k2s_ovt = nullptr;
+  const int2* k2s_ov = nullptr;
+  const int2* k2s_ovr = nullptr;
   // inverse (Alg. 3 step 5): per Cartesian target 4 polar corners (sorted node index, or
   // -(index + 1) for the conjugate mirror node) and bilinear weights
   const float2* dense_e5 = nullptr;
@@ -237,6 +277,12 @@ size_t smem_k2c_adj(const Consts& C);
 cudaError_t configure_col_kernels(const Consts& C);
 cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s);
+size_t smem_k2c_adjf(const Consts& C);
+cudaError_t launch_k2c_adjf(const DevPlan& P, cudaStream_t s);
+size_t smem_k2t_sumf(const Consts& C);
+cudaError_t launch_k2t_sumf(const DevPlan& P, cudaStream_t s);
+size_t smem_k2t_strip(const Consts& C);
+cudaError_t launch_k2t_strip(const DevPlan& P, cudaStream_t s);
 bool dct4_ok(const Consts& C);
 size_t smem_k4c(const Consts& C);
 cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s);

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtat.so")
+LIB_PATH = os.environ.get("TAT_LIB") or os.path.join(_HERE, "libtat.so")   # TAT_LIB: tuning builds
 
 TAT_OK = 0
 STATUS = {0: "TAT_OK", 1: "TAT_ERR_INVALID_ARGUMENT", 2: "TAT_ERR_UNSUPPORTED_GEOMETRY",

@@ -325,3 +325,34 @@ def test_nan_propagates(torch_cuda):
     f[0, geo.n // 2, geo.n // 3] = np.nan
     g = _run(torch_cuda, plan, f=f)
     assert np.isnan(g).any()
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_fused_adjoint_column_stage(torch_cuda, monkeypatch, name):
+    """The adjoint column stage variants: fused (TAT_K2F=1, k2c_adjf: target sums inside the
+    column kernel) and the default multi-image target sums (k2t_sumf) + k2c_adj, both on the
+    window-relative records.  Fused k2c_adjf: records
+    staged once per column, origin columns from global memory, targets with > 2 entries summed
+    by a warp in a fixed lane/butterfly order) against the two-kernel path (TAT_K2F=0:
+    k2t_sum + k2c_adj, sequential sums): equal up to the summation order of those few targets
+    (<= 1e-6 of max|A* g|), and bitwise reproducible run to run."""
+    torch = torch_cuda
+    geo = synth.geometry(name)
+    plan = _plan(geo)
+    monkeypatch.setenv("TAT_K2F", "0")
+    plan0 = _plan(geo)
+    monkeypatch.setenv("TAT_K2F", "1")
+    plan1 = _plan(geo)
+    monkeypatch.setenv("TAT_K2F", "2")
+    plan2 = _plan(geo)
+    monkeypatch.delenv("TAT_K2F")
+    assert plan1.info["launches_adjoint"] == plan0.info["launches_adjoint"] - 1
+    g = torch.from_numpy(np.stack([synth.random_data(geo.n_t, geo.n_det, 800 + b)
+                                   for b in range(geo.batch)])).cuda()
+    u0 = plan0.adjoint(g)
+    for p in (plan, plan1, plan2):
+        u = p.adjoint(g)
+        u1 = p.adjoint(g)
+        torch.cuda.synchronize()
+        assert torch.equal(u, u1)
+        assert (u - u0).abs().max().item() <= 1e-6 * u0.abs().max().item()
