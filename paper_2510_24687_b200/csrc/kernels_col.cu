@@ -979,7 +979,17 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
 // Persistent CTAs loop over the rows (b, k); the next row is prefetched into shared memory by a
 // 1-D bulk copy while the current one is transformed, and the per-thread twiddles are loaded once.
 template <int n, bool ADJ>
-__global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : 2) k4c_dct(DevPlan P) {
+#ifndef TAT_K4_MINB
+#define TAT_K4_MINB 2
+#endif
+#ifndef TAT_K4_TWS
+#define TAT_K4_TWS 0   // output twiddles staged in smem per CTA (1) or read from L1 per output
+                       // (0; measured at C3: K4 68.3 -> 66.2 us, K4T 77.9 -> 74.8 us)
+#endif
+#ifndef TAT_K4_ALDG
+#define TAT_K4_ALDG 0  // stage-A pre-twiddles from L1 at each use (1) or in registers (0)
+#endif
+__global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : TAT_K4_MINB) k4c_dct(DevPlan P) {
   using G = ColGeo<n, 4>;
   constexpr int N4 = 4 * n;
   extern __shared__ __align__(128) float2 sm[];
@@ -994,21 +1004,29 @@ __global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : 2) k4c_dc
   float2* ibuf = sm + 3 * G::WS;
   const int U = ADJ ? NL : n_t + 1;               // output twiddle index range u in [0, U)
   float4* tws = reinterpret_cast<float4*>(ibuf + 2 * IB);   // (W^u, W^{2u}), W = W_2M
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tws + U);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tws + (TAT_K4_TWS ? U : 0));
   const long rbase = (long)C.b0 * C.Kp;   // global row of local row 0
   auto issue = [&](int r, int slot) {   // thread 0: row r -> ibuf[slot] (16-B aligned range)
     const long s0 = ((rbase + r) * cnt) & ~1L, s1 = ((rbase + r) * cnt + cnt + 1) & ~1L;
     ac::mbar_expect_tx(&bar[slot], (uint32_t)(s1 - s0) * 8);
     ac::bulk_g2s(ibuf + slot * IB, in_all + s0, (uint32_t)(s1 - s0) * 8, &bar[slot]);
   };
+#if TAT_K4_ALDG
+  // pre-twiddles read from the (L1-resident, 16 KB) table at each use instead of 2 NRES R
+  // registers per thread: the register budget of 3 CTAs per SM
+  PowR<G::R, kFactPow> pw;
+  pw.init(__ldg(&P.tw_n[j & (n - 1)]));
+#else
   float2 A[G::NRES][G::R];
   PowR<G::R, kFactPow> pw;
   col_twiddles<G>(P.tw_dct4, P.tw_n, 0, j, sg, A, pw);
-  for (int u = t; u < U; u += blockDim.x) {   // output twiddles, once per CTA
-    const int u2 = 2 * u >= M2 ? 2 * u - M2 : 2 * u;
-    const float2 a = __ldg(&P.tw_dct[u]), c = __ldg(&P.tw_dct[u2]);
-    tws[u] = make_float4(a.x, a.y, c.x, c.y);
-  }
+#endif
+  if (TAT_K4_TWS)
+    for (int u = t; u < U; u += blockDim.x) {   // output twiddles, once per CTA
+      const int u2 = 2 * u >= M2 ? 2 * u - M2 : 2 * u;
+      const float2 a = __ldg(&P.tw_dct[u]), c = __ldg(&P.tw_dct[u2]);
+      tws[u] = make_float4(a.x, a.y, c.x, c.y);
+    }
   pdl_wait();
   pdl_trigger();
   if (t == 0) {
@@ -1034,7 +1052,22 @@ __global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : 2) k4c_dc
       const int i = 3 * (j + G::J * r) + e, src = ADJ ? i - 1 : i;
       x[r] = (src >= 0 && src < cnt) ? in[src] : make_float2(0.f, 0.f);
     }
+#if TAT_K4_ALDG
+#pragma unroll
+    for (int i = 0; i < G::NRES; ++i) {
+      const int s = sg + G::NG * i;
+      float2 v[G::R];
+#pragma unroll
+      for (int r = 0; r < G::R; ++r) v[r] = cmul(x[r], __ldg(&P.tw_dct4[s * n + j + G::J * r]));
+      ce::dftr<G::R, -1>(v);
+#pragma unroll
+      for (int k1 = 1; k1 < G::R; ++k1) v[k1] = pw.mul(v[k1], k1);
+#pragma unroll
+      for (int k1 = 0; k1 < G::R; ++k1) W[G::widx(s + G::L * k1, j)] = v[k1];
+    }
+#else
     stage_a_fwd<G>(x, A, pw, W, j, sg);
+#endif
     __syncthreads();
     stage_b<G, -1>(W, tl);
     __syncthreads();
@@ -1069,9 +1102,15 @@ __global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : 2) k4c_dc
       for (int q = 0; q < U4; ++q) {
         const int o = o0 + q * blockDim.x;
         const int u = ADJ ? o : o + 1;
-        const float4 tw = o < nout ? tws[u] : make_float4(0.f, 0.f, 0.f, 0.f);
-        w1[q] = make_float2(tw.x, tw.y);
-        w2[q] = make_float2(tw.z, tw.w);
+        if (TAT_K4_TWS) {
+          const float4 tw = o < nout ? tws[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+          w1[q] = make_float2(tw.x, tw.y);
+          w2[q] = make_float2(tw.z, tw.w);
+        } else {
+          const int uu = o < nout ? u : 0, u2 = 2 * uu >= M2 ? 2 * uu - M2 : 2 * uu;
+          w1[q] = __ldg(&P.tw_dct[uu]);
+          w2[q] = __ldg(&P.tw_dct[u2]);
+        }
         ml[q] = (ADJ && o < nout) ? __ldg(&P.mult[(size_t)k * NL + o]) : 0.f;
       }
 #pragma unroll
@@ -1114,14 +1153,14 @@ size_t smem_k4c(const Consts& C) {
   const int cnt = std::max(C.NL, C.n_t);
   const int R4 = col_R(C.n), J4 = C.n / R4;
   return (size_t)3 * (R4 * 4) * (J4 + 1) * 8 + (size_t)2 * ((cnt + 3) & ~1) * 8 +
-         (size_t)std::max(C.NL, C.n_t + 1) * 16 + 64;
+         (size_t)std::max(C.NL, C.n_t + 1) * 16 * TAT_K4_TWS + 64;
 }
 
 cudaError_t launch_k4c(const DevPlan& P, bool adj, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
   const int rows = C.Kp * C.batch;
-  const dim3 grid(std::min(rows, (C.n >= 1024 ? 1 : 2) * 148));
+  const dim3 grid(std::min(rows, (C.n >= 1024 ? 1 : TAT_K4_MINB) * 148));
   const dim3 blk(3 * col_T(C.n, 4));
   const size_t sm = smem_k4c(C);
   if (C.n == 1024) {
