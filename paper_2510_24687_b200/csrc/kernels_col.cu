@@ -27,9 +27,15 @@ namespace tat {
 namespace {
 
 #ifndef TAT_FACT_POW
-#define TAT_FACT_POW 1
+#define TAT_FACT_POW 0
 #endif
-constexpr bool kFactPow = TAT_FACT_POW;   // post-twiddle powers of the stage-A jobs (PowR)
+// post-twiddle powers of the stage-A jobs (PowR): all R - 1 powers in registers (0; one complex
+// multiply per point) or factored b^(k mod 4) (b^4)^(k div 4) (1; ~1.9 multiplies per point,
+// 16 fewer registers).  Measured at C3 (round 2): full powers K2 236 -> 231 us, K2Tb 218 -> 212,
+// K4 66 -> 65, K4T 75 -> 73; C5 K2 344 -> 324, K2Tb 314 -> 296.  K1 keeps the factored powers
+// (the full ones spill there: 4 bytes at 168 registers, and K1 measured 52 -> 54 us).
+constexpr bool kFactPow = TAT_FACT_POW;
+constexpr bool kFactPowK1 = true;
 
 __host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
 
@@ -832,7 +838,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPl
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + STG);
   const float* rows = reinterpret_cast<const float*>(stg);
   float2 A[G::NRES][G::R];
-  PowR<G::R, kFactPow> pw;
+  PowR<G::R, kFactPowK1> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   pdl_wait();
   pdl_trigger();
@@ -1018,7 +1024,7 @@ __global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : TAT_K4_MI
   pw.init(__ldg(&P.tw_n[j & (n - 1)]));
 #else
   float2 A[G::NRES][G::R];
-  PowR<G::R, kFactPow> pw;
+  PowR<G::R, kFactPow || n >= 1024> pw;   // (full powers spill at n = 1024)
   col_twiddles<G>(P.tw_dct4, P.tw_n, 0, j, sg, A, pw);
 #endif
   if (TAT_K4_TWS)
