@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
   }
   const int4 st = __ldg(&P.k2s_strip[s]);   // (window start, nodes, first target, targets)
   const int ntg = st.w;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(win + 2 * C.k2s_wcap + kStripOvBytes / 8);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(win + 2 * C.k2s_wcap + C.k2s_ovcap / 8);
   const size_t img = (size_t)C.half * C.NL;
   const uint32_t* rp = P.k2s_rec + (size_t)3 * st.z;
   uint32_t i01[KR], wa[KR], wb[KR];
@@ -710,17 +710,45 @@ __global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
   // shared memory once (image-independent); heavy strips (origin region) read global memory
   const int2 ovr = __ldg(&P.k2s_ovr[s]);
   const int nov = ovr.y - ovr.x;
-  const bool heavy = s < C.k2s_nheavy;
   const int e0 = nov > 0 ? __ldg(&P.k2s_ovt[ovr.x]).y : 0;
   const int ne = nov > 0 ? __ldg(&P.k2s_ovt[ovr.y - 1]).y + __ldg(&P.k2s_ovt[ovr.y - 1]).z - e0 : 0;
+  if (s < C.k2s_nheavy) {
+    // heavy strip (origin region: node window or overflow lists over the smem budgets), one
+    // image: everything from global memory (L2); the long lists one warp per target, lane l
+    // summing the entries l (mod 32) in order, a fixed xor butterfly combining the lanes
+    pdl_wait();
+    pdl_trigger();
+    const float2* __restrict__ gw = P.S2 + (size_t)bA * img + st.x;
+    float2* Rc = P.Rc + (size_t)bA * C.ntpad + st.z;
+    for (int q = t; q < ntg; q += T) {
+      const uint32_t a = __ldg(&rp[3 * q]);
+      if ((a >> 16) == 0xFFFFu) continue;
+      const float w0f = __uint_as_float(__ldg(&rp[3 * q + 1])), w1f = __uint_as_float(__ldg(&rp[3 * q + 2]));
+      const float2 acc = __fmul2_rn(make_float2(w0f, w0f), gw[a & 0xFFFFu]);
+      Rc[q] = __ffma2_rn(make_float2(w1f, w1f), gw[a >> 16], acc);
+    }
+    for (int o = ovr.x + warp; o < ovr.y; o += NW) {
+      const int4 d = __ldg(&P.k2s_ovt[o]);
+      float2 acc = make_float2(0.f, 0.f);
+      for (int e = lane; e < d.z; e += 32) {
+        const int2 en = __ldg(&P.k2s_ov[d.y + e]);
+        const float w = __int_as_float(en.y);
+        acc = __ffma2_rn(make_float2(w, w), gw[en.x], acc);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+      }
+      if (lane == 0) Rc[d.x] = acc;
+    }
+    return;
+  }
+  // light strip: overflow descriptors and entries staged in shared memory once
   int4* ovt_s = reinterpret_cast<int4*>(win + 2 * C.k2s_wcap);
   int2* ove_s = reinterpret_cast<int2*>(ovt_s + nov);
-  const int4* ovt = heavy ? P.k2s_ovt + ovr.x : ovt_s;
-  const int2* ove = heavy ? P.k2s_ov + e0 : ove_s;
-  if (!heavy) {
-    for (int i = t; i < nov; i += T) ovt_s[i] = __ldg(&P.k2s_ovt[ovr.x + i]);
-    for (int i = t; i < ne; i += T) ove_s[i] = __ldg(&P.k2s_ov[e0 + i]);
-  }
+  for (int i = t; i < nov; i += T) ovt_s[i] = __ldg(&P.k2s_ovt[ovr.x + i]);
+  for (int i = t; i < ne; i += T) ove_s[i] = __ldg(&P.k2s_ov[e0 + i]);
   auto issue = [&](int b, int slot) {
     const size_t src = (size_t)b * img + st.x;
     const size_t s0 = src & ~(size_t)1, s1 = (src + st.y + 1) & ~(size_t)1;
@@ -759,42 +787,24 @@ __global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
       const float2 acc = __fmul2_rn(make_float2(w0f, w0f), wv[a & 0xFFFFu]);
       Rc[q] = __ffma2_rn(make_float2(w1f, w1f), wv[a >> 16], acc);
     }
-    // targets with more than two entries (deterministic fixed-order sums)
-    if (!heavy) {   // light strips: one thread per target, its entries in order, all in smem
-      for (int o = t; o < nov; o += T) {
-        const int4 d = ovt_s[o];
-        const int2* en = ove_s + (d.y - e0);
-        float w = __int_as_float(en[0].y);
-        float2 acc = __fmul2_rn(make_float2(w, w), wv[en[0].x]);
-        for (int e = 1; e < d.z; ++e) {
-          w = __int_as_float(en[e].y);
-          acc = __ffma2_rn(make_float2(w, w), wv[en[e].x], acc);
-        }
-        Rc[d.x] = acc;
+    // targets with more than two entries (deterministic fixed-order sums): one thread per
+    // target, its entries in order, all in smem
+    for (int o = t; o < nov; o += T) {
+      const int4 d = ovt_s[o];
+      const int2* en = ove_s + (d.y - e0);
+      float w = __int_as_float(en[0].y);
+      float2 acc = __fmul2_rn(make_float2(w, w), wv[en[0].x]);
+      for (int e = 1; e < d.z; ++e) {
+        w = __int_as_float(en[e].y);
+        acc = __ffma2_rn(make_float2(w, w), wv[en[e].x], acc);
       }
-    } else {        // heavy strips (lists up to ~280): one warp per target, lane l sums the
-                    // entries l (mod 32) in order, a fixed xor butterfly combines the lanes
-      for (int o = warp; o < nov; o += NW) {
-        const int4 d = __ldg(&ovt[o]);
-        float2 acc = make_float2(0.f, 0.f);
-        for (int e = lane; e < d.z; e += 32) {
-          const int2 en = __ldg(&ove[d.y - e0 + e]);
-          const float w = __int_as_float(en.y);
-          acc = __ffma2_rn(make_float2(w, w), wv[en.x], acc);
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-        }
-        if (lane == 0) Rc[d.x] = acc;
-      }
+      Rc[d.x] = acc;
     }
     __syncthreads();   // win[slot] consumed
   }
 }
 
-size_t smem_k2t_strip(const Consts& C) { return (size_t)2 * C.k2s_wcap * 8 + kStripOvBytes + 16; }
+size_t smem_k2t_strip(const Consts& C) { return (size_t)2 * C.k2s_wcap * 8 + C.k2s_ovcap + 16; }
 
 cudaError_t launch_k2t_strip(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;

@@ -477,13 +477,22 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
     H.k2s_ovt.clear();
     H.k2s_ov.clear();
     H.k2s_ovptr.assign(1, 0);
+    const long kStripOvBytes = strip_ov_bytes(C.n);
+    H.k2s_ovcap = (int)kStripOvBytes;
     bool sfits = true;
+    std::vector<long> ovb(C.ncols, 0);   // overflow-list bytes of each column (targets with > 2 entries)
+    for (int p = 0; p < C.ncols; ++p)
+      for (int t = H.k2t_colptr[p]; t < H.k2t_colptr[p + 1]; ++t) {
+        const int cnt = H.k2t_tstart[t + 1] - H.k2t_tstart[t];
+        if (cnt > 2) ovb[p] += 16 + 8L * cnt;
+      }
     for (int P0 = 0; P0 < C.ncols;) {
       const int wlo = H.k2_colptr[P0 > 0 ? P0 - 1 : 0];
       int P1 = P0 + 1;
+      long ob = ovb[P0];
       while (P1 < C.ncols && H.k2_colptr[P1 + 1] - wlo <= kStripNodes &&
-             H.k2t_colptr[P1 + 1] - H.k2t_colptr[P0] <= kStripTargets)
-        ++P1;
+             H.k2t_colptr[P1 + 1] - H.k2t_colptr[P0] <= kStripTargets && ob + ovb[P1] <= kStripOvBytes)
+        ob += ovb[P1++];
       const int whi = H.k2_colptr[P1];
       if (whi - wlo >= 0xFFFF) sfits = false;   // 16-bit window offsets
       const int ta = H.k2t_colptr[P0], tb2 = H.k2t_colptr[P1];
@@ -509,16 +518,17 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
       P0 = P1;
     }
     if (!sfits) H.k2s_strip.clear();
-    // heavy strips (more overflow targets than the warps keep in registers, or lists longer
-    // than 32 entries: the origin region) first, so that they run one image per CTA at the
-    // head of the grid; every strip carries its own overflow range (k2s_ovr)
+    // heavy strips (single origin-region columns whose overflow lists or node window exceed the
+    // shared-memory budgets) first, so that they run one image per CTA at the head of the grid
+    // and read global memory; every strip carries its own overflow range (k2s_ovr)
     {
       std::vector<int> heavy, light;
       const int ns = (int)H.k2s_strip.size();
       for (int s = 0; s < ns; ++s) {
         size_t bytes = 0;   // overflow descriptors + entries, staged in shared memory
         for (int o = H.k2s_ovptr[s]; o < H.k2s_ovptr[s + 1]; ++o) bytes += 16 + 8 * (size_t)H.k2s_ovt[o].z;
-        (bytes > (size_t)kStripOvBytes ? heavy : light).push_back(s);
+        const bool hv = bytes > (size_t)kStripOvBytes || H.k2s_strip[s].y > kStripNodes;
+        (hv ? heavy : light).push_back(s);
       }
       std::vector<int4> st;
       H.k2s_ovr.clear();

@@ -256,15 +256,16 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     const char* k2f_env = getenv("TAT_K2F");
     const int k2f_mode = k2f_env ? atoi(k2f_env) : 3;
     if (col_ok(P.C) && !H.k2s_strip.empty() && k2f_mode == 3) {   // k2t_strip + k2c_adj
-      int wmax = 2;
-      for (const int4& s4 : H.k2s_strip) wmax = std::max(wmax, s4.y + 2);
+      int wmax = 2;   // the light strips' windows are staged in smem (heavy ones read global)
+      for (size_t s = H.k2s_nheavy; s < H.k2s_strip.size(); ++s) wmax = std::max(wmax, H.k2s_strip[s].y + 2);
       P.C.k2s_n = (int)H.k2s_strip.size();
+      P.C.k2s_ovcap = H.k2s_ovcap;
       P.C.k2s_wcap = (wmax + 1) & ~1;
       const char* sipc = getenv("TAT_K2S_IPC");   // tuning switch: images per CTA
       P.C.k2s_ipc = std::max(1, std::min(C.batch, sipc ? atoi(sipc) : 8));
       if (getenv("TAT_VERBOSE"))
-        fprintf(stderr, "tat: K2T mode 3 strips %d window cap %d smem %zu\n", P.C.k2s_n, P.C.k2s_wcap,
-                smem_k2t_strip(P.C));
+        fprintf(stderr, "tat: K2T mode 3 strips %d (heavy %d) window cap %d smem %zu\n", P.C.k2s_n,
+                H.k2s_nheavy, P.C.k2s_wcap, smem_k2t_strip(P.C));
       if (smem_k2t_strip(P.C) <= (size_t)kSmemLimit) {
         if ((e = upload(p, H.k2s_strip, &P.k2s_strip, tb)) != cudaSuccess) break;
         if ((e = upload(p, H.k2s_rec, &P.k2s_rec, tb)) != cudaSuccess) break;

@@ -48,6 +48,7 @@ struct Consts {
   int k2s_n = 0;     // k2t_strip: number of strips; k2s_wcap: largest strip window (nodes, even)
   int k2s_wcap = 0;
   int k2s_ipc = 0;   // k2t_strip: images per CTA (the strip's records stay in registers)
+  int k2s_ovcap = 0; // k2t_strip: smem bytes for a light strip's overflow lists
   int k2s_nheavy = 0; // k2t_strip: leading heavy strips, one image per CTA
 };
 
@@ -98,10 +99,14 @@ struct HostTables {
   std::vector<int> k2s_ovptr;       // [strips + 1] into k2s_ovt (host only, in build order)
   std::vector<int2> k2s_ovr;        // [strips] overflow range of each strip (device order)
   int k2s_nheavy = 0;               // heavy strips, placed first (one image per CTA)
+  int k2s_ovcap = 0;                // smem budget for a light strip's overflow lists (bytes)
 };
-constexpr int kStripNodes = 4096;   // k2t_strip: node-window budget of a strip (a single column may exceed it)
+constexpr int kStripNodes = 4096;   // k2t_strip: node-window budget of a strip
 constexpr int kStripTargets = 2560; // ... and its target budget
-constexpr int kStripOvBytes = 8192; // ... shared memory for a light strip's overflow lists
+// ... and for its overflow lists (descriptors + entries, staged in smem); measured at C3 / C5:
+// 8 KB -> K2Ta 93 / 142 us, 16 KB -> 65.5 / 93, 24 KB -> 68.6 / 81 (fewer heavy strips vs
+// occupancy)
+inline int strip_ov_bytes(int n) { return n >= 1024 ? 24576 : 16384; }
 
 // returns "" on success, else an error message; code receives 1 (invalid) or 2 (unsupported)
 std::string derive_consts(int n, int n_det, int n_t, double R, double c, double T, int batch,
