@@ -262,7 +262,10 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
       P.C.k2s_ovcap = H.k2s_ovcap;
       P.C.k2s_wcap = (wmax + 1) & ~1;
       const char* sipc = getenv("TAT_K2S_IPC");   // tuning switch: images per CTA
-      P.C.k2s_ipc = std::max(1, std::min(C.batch, sipc ? atoi(sipc) : 8));
+      // images per CTA: about 4.5 waves of (3 CTAs x 148 SMs) over the light strips (measured at
+      // C3: 4 -> 54.5 us, 8 -> 66, 16 -> 110; at C4 8 -> 45, 4 -> 48)
+      const int ipc_auto = (int)std::lround((double)(P.C.k2s_n - H.k2s_nheavy) * C.batch / 2000.0);
+      P.C.k2s_ipc = std::max(1, std::min(C.batch, sipc ? atoi(sipc) : ipc_auto));
       if (getenv("TAT_VERBOSE"))
         fprintf(stderr, "tat: K2T mode 3 strips %d (heavy %d) window cap %d smem %zu\n", P.C.k2s_n,
                 H.k2s_nheavy, P.C.k2s_wcap, smem_k2t_strip(P.C));

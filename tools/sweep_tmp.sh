@@ -1,5 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/sweep18_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/sweep18_pytest.log
-for c in C3 C5 C4; do
-  TAT_VERBOSE=1 python tools/time_stages.py $c 20 2>&1 | tail -2 >> gpurun_out/sweep18.txt
+for v in "TAT_K2S_IPC=4" "TAT_K2S_IPC=8" "TAT_K2S_IPC=16"; do
+  for c in C3 C5 C4; do
+    env $v python tools/time_stages.py $c 20 2>&1 | tail -1 | sed "s|^|$v |" >> gpurun_out/sweep19.txt
+  done
 done
