@@ -1084,7 +1084,8 @@ __global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : TAT_K4_MI
 #else
     stage_a_fwd<G>(x, A, pw, W, j, sg);
 #endif
-    __syncthreads();
+    // stage B of group e reads only group e's buffer: a named barrier of its G::T threads
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + e), "r"(G::T) : "memory");
     stage_b<G, -1>(W, tl);
     __syncthreads();
     // S(u) = X(u) + X(-u) = sum_e [W^{eu} Y_e(u) + conj(W^{eu}) Y_e(-u)], W = W_2M, 0 <= u < 4n;
