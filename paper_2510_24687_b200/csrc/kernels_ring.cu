@@ -46,19 +46,23 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
   constexpr int rs = rstride(nf);
   constexpr int T = G * nf / 8, Kp = nf / 2 + 1, half = nf / 2;
   constexpr int NIN = half * G / T;                      // = 4
-  constexpr int NOUT = (Kp * 2 * G + T - 1) / T;         // <= 9
+  constexpr int NOUT = (Kp * G + T - 1) / T;             // <= 5 items (k, ring pair)
   const Consts& C = P.C;
   const int NL = C.NL;
   const int b = C.b0 + blockIdx.y, j0 = blockIdx.x * (2 * G);
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S2 = P.S2 + (size_t)b * half * NL;
-  float mo[NOUT];   // multiplier values of the output phase, loaded early
+  // output item (k, gg): both rings of transform gg at harmonic k (one pair of reads of the
+  // spectrum for the two outputs); multiplier values loaded early
+  float2 mo[NOUT];
 #pragma unroll
   for (int u = 0; u < NOUT; ++u) {
     const int idx = threadIdx.x + u * T;
-    const int k = idx / (2 * G), j = j0 + (idx - k * (2 * G));
-    mo[u] = (idx < Kp * 2 * G && j < NL) ? __ldg(&P.mult[(size_t)k * NL + j]) : 0.f;
+    const int k = idx / G, ja = j0 + 2 * (idx - k * G);
+    const bool ok = idx < Kp * G;
+    mo[u] = make_float2((ok && ja < NL) ? __ldg(&P.mult[(size_t)k * NL + ja]) : 0.f,
+                        (ok && ja + 1 < NL) ? __ldg(&P.mult[(size_t)k * NL + ja + 1]) : 0.f);
   }
   pdl_wait();
   pdl_trigger();
@@ -84,16 +88,17 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
 #pragma unroll
   for (int u = 0; u < NOUT; ++u) {
     const int idx = threadIdx.x + u * T;
-    const int k = idx / (2 * G), jj = idx - k * (2 * G), j = j0 + jj;
-    if (idx < Kp * 2 * G && j < NL) {
-      const int gg = jj >> 1;
+    const int k = idx / G, gg = idx - k * G, ja = j0 + 2 * gg;
+    if (idx < Kp * G && ja < NL) {
       const float2 zk = X[gg * rs + phys(k)];
       float2 zm = X[gg * rs + phys((nf - k) & (nf - 1))];
       if (k & 1) zm = make_float2(-zm.x, -zm.y);
       // F1 = (zk + conj zm)/2 ; F2 = (zk - conj zm)/(2i)
-      const float2 F = (jj & 1) ? make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x))
-                                : make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
-      S3[(size_t)k * NL + j] = mul_ipow_(cscale(F, mo[u]), k);
+      const float2 F1 = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+      const float2 F2 = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+      float2* o = S3 + (size_t)k * NL + ja;
+      o[0] = mul_ipow_(cscale(F1, mo[u].x), k);
+      if (ja + 1 < NL) o[1] = mul_ipow_(cscale(F2, mo[u].y), k);
     }
   }
 }
@@ -140,27 +145,29 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
       }
     }
   }
-  int perm[NOUT];   // output node positions, loaded before the transform (latency hidden)
+  // output item (gg, lp): both rings of transform gg at half-plane angle lp (one pair of reads
+  // of the transform for the two nodes); node positions loaded before the transform
+  constexpr int NOUT2 = NOUT / 2;
+  int2 perm[NOUT2];
 #pragma unroll
-  for (int u = 0; u < NOUT; ++u) {
+  for (int u = 0; u < NOUT2; ++u) {
     const int idx = threadIdx.x + u * T;
-    const int jj = idx / half, lp = idx - jj * half, j = j0 + jj;
-    perm[u] = j < NL ? __ldg(&P.node_perm[(size_t)j * half + lp]) : 0;
+    const int gg = idx / half, lp = idx - gg * half, ja = j0 + 2 * gg;
+    perm[u] = make_int2(ja < NL ? __ldg(&P.node_perm[(size_t)ja * half + lp]) : 0,
+                        ja + 1 < NL ? __ldg(&P.node_perm[(size_t)(ja + 1) * half + lp]) : 0);
   }
   const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
   float2* S2 = P.S2 + (size_t)b * half * NL;
 #pragma unroll
-  for (int u = 0; u < NOUT; ++u) {
+  for (int u = 0; u < NOUT2; ++u) {
     const int idx = threadIdx.x + u * T;
-    const int jj = idx / half, lp = idx - jj * half, j = j0 + jj;
-    if (j < NL) {
-      const int gg = jj >> 1;
+    const int gg = idx / half, lp = idx - gg * half, ja = j0 + 2 * gg;
+    if (ja < NL) {
       const int l = (lp - nf / 4) & (nf - 1);
       const float2 z = X[gg * rs + phys(l)];
       const float2 zh = X[gg * rs + phys((l + half) & (nf - 1))];
-      const float2 Pv = (jj & 1) ? make_float2(0.5f * (z.y + zh.y), -0.5f * (z.x - zh.x))
-                                 : make_float2(0.5f * (z.x + zh.x), 0.5f * (z.y - zh.y));
-      S2[perm[u]] = Pv;   // adjoint S2: node order
+      S2[perm[u].x] = make_float2(0.5f * (z.x + zh.x), 0.5f * (z.y - zh.y));   // adjoint S2: node order
+      if (ja + 1 < NL) S2[perm[u].y] = make_float2(0.5f * (z.y + zh.y), -0.5f * (z.x - zh.x));
     }
   }
 }
@@ -213,11 +220,12 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
     const int pos = phys(__ldg(&P.ring[d]));
     const size_t i0 = ((size_t)b * n_t + t0) * n_det + d;
 #pragma unroll
-    for (int tt = 0; tt < 2 * G; ++tt) {
-      if (tt < tt_n) {
-        const float2 z = X[(tt >> 1) * rs + pos];
-        const size_t i = i0 + (size_t)tt * n_det;
-        gout[i] = epi_fwd<VAR>(P, i, (tt & 1) ? z.y : z.x);
+    for (int gg = 0; gg < G; ++gg) {   // transform gg: samples 2 gg (real part), 2 gg + 1 (imag)
+      if (2 * gg < tt_n) {
+        const float2 z = X[gg * rs + pos];
+        const size_t i = i0 + (size_t)(2 * gg) * n_det;
+        gout[i] = epi_fwd<VAR>(P, i, z.x);
+        if (2 * gg + 1 < tt_n) gout[i + n_det] = epi_fwd<VAR>(P, i + n_det, z.y);
       }
     }
   }
@@ -241,16 +249,16 @@ __global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restri
   pdl_wait();
   pdl_trigger();
   __syncthreads();
-  float* Af = reinterpret_cast<float*>(A);
-  // detector-major (no integer division): thread d places the 2G samples of detector d
+  // detector-major (no integer division): thread d places the 2G samples of detector d, the
+  // pair (2 gg, 2 gg + 1) as transform gg's (real, imag) at ring position r_d
   for (int d = threadIdx.x; d < n_det; d += blockDim.x) {
-    const int pos = 2 * phys(__ldg(&P.ring[d]));
+    const int pos = phys(__ldg(&P.ring[d]));
     const float* gi = gin + ((size_t)b * n_t + t0) * n_det + d;
     float gv[2 * G];
 #pragma unroll
     for (int tt = 0; tt < 2 * G; ++tt) gv[tt] = tt < tt_n ? gi[(size_t)tt * n_det] : 0.f;
 #pragma unroll
-    for (int tt = 0; tt < 2 * G; ++tt) Af[2 * (tt >> 1) * rs + pos + (tt & 1)] = gv[tt];
+    for (int gg = 0; gg < G; ++gg) A[gg * rs + pos] = make_float2(gv[2 * gg], gv[2 * gg + 1]);
   }
   const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
   float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
