@@ -15,6 +15,11 @@
 #include "tat_internal.h"
 
 namespace tat {
+#ifdef TAT_RING_NOFFT   // timing experiment only: skip the transform (wrong results)
+#define TAT_RING_FFT(nf, S) (__syncthreads(), A)
+#else
+#define TAT_RING_FFT(nf, S) cta_fft_g<nf, S>(A, B, P.tw_ring)
+#endif
 
 using namespace fe;
 
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
     A[gg * rs + phys(l)] = make_float2(va[u].x - vb[u].y, va[u].y + vb[u].x);   // va + i vb
     A[gg * rs + phys((l + half) & (nf - 1))] = make_float2(va[u].x + vb[u].y, -va[u].y + vb[u].x);
   }
-  const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
+  const float2* X = TAT_RING_FFT(nf, -1);
   float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
 #pragma unroll
   for (int u = 0; u < NOUT; ++u) {
@@ -145,29 +150,29 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
       }
     }
   }
-  // output item (gg, lp): both rings of transform gg at half-plane angle lp (one pair of reads
-  // of the transform for the two nodes); node positions loaded before the transform
-  constexpr int NOUT2 = NOUT / 2;
-  int2 perm[NOUT2];
+  // outputs in adjoint-S2 order (k3t_dst: this ring group's nodes sorted by position, ring-major
+  // runs inside each column), so that consecutive threads store to consecutive positions;
+  // the (position, source) pairs are loaded before the transform
+  const int nout = min(2 * G, NL - j0) * half;
+  const int2* dst = P.k3t_dst + (size_t)j0 * half;
+  int2 dd[NOUT];
 #pragma unroll
-  for (int u = 0; u < NOUT2; ++u) {
+  for (int u = 0; u < NOUT; ++u) {
     const int idx = threadIdx.x + u * T;
-    const int gg = idx / half, lp = idx - gg * half, ja = j0 + 2 * gg;
-    perm[u] = make_int2(ja < NL ? __ldg(&P.node_perm[(size_t)ja * half + lp]) : 0,
-                        ja + 1 < NL ? __ldg(&P.node_perm[(size_t)(ja + 1) * half + lp]) : 0);
+    dd[u] = idx < nout ? __ldg(&dst[idx]) : make_int2(0, 0);
   }
-  const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
+  const float2* X = TAT_RING_FFT(nf, 1);
   float2* S2 = P.S2 + (size_t)b * half * NL;
 #pragma unroll
-  for (int u = 0; u < NOUT2; ++u) {
+  for (int u = 0; u < NOUT; ++u) {
     const int idx = threadIdx.x + u * T;
-    const int gg = idx / half, lp = idx - gg * half, ja = j0 + 2 * gg;
-    if (ja < NL) {
+    if (idx < nout) {
+      const int jj = dd[u].y >> 11, lp = dd[u].y & 2047, gg = jj >> 1;
       const int l = (lp - nf / 4) & (nf - 1);
       const float2 z = X[gg * rs + phys(l)];
       const float2 zh = X[gg * rs + phys((l + half) & (nf - 1))];
-      S2[perm[u].x] = make_float2(0.5f * (z.x + zh.x), 0.5f * (z.y - zh.y));   // adjoint S2: node order
-      if (ja + 1 < NL) S2[perm[u].y] = make_float2(0.5f * (z.y + zh.y), -0.5f * (z.x - zh.x));
+      S2[dd[u].x] = (jj & 1) ? make_float2(0.5f * (z.y + zh.y), -0.5f * (z.x - zh.x))
+                             : make_float2(0.5f * (z.x + zh.x), 0.5f * (z.y - zh.y));
     }
   }
 }
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
       }
     }
   }
-  const float2* X = cta_fft_g<nf, 1>(A, B, P.tw_ring);
+  const float2* X = TAT_RING_FFT(nf, 1);
   const int tt_n = min(2 * G, n_t - t0);
   // detector-major loop (no integer division): thread d restricts all 2G samples of detector d
   for (int d = threadIdx.x; d < n_det; d += blockDim.x) {
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restri
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) A[gg * rs + pos] = make_float2(gv[2 * gg], gv[2 * gg + 1]);
   }
-  const float2* X = cta_fft_g<nf, -1>(A, B, P.tw_ring);
+  const float2* X = TAT_RING_FFT(nf, -1);
   float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
 #pragma unroll
   for (int u = 0; u < NOUT; ++u) {

@@ -314,9 +314,9 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
       q0v[i] = (int)fv; bv[i] = v - fv;
     }
   }
-  // K2 forward: counting sort by p0, stable in (l', j).  Forward S2 is ring-major [j][l']
-  // (K2 scatters node values to ring slots, K3 reads rings); adjoint S2 is in this sorted node
-  // order (K3T scatters through node_perm, the K2T target sums read contiguous node ranges).
+  // K2 forward: counting sort by p0, then q0 (gather order).  Forward S2 is ring-major [j][l']
+  // (K2 scatters node values to ring slots, K3 reads rings); the adjoint S2 uses the same
+  // column blocks (below).
   H.k2_colptr.assign(C.ncols + 1, 0);
   for (long i = 0; i < nodes; ++i) H.k2_colptr[p0v[i] + 1]++;
   for (int p = 0; p < C.ncols; ++p) H.k2_colptr[p + 1] += H.k2_colptr[p];
@@ -343,9 +343,34 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
       e.w = fbits((float)bv[i]);
       const int sp = pos[p0v[i]]++;
       H.k2_nodes[sp] = e;
-      sorted_pos[i] = sp;
-      const int lp = (int)(i / NL), j = (int)(i % NL);
-      H.node_perm[(size_t)j * half + lp] = sp;
+    }
+  }
+  // adjoint S2 order: the same column blocks (k2_colptr), ring-major (j, then l') inside each
+  // column, so that the nodes K3T produces for one ring group land in one contiguous run per
+  // column (K3T then writes them in destination order, k3t_dst) while the K2T target sums
+  // still read one contiguous window per column / strip
+  {
+    std::vector<int> pos(H.k2_colptr.begin(), H.k2_colptr.end() - 1);
+    for (int j = 0; j < NL; ++j)
+      for (int lp = 0; lp < half; ++lp) {
+        const long i = (long)lp * NL + j;
+        sorted_pos[i] = pos[p0v[i]]++;
+        H.node_perm[(size_t)j * half + lp] = sorted_pos[i];
+      }
+  }
+  // K3T output order: per ring group of 2G rings (one K3T CTA; G = min(4096 / n_phi, 16)), its
+  // nodes sorted by adjoint position: (position, (ring in group) << 11 | l')
+  {
+    const int G2 = 2 * std::min(4096 / nphi, 16);
+    H.k3t_dst.clear();
+    H.k3t_dst.reserve(nodes);
+    for (int j0 = 0; j0 < NL; j0 += G2) {
+      const size_t base = H.k3t_dst.size();
+      for (int jj = 0; jj < G2 && j0 + jj < NL; ++jj)
+        for (int lp = 0; lp < half; ++lp)
+          H.k3t_dst.push_back(make_int2(H.node_perm[(size_t)(j0 + jj) * half + lp], (jj << 11) | lp));
+      std::sort(H.k3t_dst.begin() + base, H.k3t_dst.end(),
+                [](const int2& a, const int2& b) { return a.x < b.x; });
     }
   }
   // K2T: entries (p, q mod N, src, w) for corners with non-zero weight; group by (p, q)

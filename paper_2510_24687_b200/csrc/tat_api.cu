@@ -202,6 +202,7 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
     if ((e = upload(p, H.k2_colptr, &P.k2_colptr, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2_nodes, &P.k2_nodes, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.node_perm, &P.node_perm, tb)) != cudaSuccess) break;
+    if ((e = upload(p, H.k3t_dst, &P.k3t_dst, tb)) != cudaSuccess) break;
     p->node_perm = H.node_perm;
     if ((e = upload(p, H.k2t_colptr, &P.k2t_colptr, tb)) != cudaSuccess) break;
     if ((e = upload(p, H.k2t_tq, &P.k2t_tq, tb)) != cudaSuccess) break;

@@ -65,7 +65,8 @@ struct HostTables {
   // K2 forward gather: half-plane nodes sorted by p0
   std::vector<int> k2_colptr;       // [ncols + 1]
   std::vector<int4> k2_nodes;       // (l'*NL + j, q0, alpha bits, beta bits), sorted by p0
-  std::vector<int> node_perm;       // [NL][n_ring/2]: (j, l') -> position in the sorted order
+  std::vector<int> node_perm;       // [NL][n_ring/2]: (j, l') -> adjoint S2 position
+  std::vector<int2> k3t_dst;        // K3T: per ring group, (adjoint position, jj << 11 | l') sorted
   // K2T transposed gather: per column p, targets (q mod N) with entry ranges
   std::vector<int> k2t_colptr;      // [ncols + 1] into targets
   std::vector<int> k2t_tq;          // [T] q mod N
@@ -130,6 +131,7 @@ struct DevPlan {
   const int* k2_colptr = nullptr;
   const int4* k2_nodes = nullptr;
   const int* node_perm = nullptr;
+  const int2* k3t_dst = nullptr;
   const int* k2t_colptr = nullptr;
   const int* k2t_tq = nullptr;
   const int4* k2t_rec = nullptr;
