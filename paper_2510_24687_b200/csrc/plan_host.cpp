@@ -314,9 +314,13 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
       q0v[i] = (int)fv; bv[i] = v - fv;
     }
   }
-  // K2 forward: counting sort by p0, then q0 (gather order).  Forward S2 is ring-major [j][l']
-  // (K2 scatters node values to ring slots, K3 reads rings); the adjoint S2 uses the same
-  // column blocks (below).
+  // Node order: column blocks by p0 (k2_colptr), ring-major (j, then l') inside each column.
+  // Forward S2 is ring-major [j][l'] (K2 gathers the nodes of a column in this order, so that
+  // the nodes of one ring arc are stored to neighbouring slots; K3 reads whole rings).  The
+  // adjoint S2 is in the node order itself (node_perm: (j, l') -> position): K3T stores a ring
+  // group's nodes in destination order (k3t_dst, contiguous runs per column) and the K2T
+  // target sums read one contiguous window per column / strip.  (Measured: the forward in node
+  // order too, K3 reading through k3t_dst, was K2 -3.6 us but K3 +17.5 us at C3.)
   H.k2_colptr.assign(C.ncols + 1, 0);
   for (long i = 0; i < nodes; ++i) H.k2_colptr[p0v[i] + 1]++;
   for (int p = 0; p < C.ncols; ++p) H.k2_colptr[p + 1] += H.k2_colptr[p];
@@ -324,38 +328,19 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
   H.node_perm.assign(nodes, 0);
   std::vector<int> sorted_pos(nodes);
   {
-    // within a column, nodes are ordered by q0 so that neighbouring Cartesian targets of the
-    // transposed bilinear read neighbouring node values (L1 locality in K2Ta)
-    std::vector<long> byq(nodes);
-    {
-      std::vector<int> cq(N + 2, 0);
-      for (long i = 0; i < nodes; ++i) cq[q0v[i] + N / 2 + 1]++;
-      for (int q = 0; q <= N; ++q) cq[q + 1] += cq[q];
-      for (long i = 0; i < nodes; ++i) byq[cq[q0v[i] + N / 2]++] = i;
-    }
-    std::vector<int> pos(H.k2_colptr.begin(), H.k2_colptr.end() - 1);
-    for (long ii = 0; ii < nodes; ++ii) {
-      const long i = byq[ii];
-      int4 e;
-      e.x = (int)((i % NL) * half + i / NL);   // S2 slot, ring-major [j][l']
-      e.y = q0v[i];
-      e.z = fbits((float)av[i]);
-      e.w = fbits((float)bv[i]);
-      const int sp = pos[p0v[i]]++;
-      H.k2_nodes[sp] = e;
-    }
-  }
-  // adjoint S2 order: the same column blocks (k2_colptr), ring-major (j, then l') inside each
-  // column, so that the nodes K3T produces for one ring group land in one contiguous run per
-  // column (K3T then writes them in destination order, k3t_dst) while the K2T target sums
-  // still read one contiguous window per column / strip
-  {
     std::vector<int> pos(H.k2_colptr.begin(), H.k2_colptr.end() - 1);
     for (int j = 0; j < NL; ++j)
       for (int lp = 0; lp < half; ++lp) {
         const long i = (long)lp * NL + j;
-        sorted_pos[i] = pos[p0v[i]]++;
-        H.node_perm[(size_t)j * half + lp] = sorted_pos[i];
+        const int sp = pos[p0v[i]]++;
+        sorted_pos[i] = sp;
+        H.node_perm[(size_t)j * half + lp] = sp;
+        int4 e;
+        e.x = j * half + lp;   // forward S2 slot, ring-major [j][l']
+        e.y = q0v[i];
+        e.z = fbits((float)av[i]);
+        e.w = fbits((float)bv[i]);
+        H.k2_nodes[sp] = e;
       }
   }
   // K3T output order: per ring group of 2G rings (one K3T CTA; G = min(4096 / n_phi, 16)), its
