@@ -279,8 +279,8 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPl
   const Consts& C = P.C;
   const int t = threadIdx.x, j = t % J, sg = t / J;
   const int b = C.b0 + blockIdx.y;
-  const int P0 = blockIdx.x * C.col_strip;
-  const int Pend = min(P0 + C.col_strip, C.ncols);
+  const int P0 = blockIdx.x * C.col_strip_adj;
+  const int Pend = min(P0 + C.col_strip_adj, C.ncols);
   const int RB = C.k2c_rbuf;                                  // entries per target buffer
   float2* Wb = sm;
   float2* rbuf = sm + G::WS;
@@ -1256,7 +1256,7 @@ cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s) {
 cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
-  const dim3 grid((C.ncols + C.col_strip - 1) / C.col_strip, C.batch);
+  const dim3 grid((C.ncols + C.col_strip_adj - 1) / C.col_strip_adj, C.batch);
   const dim3 blk(col_T(C.n, 8));
   const bool ch = P.k2c_chord != nullptr;
   if (C.n == 1024) e = ch ? launch_pdl(C.pdl, k2c_adj<1024, true>, grid, blk, smem_k2c_adj(C), s, P)

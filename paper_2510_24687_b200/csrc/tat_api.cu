@@ -239,6 +239,10 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
       P.C.k2t_win = std::max(mw, 1);
       const char* pdl = getenv("TAT_PDL");   // debugging switch: TAT_PDL=0 disables PDL
       P.C.pdl = pdl ? atoi(pdl) : 1;
+      const char* sf = getenv("TAT_STRIP_FWD");   // tuning switches: columns per CTA of K2 / K2Tb
+      const char* sa = getenv("TAT_STRIP_ADJ");
+      if (sf) P.C.col_strip = std::max(2, atoi(sf));
+      if (sa) P.C.col_strip_adj = std::max(1, atoi(sa));
     }
     if ((size_t)P.C.k2t_win * 8 > 227 * 1024) {
       e = cudaErrorInvalidConfiguration;

@@ -21,8 +21,9 @@ struct Consts {
   int k5ttc_kp = 0; // dense K5T on tcgen05: n_det rounded up to kK5tcKC (0: SIMT path)
   int k5ttc_nt = 0; // its N tile (<= 256, multiple of 16) and number of N tiles over 2 (K+1)
   int k5ttc_nb = 0;
-  int col_strip = 16; // K2 / K2Tb: columns per CTA (k2c_fwd recomputes one halo column;
+  int col_strip = 16; // K2: columns per CTA (k2c_fwd recomputes one halo column;
                       // 12-16 measured best at C3, 20-32 slower)
+  int col_strip_adj = 16; // K2Tb (k2c_adj): columns per CTA
   double R = 1, c = 1, T = 1;
   double h = 0, T_new0 = 0, T_new = 0, Lbox = 0, dxi = 0, dt = 0, dlam = 0, lam_max = 0;
   double wJ = 1, omega = 0;
