@@ -229,17 +229,19 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_fwd(DevPl
       stage_a_fwd<G>(x, A, pw, Fcur, j, sg);
     }
     // first node record of this column's gather, loaded while stage B runs (after stage A, whose
-    // registers are dead by then)
+    // registers are dead by then).  (Measured: all records by cp.async into the consumed input
+    // slot instead: K2 229 -> 239 us at C3; the gather is not record-latency bound.)
     const int e0 = (p > P0) ? __ldg(&P.k2_colptr[p - 1]) : 0;
     const int e1 = (p > P0) ? __ldg(&P.k2_colptr[p]) : 0;
-    int4 nd0 = make_int4(0, 0, 0, 0);
-    if (e0 + t < e1) nd0 = __ldg(&P.k2_nodes[e0 + t]);
+    int4 nd0 = make_int4(0, 0, 0, 0), nd1 = make_int4(0, 0, 0, 0);   // (the second for columns
+    if (e0 + t < e1) nd0 = __ldg(&P.k2_nodes[e0 + t]);                // with more than T nodes)
+    if (e0 + t + G::T < e1) nd1 = __ldg(&P.k2_nodes[e0 + t + G::T]);
     __syncthreads();
     stage_b<G, -1>(Fcur, t);   // stage B (in place)
     __syncthreads();
     if (p > P0) {   // bilinear gather of the nodes with p0 = p - 1 (Alg. 1 step 3)
       int e = e0 + t;
-      int4 nd = nd0;
+      int4 nd = nd0, nn = nd1;
       while (e < e1) {
         const float a = __int_as_float(nd.z), bb = __int_as_float(nd.w);
         const int i00 = G::fq(nd.y & N1), i01 = G::fq((nd.y + 1) & N1);
@@ -248,7 +250,8 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_fwd(DevPl
         const float2 c1 = __ffma2_rn(make_float2(a, a), csub(f11, f01), f01);
         S2[nd.x] = __ffma2_rn(make_float2(bb, bb), csub(c1, c0), c0);
         e += G::T;
-        if (e < e1) nd = __ldg(&P.k2_nodes[e]);
+        nd = nn;
+        if (e + G::T < e1) nn = __ldg(&P.k2_nodes[e + G::T]);
       }
     }
     __syncthreads();

@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-for v in "TAT_STRIP_ADJ=16" "TAT_STRIP_ADJ=15" "TAT_STRIP_ADJ=12" "TAT_STRIP_ADJ=10" "TAT_STRIP_ADJ=8" "TAT_STRIP_FWD=15" "TAT_STRIP_FWD=14" "TAT_STRIP_FWD=18"; do for c in C3 C4; do
-  env $v python tools/time_stages.py $c 20 2>&1 | tail -1 | sed "s|^|$v |" >> gpurun_out/sweep28.txt
-done; done
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/sweep31_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/sweep31_pytest.log
+for c in C3 C5 C4; do
+  python tools/time_stages.py $c 20 2>&1 | tail -1 >> gpurun_out/sweep31.txt
+done
