@@ -248,7 +248,12 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_fwd(DevPl
         const float2 f00 = Fprev[i00], f01 = Fprev[i01], f10 = Fcur[i00], f11 = Fcur[i01];
         const float2 c0 = __ffma2_rn(make_float2(a, a), csub(f10, f00), f00);
         const float2 c1 = __ffma2_rn(make_float2(a, a), csub(f11, f01), f01);
+#ifndef TAT_K2_NOSTORE
         S2[nd.x] = __ffma2_rn(make_float2(bb, bb), csub(c1, c0), c0);
+#else   // timing experiment only (wrong results): the stores skipped unless impossible
+        const float2 vv = __ffma2_rn(make_float2(bb, bb), csub(c1, c0), c0);
+        if (vv.x == 1.2345e-38f) S2[nd.x] = vv;
+#endif
         e += G::T;
         nd = nn;
         if (e + G::T < e1) nn = __ldg(&P.k2_nodes[e + G::T]);

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/sweep31_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/sweep31_pytest.log
-for c in C3 C5 C4; do
-  python tools/time_stages.py $c 20 2>&1 | tail -1 >> gpurun_out/sweep31.txt
-done
+for lib in "" variants/nostore.so; do for c in C3 C5; do
+  TAT_LIB=$lib python tools/time_stages.py $c 20 2>&1 | tail -1 | sed "s|^|lib=$lib |" >> gpurun_out/sweep32.txt
+done; done
