@@ -679,7 +679,11 @@ __global__ void __launch_bounds__(kSumfT) k2t_sumf(DevPlan P) {
 // first overflow targets (KO per warp, one entry per lane) are image-independent and loaded into
 // registers ONCE; per image only the window arrives (bulk copy, double-buffered one image ahead)
 // and the sums are stored, so the per-image critical path is one bulk copy.
+#ifndef TAT_STRIP_SLOTS
+#define TAT_STRIP_SLOTS 2   // measured at C3: 2 -> K2Ta 54.7 us, 3 -> 57.8, 4 -> 65.7
+#endif
 constexpr int kStripT = 256, kStripKR = 10;
+constexpr int kStripSlots = TAT_STRIP_SLOTS;   // node-window buffers (windows in flight + 1)
 __global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
   constexpr int T = kStripT, KR = kStripKR, NW = T / 32;
   extern __shared__ __align__(128) float2 win[];
@@ -702,7 +706,7 @@ __global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
   }
   const int4 st = __ldg(&P.k2s_strip[s]);   // (window start, nodes, first target, targets)
   const int ntg = st.w;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(win + 2 * C.k2s_wcap + C.k2s_ovcap / 8);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(win + kStripSlots * C.k2s_wcap + C.k2s_ovcap / 8);
   const size_t img = (size_t)C.half * C.NL;
   const uint32_t* rp = P.k2s_rec + (size_t)3 * st.z;
   uint32_t i01[KR], wa[KR], wb[KR];
@@ -753,7 +757,7 @@ __global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
     return;
   }
   // light strip: overflow descriptors and entries staged in shared memory once
-  int4* ovt_s = reinterpret_cast<int4*>(win + 2 * C.k2s_wcap);
+  int4* ovt_s = reinterpret_cast<int4*>(win + kStripSlots * C.k2s_wcap);
   int2* ove_s = reinterpret_cast<int2*>(ovt_s + nov);
   for (int i = t; i < nov; i += T) ovt_s[i] = __ldg(&P.k2s_ovt[ovr.x + i]);
   for (int i = t; i < ne; i += T) ove_s[i] = __ldg(&P.k2s_ov[e0 + i]);
@@ -764,21 +768,21 @@ __global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
     ac::bulk_g2s(win + slot * C.k2s_wcap, P.S2 + s0, (uint32_t)(s1 - s0) * 8, &bar[slot]);
   };
   if (t == 0) {
-    ac::mbar_init(&bar[0], 1);
-    ac::mbar_init(&bar[1], 1);
+    for (int q = 0; q < kStripSlots; ++q) ac::mbar_init(&bar[q], 1);
     ac::fence_mbar_init();
   }
   pdl_wait();
   pdl_trigger();
-  if (t == 0) issue(bA, 0);
+  if (t == 0)   // windows kStripSlots - 1 images ahead
+    for (int q = 0; q < kStripSlots - 1 && bA + q < bB; ++q) issue(bA + q, q);
   __syncthreads();
   for (int b = bA; b < bB; ++b) {
-    const int it = b - bA, slot = it & 1;
-    if (t == 0 && b + 1 < bB) {
+    const int it = b - bA, slot = it % kStripSlots;
+    if (t == 0 && b + kStripSlots - 1 < bB) {   // the slot consumed in the previous iteration
       ac::fence_proxy_async();
-      issue(b + 1, slot ^ 1);
+      issue(b + kStripSlots - 1, (it + kStripSlots - 1) % kStripSlots);
     }
-    ac::mbar_wait(&bar[slot], (it >> 1) & 1);
+    ac::mbar_wait(&bar[slot], (it / kStripSlots) & 1);
     const float2* wv = win + slot * C.k2s_wcap + (int)(((size_t)b * img + st.x) & 1);
     float2* Rc = P.Rc + (size_t)b * C.ntpad + st.z;
 #pragma unroll
@@ -812,7 +816,9 @@ __global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
   }
 }
 
-size_t smem_k2t_strip(const Consts& C) { return (size_t)2 * C.k2s_wcap * 8 + C.k2s_ovcap + 16; }
+size_t smem_k2t_strip(const Consts& C) {
+  return (size_t)kStripSlots * C.k2s_wcap * 8 + C.k2s_ovcap + 8 * kStripSlots;
+}
 
 cudaError_t launch_k2t_strip(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
