@@ -180,8 +180,16 @@ __device__ __forceinline__ float2 residue_sum(const float2* W, int y) {
 }
 
 // ================================================================== forward
+#ifndef TAT_K2_3BUF
+#define TAT_K2_3BUF 0   // three column buffers at every n (default: only where occupancy is 1 anyway)
+#endif
+// Three column buffers drop the barrier between a column's gather and the next stage A.  At
+// n >= 1024 one CTA fits per SM either way and the third buffer is free (C5 K2 300 -> 290 us); at
+// n = 512 it costs the third resident CTA (C3 K2 229 -> 252 us), so two buffers there.
+__host__ __device__ constexpr int k2_bufs(int n) { return (TAT_K2_3BUF || n >= 1024) ? 3 : 2; }
 template <int n>
-__global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_fwd(DevPlan P) {
+__global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : (TAT_K2_3BUF ? 2 : 3)) k2c_fwd(DevPlan P) {
+  constexpr int kK2Bufs = k2_bufs(n);
   using G = ColGeo<n>;
   constexpr int R = G::R, J = G::J, NRES = G::NRES;
   extern __shared__ __align__(128) float2 sm[];
@@ -194,7 +202,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_fwd(DevPl
   const int plast = min(Pend, C.ncols - 1);
   float2* Fa = sm;
   float2* Fb = sm + G::WS;
-  float2* xbuf = sm + 2 * G::WS;                          // 2 x n, TMA destination
+  float2* xbuf = sm + kK2Bufs * G::WS;                    // 2 x n, TMA destination
   uint64_t* bar = reinterpret_cast<uint64_t*>(xbuf + 2 * n);
   float2 A[NRES][R];
   PowR<G::R, kFactPow> pw;
@@ -259,10 +267,16 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_fwd(DevPl
         if (e + G::T < e1) nn = __ldg(&P.k2_nodes[e + G::T]);
       }
     }
-    __syncthreads();
-    float2* tmp = Fprev;
-    Fprev = Fcur;
-    Fcur = tmp;
+    if (kK2Bufs == 2) {
+      __syncthreads();   // the next stage A overwrites Fprev
+      float2* tmp = Fprev;
+      Fprev = Fcur;
+      Fcur = tmp;
+    } else {             // three buffers: the next stage A writes the third one
+      float2* nxt = (Fcur == Fa) ? Fb : (Fcur == Fb ? sm + 2 * G::WS : Fa);
+      Fprev = Fcur;
+      Fcur = nxt;
+    }
   }
   if (Pend == C.ncols) {   // p0 = N/2: alpha == 0, only F[N/2] is used
     for (int e = P.k2_colptr[C.ncols - 1] + t; e < P.k2_colptr[C.ncols]; e += G::T) {
@@ -1213,7 +1227,7 @@ bool col_ok(const Consts& C) { return C.Lres == 8 && (C.n == 256 || C.n == 512 |
 
 size_t smem_k2c_fwd(const Consts& C) {
   const int Q0 = col_R(C.n) * 8, J = C.n / col_R(C.n);
-  return (size_t)2 * Q0 * (J + 1) * 8 + (size_t)2 * C.n * 8 + 64;
+  return (size_t)k2_bufs(C.n) * Q0 * (J + 1) * 8 + (size_t)2 * C.n * 8 + 64;
 }
 size_t smem_k2c_adj(const Consts& C) {
   const int Q0 = col_R(C.n) * 8, J = C.n / col_R(C.n);
