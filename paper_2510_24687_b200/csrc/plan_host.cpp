@@ -43,6 +43,7 @@ std::string derive_consts(int n, int n_det, int n_t, double R, double c, double 
 
   C = Consts();
   C.n = n; C.n_det = n_det; C.n_t = n_t; C.batch = batch; C.R = R; C.c = c; C.T = T;
+  if (const char* r2 = std::getenv("TAT_RING2")) C.ring2 = std::atoi(r2);   // tuning switch: 0 = Stockham ring kernels
   C.h = 2.0 / n;
   C.T_new0 = std::max(2.0 * c * T, 6.0);
   C.Lbox = std::pow(2.0, std::ceil(std::log2(C.T_new0 + 2.0) - 1e-12));
@@ -346,7 +347,7 @@ void build_tables(const Consts& C, const std::vector<int>& ring, const double* a
   // K3T output order: per ring group of 2G rings (one K3T CTA; G = min(4096 / n_phi, 16)), its
   // nodes sorted by adjoint position: (position, (ring in group) << 11 | l')
   {
-    const int G2 = 2 * std::min(4096 / nphi, 16);
+    const int G2 = k3t_group_rings(C);
     H.k3t_dst.clear();
     H.k3t_dst.reserve(nodes);
     for (int j0 = 0; j0 < NL; j0 += G2) {

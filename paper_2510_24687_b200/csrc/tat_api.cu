@@ -242,8 +242,7 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
       const char* sf = getenv("TAT_STRIP_FWD");   // tuning switches: columns per CTA of K2 / K2Tb
       const char* sa = getenv("TAT_STRIP_ADJ");
       if (sf) P.C.col_strip = std::max(2, atoi(sf));
-      if (sa) P.C.col_strip_adj = std::max(1, atoi(sa));
-    }
+      if (sa) P.C.col_strip_adj = std::max(1, atoi(sa));    }
     if ((size_t)P.C.k2t_win * 8 > 227 * 1024) {
       e = cudaErrorInvalidConfiguration;
       break;

@@ -1,6 +1,7 @@
 // Internal declarations shared by the host plan builder and the sm_100a kernels.
 // Nothing here is part of the public ABI (see include/tat.h).
 #pragma once
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
 #include <string>
@@ -24,6 +25,8 @@ struct Consts {
   int col_strip = 16; // K2: columns per CTA (k2c_fwd recomputes one halo column;
                       // 12-16 measured best at C3, 20-32 slower)
   int col_strip_adj = 16; // K2Tb (k2c_adj): columns per CTA
+  int ring2 = 11;   // n_ring = 512: two-stage ring kernels instead of the Stockham ones (bits: ring2_on;
+                    // K5 keeps the Stockham kernel: 22.5 vs 22.7 us at C3)
   double R = 1, c = 1, T = 1;
   double h = 0, T_new0 = 0, T_new = 0, Lbox = 0, dxi = 0, dt = 0, dlam = 0, lam_max = 0;
   double wJ = 1, omega = 0;
@@ -109,6 +112,13 @@ constexpr int kStripTargets = 2560; // ... and its target budget
 // 8 KB -> K2Ta 93 / 142 us, 16 KB -> 65.5 / 93, 24 KB -> 68.6 / 81 (fewer heavy strips vs
 // occupancy)
 inline int strip_ov_bytes(int n) { return n >= 1024 ? 24576 : 16384; }
+// two-stage ring kernels (n_ring = 512): ring pairs per CTA; rings per K3T CTA (k3t_dst groups)
+constexpr int kRing2G = 16;
+// C.ring2 bits: 1 K3, 2 K3T, 4 K5, 8 K5T
+inline bool ring2_on(const Consts& C, int bit) { return (C.ring2 & bit) && C.n_ring == 512; }
+inline int k3t_group_rings(const Consts& C) {
+  return ring2_on(C, 2) ? 2 * kRing2G : 2 * std::min(4096 / C.n_ring, 16);
+}
 
 // returns "" on success, else an error message; code receives 1 (invalid) or 2 (unsupported)
 std::string derive_consts(int n, int n_det, int n_t, double R, double c, double T, int batch,
