@@ -12,7 +12,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libtat.so")
-SOURCES = ["tat_api.cu", "kernels.cu", "kernels_fft.cu", "kernels_ring.cu", "kernels_dct.cu",
+SOURCES = ["tat_api.cu", "kernels.cu", "kernels_fft.cu", "kernels_ring.cu", "kernels_ring2.cu", "kernels_dct.cu",
            "kernels_col.cu", "kernels_util.cu", "kernels_inv.cu", "kernels_dense.cu",
            "plan_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

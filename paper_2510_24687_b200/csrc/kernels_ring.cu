@@ -11,7 +11,6 @@
 //
 // Each CTA stages its tile through shared memory so that every global access is a contiguous
 // run along the fastest axis, then runs G transforms with cta_fft (G = blockDim.x / (n_phi/8)).
-#include "col_engine.cuh"
 #include "fft_engine.cuh"
 #include "tat_internal.h"
 
@@ -36,11 +35,6 @@ __device__ __forceinline__ float2 mul_ipow_(float2 a, int e) {
     case 2: return make_float2(-a.x, -a.y);
     default: return make_float2(a.y, -a.x);
   }
-}
-// i^e m a without branches (e varies across the lanes of a warp): the sign of i^e folded into m
-__device__ __forceinline__ float2 ipow_scale(float2 a, float m, int e) {
-  const float2 r = (e & 1) ? make_float2(-a.y, a.x) : a;
-  return cscale(r, (e & 2) ? -m : m);
 }
 
 // Global loads of each phase are issued together (unrolled item loops, registers) before any
@@ -111,230 +105,6 @@ __global__ void __launch_bounds__(512) k3_ring(DevPlan P) {
       o[0] = mul_ipow_(cscale(F1, mo[u].x), k);   // (measured: ipow_scale here 37.3 -> 39.1 us at C4)
       if (ja + 1 < NL) o[1] = mul_ipow_(cscale(F2, mo[u].y), k);
     }
-  }
-}
-
-// ------------------------------------------------------------------ K3, two-stage (n_phi = 512)
-// The same transform as k3_ring with one shared-memory crossing per point instead of a Stockham
-// pass per radix-8 level: l = j + 16 r, k = k1 + 32 k2,
-//   Z[k1 + 32 k2] = sum_j W_16^{j k2} W_512^{j k1} sum_r z[j + 16 r] W_32^{r k1}.
-// Stage A (thread (j, gg)): the 16 half-plane samples j + 16 m of both rings of ring pair gg are
-// loaded straight from S2 into registers (coalesced: consecutive j, consecutive l'); each gives
-// two points of the completed ring (l and l + 256, the second conjugated); 32-point DFT over r,
-// twiddle W_512^{j k1}, one store per point.  Stage B (thread (kp, gg)): the two 16-point DFTs over
-// j of k1 = kp and k1 = 32 - kp (kp = 0: k1 = 0 and 16), so that Z[k] and Z[-k] -- both needed
-// to separate the two rings -- are in the same thread; outputs stored straight to S3 (the
-// threads of one kp cover 2G consecutive rings: contiguous runs of S3 row k).
-namespace {
-constexpr int kR2G = kRing2G;                       // ring pairs per CTA (32 rings)
-constexpr int kR2P = 33;                            // Y row stride (j): odd
-constexpr int kR2S = 16 * kR2P + 16 / kR2G;         // Y stride per ring pair: odd for G = 16
-}  // namespace
-#ifndef TAT_R2_MINB
-#define TAT_R2_MINB 2   // CTAs per SM the two-stage ring kernels are compiled for
-#endif
-#ifndef TAT_R2_MINB_K3
-#define TAT_R2_MINB_K3 TAT_R2_MINB
-#endif
-#ifndef TAT_R2_MINB_K3T
-#define TAT_R2_MINB_K3T TAT_R2_MINB
-#endif
-#ifndef TAT_R2_MINB_K5
-#define TAT_R2_MINB_K5 TAT_R2_MINB
-#endif
-#ifndef TAT_R2_MINB_K5T
-#define TAT_R2_MINB_K5T 3
-#endif
-#ifndef TAT_R2_TWLD
-#define TAT_R2_TWLD 0   // stage-A twiddles W^{j k1}: 1 = table loads (L1), 0 = powers in registers
-#endif
-// y[k1] = x[k1] W_512^{+-j k1} (CONJ: the conjugate twiddles), k1 < 32
-template <bool CONJ>
-__device__ __forceinline__ void r2_twiddle_store(float2* y, const float2 (&x)[32], const float2* __restrict__ tw,
-                                                 int j) {
-  y[0] = x[0];
-#if TAT_R2_TWLD
-#pragma unroll
-  for (int k1 = 1; k1 < 32; ++k1) {
-    const float2 w = __ldg(&tw[(j * k1) & 511]);
-    y[k1] = CONJ ? cmulc(x[k1], w) : cmul(x[k1], w);
-  }
-#else
-  float2 pw[32];
-  const float2 w = __ldg(&tw[j]);
-  ce::pow_tree<32>(CONJ ? make_float2(w.x, -w.y) : w, pw);
-#pragma unroll
-  for (int k1 = 1; k1 < 32; ++k1) y[k1] = cmul(x[k1], pw[k1]);
-#endif
-}
-__global__ void __launch_bounds__(16 * kR2G, TAT_R2_MINB_K3) k3_ring2(DevPlan P) {
-  constexpr int half = 256, G = kR2G;   // n_phi = 512
-  extern __shared__ float2 sm[];
-  const Consts& C = P.C;
-  const int NL = C.NL;
-  const int b = C.b0 + blockIdx.y, j0 = blockIdx.x * (2 * G);
-  const float2* S2 = P.S2 + (size_t)b * half * NL;
-  float2* Y = sm;
-  pdl_wait();
-  pdl_trigger();
-  {   // stage A
-    const int j = threadIdx.x & 15, gg = threadIdx.x >> 4, ja = j0 + 2 * gg;
-    const float2* ra = S2 + (size_t)ja * half + j;
-    float2 va[16], vb[16];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      va[m] = ja < NL ? ra[16 * m] : make_float2(0.f, 0.f);
-      vb[m] = ja + 1 < NL ? ra[half + 16 * m] : make_float2(0.f, 0.f);
-    }
-    float2 x[32];
-#pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const float2 d = make_float2(va[m].x - vb[m].y, va[m].y + vb[m].x);    // va + i vb
-      const float2 c = make_float2(va[m].x + vb[m].y, -va[m].y + vb[m].x);   // conj va + i conj vb
-      x[m < 8 ? m + 24 : m - 8] = d;   // l' = j + 16 m -> l = l' - 128 (mod 512)
-      x[m + 8] = c;                    // l + 256
-    }
-    ce::dftr<32, -1>(x);
-    r2_twiddle_store<false>(Y + gg * kR2S + j * kR2P, x, P.tw_ring, j);   // x W_512^{j k1}
-  }
-  // multiplier values of this thread's 16 (kp = 0: 17) outputs, loaded before the barrier so
-  // that their latency overlaps stage B (output slot s: k = kout(s), see below)
-  const int gg = threadIdx.x % G, kp = threadIdx.x / G, ja = j0 + 2 * gg;
-  const int ka = kp == 0 ? 0 : kp, kb = kp == 0 ? 16 : 32 - kp;
-  auto kout = [&](int s) { return kp == 0 ? (s <= 8 ? 32 * s : 16 + 32 * (s - 9)) : (s < 8 ? ka + 32 * s : kb + 32 * (s - 8)); };
-  const bool ok0 = ja < NL, ok1 = ja + 1 < NL;
-  float2 mo[17];
-#pragma unroll
-  for (int s = 0; s < 17; ++s) {
-    const int k = kout(s);
-    const bool v = s < 16 || kp == 0;
-    mo[s] = make_float2(v && ok0 ? __ldg(&P.mult[(size_t)k * NL + ja]) : 0.f,
-                        v && ok1 ? __ldg(&P.mult[(size_t)k * NL + ja + 1]) : 0.f);
-  }
-  __syncthreads();
-  {   // stage B + output
-    const float2* y = Y + gg * kR2S;
-    float2 za[16], zb[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      za[j] = y[j * kR2P + ka];
-      zb[j] = y[j * kR2P + kb];
-    }
-    ce::dftr<16, -1>(za);   // Z[ka + 32 k2]
-    ce::dftr<16, -1>(zb);   // Z[kb + 32 k2]
-    float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
-    // output k from Z[k] and Z[-k]; (k1, k2) -> -k = (32 - k1) + 32 (15 - k2) for k1 > 0,
-    // (0, k2) -> (0, 16 - k2) (mod 16)
-    auto out = [&](int s, float2 zk, float2 zm) {
-      const int k = kout(s);
-      if (k & 1) zm = make_float2(-zm.x, -zm.y);
-      const float2 F1 = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
-      const float2 F2 = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
-      float2* o = S3 + (size_t)k * NL + ja;
-      if (ok0) o[0] = ipow_scale(F1, mo[s].x, k);
-      if (ok1) o[1] = ipow_scale(F2, mo[s].y, k);
-    };
-    if (kp == 0) {
-#pragma unroll
-      for (int k2 = 0; k2 <= 8; ++k2) out(k2, za[k2 & 15], za[(16 - k2) & 15]);
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) out(9 + k2, zb[k2], zb[15 - k2]);
-    } else {
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) out(k2, za[k2], zb[15 - k2]);
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) out(8 + k2, zb[k2], za[15 - k2]);
-    }
-  }
-}
-
-// ------------------------------------------------------------------ K3T, two-stage (n_phi = 512)
-// The transpose of k3_ring2, as k3t_ring computes it (below), with k = a + 16 r, l = k1 + 32 k2:
-//   z[k1 + 32 k2] = sum_a W_16^{-a k2} W_512^{-a k1} sum_r Z[a + 16 r] W_32^{-r k1}.
-// Stage A (thread (a, gg); lanes = ring pairs, so each S3 row k is read as one contiguous run of
-// 2G rings): Z[k] for k <= 256 from S3 row k, for k > 256 from row 512 - k by the completion
-// (read twice, from L1/L2, instead of a shared-memory pass); 32-point DFT, twiddle.  Stage B
-// (thread (kp, gg)): 16-point DFTs of k1 = kp and kp + 16, in place.  Output as in k3t_ring: the
-// group's nodes in destination order (k3t_dst, groups of 2G rings).
-__global__ void __launch_bounds__(16 * kR2G, TAT_R2_MINB_K3T) k3t_ring2(DevPlan P) {
-  constexpr int nf = 512, half = 256, G = kR2G;
-  extern __shared__ float2 sm[];
-  const Consts& C = P.C;
-  const int NL = C.NL;
-  const int b = C.b0 + blockIdx.y, j0 = blockIdx.x * (2 * G);
-  float2* Y = sm;
-  const int gg0 = threadIdx.x % G, i0 = threadIdx.x / G;   // (a or kp, gg) of both stages
-  const int ja = j0 + 2 * gg0;
-  const bool ok0 = ja < NL, ok1 = ja + 1 < NL;
-  pdl_wait();
-  pdl_trigger();
-  {   // stage A
-    const int a = i0;
-    const float2* S3 = P.S3 + (size_t)b * C.Kp * NL + ja;
-    float2 x[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const int k = a + 16 * r;
-      const bool dir = k <= half;
-      const int kk = dir ? k : nf - k;
-      const float2 e1 = ok0 ? S3[(size_t)kk * NL] : make_float2(0.f, 0.f);
-      const float2 e2 = ok1 ? S3[(size_t)kk * NL + 1] : make_float2(0.f, 0.f);
-      if (dir) {
-        x[r] = make_float2(e1.x - e2.y, e1.y + e2.x);   // E1 + i E2 (slot 256 is -K)
-      } else {
-        const float sg = (kk & 1) ? -1.f : 1.f;         // E(-k) = (-1)^k conj E(k)
-        x[r] = make_float2(sg * (e1.x + e2.y), sg * (-e1.y + e2.x));
-      }
-    }
-    ce::dftr<32, 1>(x);
-    r2_twiddle_store<true>(Y + gg0 * kR2S + a * kR2P, x, P.tw_ring, a);   // x W_512^{-a k1}
-  }
-  __syncthreads();
-  // the output records (position, source) of the first chunk, loaded during stage B
-  const int nout = min(2 * G, NL - j0) * half;
-  const int2* dst = P.k3t_dst + (size_t)j0 * half;
-  constexpr int T = 16 * G, U = 8;
-  int2 dd[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int i = threadIdx.x + u * T;
-    dd[u] = i < nout ? __ldg(&dst[i]) : make_int2(0, 0);
-  }
-  {   // stage B, in place: Y[gg][k2][k1] = z[k1 + 32 k2]
-    float2* y = Y + gg0 * kR2S;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k1 = i0 + 16 * h;
-      float2 z[16];
-#pragma unroll
-      for (int a = 0; a < 16; ++a) z[a] = y[a * kR2P + k1];
-      ce::dftr<16, 1>(z);
-#pragma unroll
-      for (int k2 = 0; k2 < 16; ++k2) y[k2 * kR2P + k1] = z[k2];
-    }
-  }
-  __syncthreads();
-  float2* S2 = P.S2 + (size_t)b * half * NL;
-  for (int i = threadIdx.x; i < nout; i += U * T) {
-    int2 dn[U];   // next chunk's records, in flight while this chunk is stored
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int in = i + (U + u) * T;
-      dn[u] = in < nout ? __ldg(&dst[in]) : make_int2(0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (i + u * T < nout) {
-        const int jj = dd[u].y >> 11, lp = dd[u].y & 2047, gg = jj >> 1;
-        const int l = (lp - nf / 4) & (nf - 1), lh = (l + half) & (nf - 1);
-        const float2 z = Y[gg * kR2S + (l >> 5) * kR2P + (l & 31)];
-        const float2 zh = Y[gg * kR2S + (lh >> 5) * kR2P + (lh & 31)];
-        S2[dd[u].x] = (jj & 1) ? make_float2(0.5f * (z.y + zh.y), -0.5f * (z.x - zh.x))
-                               : make_float2(0.5f * (z.x + zh.x), 0.5f * (z.y - zh.y));
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) dd[u] = dn[u];
   }
 }
 
@@ -466,150 +236,6 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
   }
 }
 
-// ------------------------------------------------------------------ K5 / K5T, two-stage (n_phi = 512)
-// K5: the C2R synthesis of k5_ring with k = a + 16 r, l = k1 + 32 k2 (as k3t_ring2): stage A reads
-// S4 rows straight into registers (lanes = transforms: contiguous runs of 2G time samples of row
-// k; k > 256 from row 512 - k by the completion), stage B in place, then the detector restriction
-// from shared memory as in k5_ring.
-template <bool VAR>
-__global__ void __launch_bounds__(16 * kR2G, TAT_R2_MINB_K5) k5_ring2(DevPlan P, float* __restrict__ gout) {
-  constexpr int nf = 512, half = 256, G = kR2G;
-  extern __shared__ float2 sm[];
-  const Consts& C = P.C;
-  const int n_t = C.n_t, n_det = C.n_det;
-  const int b = C.b0 + blockIdx.y, t0 = blockIdx.x * (2 * G);
-  float2* Y = sm;
-  const int gg0 = threadIdx.x % G, i0 = threadIdx.x / G;
-  const int t = t0 + 2 * gg0;
-  const bool ok0 = t < n_t, ok1 = t + 1 < n_t;
-  pdl_wait();
-  pdl_trigger();
-  {   // stage A
-    const int a = i0;
-    const float2* S4 = P.S4 + (size_t)b * C.Kp * n_t + t;
-    float2 x[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const int k = a + 16 * r;
-      const bool dir = k <= half;
-      const int kk = dir ? k : nf - k;
-      const float2 v0 = ok0 ? S4[(size_t)kk * n_t] : make_float2(0.f, 0.f);
-      const float2 v1 = ok1 ? S4[(size_t)kk * n_t + 1] : make_float2(0.f, 0.f);
-      if (k == 0 || k == half) x[r] = make_float2(v0.x, v1.x);   // real parts (C2R convention)
-      else if (dir) x[r] = make_float2(v0.x - v1.y, v0.y + v1.x);  // v0 + i v1
-      else x[r] = make_float2(v0.x + v1.y, -v0.y + v1.x);         // conj v0 + i conj v1
-    }
-    ce::dftr<32, 1>(x);
-    r2_twiddle_store<true>(Y + gg0 * kR2S + a * kR2P, x, P.tw_ring, a);   // x W_512^{-a k1}
-  }
-  __syncthreads();
-  {   // stage B, in place: Y[gg][k2][k1] = X[k1 + 32 k2]
-    float2* y = Y + gg0 * kR2S;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k1 = i0 + 16 * h;
-      float2 z[16];
-#pragma unroll
-      for (int a = 0; a < 16; ++a) z[a] = y[a * kR2P + k1];
-      ce::dftr<16, 1>(z);
-#pragma unroll
-      for (int k2 = 0; k2 < 16; ++k2) y[k2 * kR2P + k1] = z[k2];
-    }
-  }
-  __syncthreads();
-  const int tt_n = min(2 * G, n_t - t0);
-  for (int d = threadIdx.x; d < n_det; d += blockDim.x) {
-    const int l = __ldg(&P.ring[d]);
-    const int pos = (l >> 5) * kR2P + (l & 31);
-    const size_t i0g = ((size_t)b * n_t + t0) * n_det + d;
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg) {   // transform gg: samples 2 gg (real part), 2 gg + 1 (imag)
-      if (2 * gg < tt_n) {
-        const float2 z = Y[gg * kR2S + pos];
-        const size_t i = i0g + (size_t)(2 * gg) * n_det;
-        gout[i] = epi_fwd<VAR>(P, i, z.x);
-        if (2 * gg + 1 < tt_n) gout[i + n_det] = epi_fwd<VAR>(P, i + n_det, z.y);
-      }
-    }
-  }
-}
-
-// K5T: detectors placed at their ring positions in shared memory (zeros elsewhere unless every
-// position has a detector), then the two stages of k3_ring2 (stage A reading shared memory) with
-// the outputs of each (k, -k) pair formed in one thread and stored straight to S4 (contiguous runs
-// of 2G time samples of row k).
-__global__ void __launch_bounds__(16 * kR2G, TAT_R2_MINB_K5T) k5t_ring2(DevPlan P, const float* __restrict__ gin) {
-  constexpr int nf = 512, G = kR2G;
-  constexpr int XS = nf + nf / 32 + 1;   // input row stride: l + (l >> 5), odd
-  extern __shared__ float2 sm[];
-  const Consts& C = P.C;
-  const int n_t = C.n_t, n_det = C.n_det;
-  const int b = C.b0 + blockIdx.y, t0 = blockIdx.x * (2 * G);
-  float2* X0 = sm;                  // [G][XS] detector samples on the ring
-  float2* Y = sm;                   // [G][kR2S] after stage A's reads (aliases X0)
-  const int tt_n = min(2 * G, n_t - t0);
-  if (n_det < nf)
-    for (int i = threadIdx.x; i < G * XS; i += blockDim.x) X0[i] = make_float2(0.f, 0.f);
-  pdl_wait();
-  pdl_trigger();
-  if (n_det < nf) __syncthreads();
-  for (int d = threadIdx.x; d < n_det; d += blockDim.x) {
-    const int l = __ldg(&P.ring[d]);
-    const float* gi = gin + ((size_t)b * n_t + t0) * n_det + d;
-    float gv[2 * G];
-#pragma unroll
-    for (int tt = 0; tt < 2 * G; ++tt) gv[tt] = tt < tt_n ? gi[(size_t)tt * n_det] : 0.f;
-#pragma unroll
-    for (int gg = 0; gg < G; ++gg) X0[gg * XS + l + (l >> 5)] = make_float2(gv[2 * gg], gv[2 * gg + 1]);
-  }
-  __syncthreads();
-  {   // stage A (thread (j, gg)): x[r] = X0[gg][j + 16 r]
-    const int j = threadIdx.x & 15, gg = threadIdx.x >> 4;
-    float2 x[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const int l = j + 16 * r;
-      x[r] = X0[gg * XS + l + (l >> 5)];
-    }
-    __syncthreads();   // Y aliases X0
-    ce::dftr<32, -1>(x);
-    r2_twiddle_store<false>(Y + gg * kR2S + j * kR2P, x, P.tw_ring, j);   // x W_512^{j k1}
-  }
-  __syncthreads();
-  {   // stage B + output
-    const int gg = threadIdx.x % G, kp = threadIdx.x / G, t = t0 + 2 * gg;
-    const int ka = kp == 0 ? 0 : kp, kb = kp == 0 ? 16 : 32 - kp;
-    const float2* y = Y + gg * kR2S;
-    float2 za[16], zb[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      za[j] = y[j * kR2P + ka];
-      zb[j] = y[j * kR2P + kb];
-    }
-    ce::dftr<16, -1>(za);
-    ce::dftr<16, -1>(zb);
-    float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
-    const bool ok0 = t < n_t, ok1 = t + 1 < n_t;
-    // even sample: (Z[k] + conj Z[-k]) / 2 ; odd sample: (Z[k] - conj Z[-k]) / (2i)
-    auto out = [&](int k, float2 zk, float2 zm) {
-      float2* o = S4 + (size_t)k * n_t + t;
-      if (ok0) o[0] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
-      if (ok1) o[1] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
-    };
-    if (kp == 0) {
-#pragma unroll
-      for (int k2 = 0; k2 <= 8; ++k2) out(32 * k2, za[k2 & 15], za[(16 - k2) & 15]);
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) out(16 + 32 * k2, zb[k2], zb[15 - k2]);
-    } else {
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) out(ka + 32 * k2, za[k2], zb[15 - k2]);
-#pragma unroll
-      for (int k2 = 0; k2 < 8; ++k2) out(kb + 32 * k2, zb[k2], za[15 - k2]);
-    }
-  }
-}
-
 // ------------------------------------------------------------------ K5T
 template <int nf>
 __global__ void __launch_bounds__(512) k5t_ring(DevPlan P, const float* __restrict__ gin) {
@@ -691,22 +317,14 @@ cudaError_t configure_ring_kernels(const Consts& C) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k5t_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   });
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k3_ring2, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k3t_ring2, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k5t_ring2, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e == cudaSuccess) e = configure_ring2_kernels(C);
   return e;
 }
 
 cudaError_t launch_k3(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
-  if (ring2_on(C, 1)) {
-    e = launch_pdl(C.pdl, k3_ring2, dim3((C.NL + 2 * kR2G - 1) / (2 * kR2G), C.batch), dim3(16 * kR2G),
-                   (size_t)kR2G * kR2S * sizeof(float2), s, P);
-    return e != cudaSuccess ? e : cudaGetLastError();
-  }
+  if (ring2_on(C, 1)) return launch_ring2(P, 1, nullptr, nullptr, s);
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
@@ -717,11 +335,7 @@ cudaError_t launch_k3(const DevPlan& P, cudaStream_t s) {
 cudaError_t launch_k3t(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
-  if (ring2_on(C, 2)) {
-    e = launch_pdl(C.pdl, k3t_ring2, dim3((C.NL + 2 * kR2G - 1) / (2 * kR2G), C.batch), dim3(16 * kR2G),
-                   (size_t)kR2G * kR2S * sizeof(float2), s, P);
-    return e != cudaSuccess ? e : cudaGetLastError();
-  }
+  if (ring2_on(C, 2)) return launch_ring2(P, 2, nullptr, nullptr, s);
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
@@ -732,13 +346,7 @@ cudaError_t launch_k3t(const DevPlan& P, cudaStream_t s) {
 cudaError_t launch_k5(const DevPlan& P, float* g, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
-  if (ring2_on(C, 4)) {
-    const dim3 grid((C.n_t + 2 * kR2G - 1) / (2 * kR2G), C.batch), blk(16 * kR2G);
-    const size_t sm2 = (size_t)kR2G * kR2S * sizeof(float2);
-    e = P.lowk_add ? launch_pdl(C.pdl, k5_ring2<true>, grid, blk, sm2, s, P, g)
-                   : launch_pdl(C.pdl, k5_ring2<false>, grid, blk, sm2, s, P, g);
-    return e != cudaSuccess ? e : cudaGetLastError();
-  }
+  if (ring2_on(C, 4)) return launch_ring2(P, 4, nullptr, g, s);
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
@@ -752,11 +360,7 @@ cudaError_t launch_k5(const DevPlan& P, float* g, cudaStream_t s) {
 cudaError_t launch_k5t(const DevPlan& P, const float* g, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
-  if (ring2_on(C, 8)) {
-    e = launch_pdl(C.pdl, k5t_ring2, dim3((C.n_t + 2 * kR2G - 1) / (2 * kR2G), C.batch), dim3(16 * kR2G),
-                   (size_t)kR2G * kR2S * sizeof(float2), s, P, g);
-    return e != cudaSuccess ? e : cudaGetLastError();
-  }
+  if (ring2_on(C, 8)) return launch_ring2(P, 8, g, nullptr, s);
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();

@@ -25,8 +25,9 @@ struct Consts {
   int col_strip = 16; // K2: columns per CTA (k2c_fwd recomputes one halo column;
                       // 12-16 measured best at C3, 20-32 slower)
   int col_strip_adj = 16; // K2Tb (k2c_adj): columns per CTA
-  int ring2 = 11;   // n_ring = 512: two-stage ring kernels instead of the Stockham ones (bits: ring2_on;
-                    // K5 keeps the Stockham kernel: 22.5 vs 22.7 us at C3)
+  int ring2 = -1;   // two-stage ring kernels (n_ring 256 / 512) instead of the Stockham ones: bit
+                    // mask (ring2_on), -1 = auto (all; K5 at n_ring = 512 stays Stockham: 21.8 vs
+                    // 22.0 us at C3, while at 256 the two-stage K5 wins: 24.1 -> 22.3 at C4)
   double R = 1, c = 1, T = 1;
   double h = 0, T_new0 = 0, T_new = 0, Lbox = 0, dxi = 0, dt = 0, dlam = 0, lam_max = 0;
   double wJ = 1, omega = 0;
@@ -112,10 +113,15 @@ constexpr int kStripTargets = 2560; // ... and its target budget
 // 8 KB -> K2Ta 93 / 142 us, 16 KB -> 65.5 / 93, 24 KB -> 68.6 / 81 (fewer heavy strips vs
 // occupancy)
 inline int strip_ov_bytes(int n) { return n >= 1024 ? 24576 : 16384; }
-// two-stage ring kernels (n_ring = 512): ring pairs per CTA; rings per K3T CTA (k3t_dst groups)
+// two-stage ring kernels (kernels_ring2.cu, n_ring = 256 / 512): transforms (ring pairs) per CTA;
+// rings per K3T CTA (k3t_dst groups)
 constexpr int kRing2G = 16;
 // C.ring2 bits: 1 K3, 2 K3T, 4 K5, 8 K5T
-inline bool ring2_on(const Consts& C, int bit) { return (C.ring2 & bit) && C.n_ring == 512; }
+inline bool ring2_size_ok(int n_ring) { return n_ring == 256 || n_ring == 512; }
+inline bool ring2_on(const Consts& C, int bit) {
+  const int m = C.ring2 >= 0 ? C.ring2 : (C.n_ring == 256 ? 15 : 11);
+  return (m & bit) && ring2_size_ok(C.n_ring);
+}
 inline int k3t_group_rings(const Consts& C) {
   return ring2_on(C, 2) ? 2 * kRing2G : 2 * std::min(4096 / C.n_ring, 16);
 }
@@ -277,6 +283,9 @@ cudaError_t launch_k1t(const DevPlan& P, const CUtensorMap& tm, float* f, cudaSt
 bool ring_fast_ok(const Consts& C);
 size_t smem_ring_fast(const Consts& C);
 cudaError_t configure_ring_kernels(const Consts& C);
+cudaError_t configure_ring2_kernels(const Consts& C);
+// two-stage ring kernels: which = 1 K3, 2 K3T, 4 K5 (g out), 8 K5T (g in)
+cudaError_t launch_ring2(const DevPlan& P, int which, const float* gin, float* gout, cudaStream_t s);
 cudaError_t launch_k3(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k3t(const DevPlan& P, cudaStream_t s);
 cudaError_t launch_k5(const DevPlan& P, float* g, cudaStream_t s);

@@ -358,21 +358,22 @@ def test_fused_adjoint_column_stage(torch_cuda, monkeypatch, name):
         assert (u - u0).abs().max().item() <= 1e-6 * u0.abs().max().item()
 
 
-def test_ring_engines_agree_c3(torch_cuda, monkeypatch):
-    """n_phi = 512: the two-stage ring kernels (k3_ring2 / k3t_ring2 / k5_ring2 / k5t_ring2,
-    TAT_RING2 bit mask; default 11 = all but K5) against the radix-8 Stockham ring kernels
-    (TAT_RING2=0): the same transforms in a different summation order, so A f and A* g agree to
-    fp32 rounding (<= 2e-6 of the maximum); the default path is the one the full-size oracle
-    parity tests check."""
+@pytest.mark.parametrize("name", ["C3", "C4", "C2"])
+def test_ring_engines_agree(torch_cuda, monkeypatch, name):
+    """n_phi = 512 / 256: the two-stage ring kernels (kernels_ring2.cu: K3 / K3T / K5 / K5T,
+    TAT_RING2 bit mask; default auto) against the radix-8 Stockham ring kernels (TAT_RING2=0):
+    the same transforms in a different summation order, so A f and A* g agree to fp32 rounding
+    (<= 2e-6 of the maximum); the default path is the one the full-size oracle parity tests
+    check."""
     torch = torch_cuda
-    geo = synth.geometry("C3")
+    geo = synth.geometry(name)
     plans = {}
     for r in ("0", "15"):
         monkeypatch.setenv("TAT_RING2", r)
         plans[r] = _plan(geo)
     monkeypatch.delenv("TAT_RING2")
     plans["default"] = _plan(geo)
-    f = torch.from_numpy(synth.phantom_batch("C3")).cuda()
+    f = torch.from_numpy(synth.phantom_batch(name)).cuda()
     g = torch.from_numpy(np.stack([synth.random_data(geo.n_t, geo.n_det, 900 + b)
                                    for b in range(geo.batch)])).cuda()
     a0, u0 = plans["0"].forward(f), plans["0"].adjoint(g)

@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/sweep42_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/sweep42_pytest.log
-for c in C3 C4 C5; do
-  python tools/time_stages.py $c 20 2>&1 | tail -1 >> gpurun_out/sweep42.txt
-done
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/sweep52_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/sweep52_pytest.log
+for c in C3 C4 C5 C2; do python tools/time_stages.py $c 20 2>&1 | tail -1 >> gpurun_out/sweep52.txt; done
