@@ -35,6 +35,9 @@ using namespace fe;
 #ifndef TAT_R2_MINB
 #define TAT_R2_MINB 2   // CTAs per SM the two-stage ring kernels are compiled for
 #endif
+#ifndef TAT_R2_MINB_K5
+#define TAT_R2_MINB_K5 3    // (measured at C4: K5 22.2 -> 20.5 us at 3; used at n_phi = 256 only)
+#endif
 #ifndef TAT_R2_MINB_K5T
 #define TAT_R2_MINB_K5T 3   // (measured at C3: K5T 22.4 -> 20.8 us at 3; K3 spills at 3)
 #endif
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(R2<nf>::T, TAT_R2_MINB) k3t_ring2(DevPlan P) {
 // ------------------------------------------------------------------ K5
 // transform gg carries time samples t0 + 2 gg (real part) and t0 + 2 gg + 1 (imaginary part)
 template <int nf, bool VAR>
-__global__ void __launch_bounds__(R2<nf>::T, TAT_R2_MINB) k5_ring2(DevPlan P, float* __restrict__ gout) {
+__global__ void __launch_bounds__(R2<nf>::T, TAT_R2_MINB_K5) k5_ring2(DevPlan P, float* __restrict__ gout) {
   using Q = R2<nf>;
   constexpr int R = Q::R, J = Q::J, G = Q::G, half = Q::half;
   extern __shared__ float2 sm[];

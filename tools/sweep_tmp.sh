@@ -1,3 +1,7 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/sweep52_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/sweep52_pytest.log
-for c in C3 C4 C5 C2; do python tools/time_stages.py $c 20 2>&1 | tail -1 >> gpurun_out/sweep52.txt; done
+for rep in 1 2; do
+python tools/time_stages.py C3 20 2>&1 | tail -1 | sed "s|^|base |" >> gpurun_out/sweep54.txt
+TAT_RING2=15 TAT_LIB=variants/k5m3.so python tools/time_stages.py C3 20 2>&1 | tail -1 | sed "s|^|k5m3 r15 |" >> gpurun_out/sweep54.txt
+TAT_LIB=variants/k5m3.so python tools/time_stages.py C4 20 2>&1 | tail -1 | sed "s|^|k5m3 C4 |" >> gpurun_out/sweep54.txt
+python tools/time_stages.py C4 20 2>&1 | tail -1 | sed "s|^|base C4 |" >> gpurun_out/sweep54.txt
+done
