@@ -47,15 +47,18 @@ namespace {
 template <int nf>
 struct R2 {
   static constexpr int R = nf >= 512 ? 32 : 16;   // stage-A DFT length (over r)
-  static constexpr int J = nf / R;                  // stage-B DFT length (over j) = 16
-  static constexpr int G = kRing2G;                 // transforms per CTA
-  static constexpr int T = G * J;                   // threads (stage A: one per (j, gg))
-  static constexpr int NB = G * R / 2;              // stage-B jobs (kp, gg)
+  static constexpr int J = nf / R;                  // stage-B DFT length (over j): 16, or 32 at 1024
+  static constexpr int G = ring2_G(nf);             // transforms per CTA (16, or 8 at 1024)
+  static constexpr int T = G * J;                   // threads (stage A: one per (j, gg)) = 256
+  static constexpr int CPT = J == 32 ? 1 : 2;       // stage-B columns k1 per thread
+  static constexpr int NB = G * R / CPT;            // stage-B jobs (kp, gg)
   static constexpr int P = R + 1;                   // Y row stride (j): odd
-  static constexpr int S = J * P + 1;               // Y stride per transform: odd
+  // Y stride per transform: odd for G = 16 (lanes = 16 transforms in a half-warp), 2 mod 16 for
+  // G = 8 (lanes = 8 transforms x 2 rows / columns)
+  static constexpr int S = J * P + (G == 16 ? 1 : 2);
   static constexpr int half = nf / 2, quarter = nf / 4;
   static constexpr int XS = nf + nf / 32 + 1;       // K5T input row stride (l + l / 32): odd
-  static_assert(J == 16 && G == 16, "ring2 layout");
+  static_assert(T == 256 && (J == 16 || nf == 1024), "ring2 layout");
   // element l = k1 + R k2 of transform gg after stage B
   __device__ static __forceinline__ int yidx(int gg, int l) {
     return gg * S + (int)((unsigned)l / R) * P + (int)((unsigned)l % R);
@@ -130,22 +133,25 @@ __device__ __forceinline__ int r2_kout(int kp, int ka, int kb, int s) {
   return kp == 0 ? (s <= H ? R * s : R / 2 + R * (s - H - 1)) : (s < H ? ka + R * s : kb + R * (s - H));
 }
 
-// Stage B of the inverse-sign transforms (K3T, K5), in place: Y[gg][k2][k1] = z[k1 + R k2]
-template <int nf>
-__device__ __forceinline__ void r2_stage_b_inv(float2* Y, int gg, int kp) {
+// Stage B in place (sign S): Y[gg][k2][k1] = sum_j W_J^{S j k2} Y[gg][j][k1] for the CPT
+// columns k1 = kp + (R / CPT) h of thread (kp, gg)
+template <int nf, int S>
+__device__ __forceinline__ void r2_stage_b_inplace(float2* Y, int gg, int kp) {
   using Q = R2<nf>;
   float2* y = Y + gg * Q::S;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int k1 = kp + (Q::R / 2) * h;
-    float2 z[16];
+  for (int h = 0; h < Q::CPT; ++h) {
+    const int k1 = kp + (Q::R / Q::CPT) * h;
+    float2 z[Q::J];
 #pragma unroll
     for (int a = 0; a < Q::J; ++a) z[a] = y[a * Q::P + k1];
-    ce::dftr<Q::J, 1>(z);
+    ce::dftr<Q::J, S>(z);
 #pragma unroll
     for (int k2 = 0; k2 < Q::J; ++k2) y[k2 * Q::P + k1] = z[k2];
   }
 }
+template <int nf>
+__device__ __forceinline__ void r2_stage_b_inv(float2* Y, int gg, int kp) { r2_stage_b_inplace<nf, 1>(Y, gg, kp); }
 
 }  // namespace
 
@@ -183,6 +189,36 @@ __global__ void __launch_bounds__(R2<nf>::T, TAT_R2_MINB) k3_ring2(DevPlan P) {
     }
     r2_stage_a_fwd<nf>(x, Y, P.tw_ring, j, gg);
   }
+  if constexpr (J == 32) {   // n_phi = 1024: stage B in place, then the (k, -k) pairs from smem
+    const int gg = threadIdx.x % G, kk = threadIdx.x / G, ja = j0 + 2 * gg;   // item (k, gg)
+    const bool ok0 = ja < NL, ok1 = ja + 1 < NL;
+    constexpr int NI = (half + 1 + Q::T / G - 1) / (Q::T / G);                   // items per thread
+    float2 mo[NI];
+#pragma unroll
+    for (int u = 0; u < NI; ++u) {
+      const int k = kk + (Q::T / G) * u;
+      mo[u] = make_float2(k <= half && ok0 ? __ldg(&P.mult[(size_t)k * NL + ja]) : 0.f,
+                          k <= half && ok1 ? __ldg(&P.mult[(size_t)k * NL + ja + 1]) : 0.f);
+    }
+    __syncthreads();
+    r2_stage_b_inplace<nf, -1>(Y, gg, kk);
+    __syncthreads();
+    float2* S3 = P.S3 + (size_t)b * C.Kp * NL;
+#pragma unroll
+    for (int u = 0; u < NI; ++u) {
+      const int k = kk + (Q::T / G) * u;
+      if (k <= half) {
+        const float2 zk = Y[Q::yidx(gg, k)];
+        float2 zm = Y[Q::yidx(gg, (nf - k) & (nf - 1))];
+        if (k & 1) zm = make_float2(-zm.x, -zm.y);
+        const float2 F1 = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+        const float2 F2 = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+        float2* o = S3 + (size_t)k * NL + ja;
+        if (ok0) o[0] = ipow_scale(F1, mo[u].x, k);
+        if (ok1) o[1] = ipow_scale(F2, mo[u].y, k);
+      }
+    }
+  } else {
   // multiplier values of this thread's outputs, loaded before the barrier (latency under stage B)
   const int gg = threadIdx.x % G, kp = threadIdx.x / G, ja = j0 + 2 * gg;
   const bool act = threadIdx.x < Q::NB;
@@ -209,6 +245,7 @@ __global__ void __launch_bounds__(R2<nf>::T, TAT_R2_MINB) k3_ring2(DevPlan P) {
       if (ok0) o[0] = ipow_scale(F1, mo[s].x, k);
       if (ok1) o[1] = ipow_scale(F2, mo[s].y, k);
     });
+  }
   }
 }
 
@@ -374,8 +411,21 @@ __global__ void __launch_bounds__(R2<nf>::T, TAT_R2_MINB_K5T) k5t_ring2(DevPlan 
     r2_stage_a_fwd<nf>(x, Y, P.tw_ring, j, gg);
   }
   __syncthreads();
-  if (threadIdx.x < Q::NB) {   // stage B + output: (Z[k] + conj Z[-k]) / 2 (even sample),
-                               // (Z[k] - conj Z[-k]) / 2i (odd sample)
+  if constexpr (J == 32) {   // n_phi = 1024: stage B in place, then the (k, -k) pairs from smem
+    const int gg = threadIdx.x % G, kk = threadIdx.x / G, t = t0 + 2 * gg;
+    r2_stage_b_inplace<nf, -1>(Y, gg, kk);
+    __syncthreads();
+    float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
+    const bool ok0 = t < n_t, ok1 = t + 1 < n_t;
+    for (int k = kk; k <= Q::half; k += Q::T / G) {
+      const float2 zk = Y[Q::yidx(gg, k)];
+      const float2 zm = Y[Q::yidx(gg, (nf - k) & (nf - 1))];
+      float2* o = S4 + (size_t)k * n_t + t;
+      if (ok0) o[0] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+      if (ok1) o[1] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+    }
+  } else if (threadIdx.x < Q::NB) {   // stage B + output: (Z[k] + conj Z[-k]) / 2 (even
+                                      // sample), (Z[k] - conj Z[-k]) / 2i (odd sample)
     const int gg = threadIdx.x % G, kp = threadIdx.x / G, t = t0 + 2 * gg;
     const int ka = kp == 0 ? 0 : kp, kb = kp == 0 ? R / 2 : R - kp;
     float2 za[16], zb[16];
@@ -402,6 +452,7 @@ static size_t r2_smem() {
   switch (C.n_ring) {                                           \
     case 256: { constexpr int NF = 256; __VA_ARGS__; } break;   \
     case 512: { constexpr int NF = 512; __VA_ARGS__; } break;   \
+    case 1024: { constexpr int NF = 1024; __VA_ARGS__; } break; \
     default: return cudaErrorInvalidValue;                      \
   }
 
@@ -424,7 +475,7 @@ cudaError_t configure_ring2_kernels(const Consts& C) {
 cudaError_t launch_ring2(const DevPlan& P, int which, const float* gin, float* gout, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
-  const int G = kRing2G;
+  const int G = ring2_G(C.n_ring);
   const dim3 gj((C.NL + 2 * G - 1) / (2 * G), C.batch), gt((C.n_t + 2 * G - 1) / (2 * G), C.batch);
   TAT_RING2_SWITCH({
     const dim3 blk(R2<NF>::T);

@@ -113,17 +113,17 @@ constexpr int kStripTargets = 2560; // ... and its target budget
 // 8 KB -> K2Ta 93 / 142 us, 16 KB -> 65.5 / 93, 24 KB -> 68.6 / 81 (fewer heavy strips vs
 // occupancy)
 inline int strip_ov_bytes(int n) { return n >= 1024 ? 24576 : 16384; }
-// two-stage ring kernels (kernels_ring2.cu, n_ring = 256 / 512): transforms (ring pairs) per CTA;
-// rings per K3T CTA (k3t_dst groups)
-constexpr int kRing2G = 16;
+// two-stage ring kernels (kernels_ring2.cu, n_ring in {256, 512, 1024}): transforms (ring pairs)
+// per CTA (ring2_G), hence rings per K3T CTA (k3t_dst groups)
+__host__ __device__ constexpr int ring2_G(int n_ring) { return n_ring >= 1024 ? 8 : 16; }
 // C.ring2 bits: 1 K3, 2 K3T, 4 K5, 8 K5T
-inline bool ring2_size_ok(int n_ring) { return n_ring == 256 || n_ring == 512; }
+inline bool ring2_size_ok(int n_ring) { return n_ring == 256 || n_ring == 512 || n_ring == 1024; }
 inline bool ring2_on(const Consts& C, int bit) {
-  const int m = C.ring2 >= 0 ? C.ring2 : (C.n_ring == 256 ? 15 : 11);
+  const int m = C.ring2 >= 0 ? C.ring2 : (C.n_ring == 512 ? 11 : 15);
   return (m & bit) && ring2_size_ok(C.n_ring);
 }
 inline int k3t_group_rings(const Consts& C) {
-  return ring2_on(C, 2) ? 2 * kRing2G : 2 * std::min(4096 / C.n_ring, 16);
+  return ring2_on(C, 2) ? 2 * ring2_G(C.n_ring) : 2 * std::min(4096 / C.n_ring, 16);
 }
 
 // returns "" on success, else an error message; code receives 1 (invalid) or 2 (unsupported)

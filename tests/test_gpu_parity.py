@@ -358,9 +358,9 @@ def test_fused_adjoint_column_stage(torch_cuda, monkeypatch, name):
         assert (u - u0).abs().max().item() <= 1e-6 * u0.abs().max().item()
 
 
-@pytest.mark.parametrize("name", ["C3", "C4", "C2"])
+@pytest.mark.parametrize("name", ["C3", "C4", "C2", "C5"])
 def test_ring_engines_agree(torch_cuda, monkeypatch, name):
-    """n_phi = 512 / 256: the two-stage ring kernels (kernels_ring2.cu: K3 / K3T / K5 / K5T,
+    """n_phi = 512 / 256 / 1024 (C5: a 270-degree arc): the two-stage ring kernels (kernels_ring2.cu: K3 / K3T / K5 / K5T,
     TAT_RING2 bit mask; default auto) against the radix-8 Stockham ring kernels (TAT_RING2=0):
     the same transforms in a different summation order, so A f and A* g agree to fp32 rounding
     (<= 2e-6 of the maximum); the default path is the one the full-size oracle parity tests

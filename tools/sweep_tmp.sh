@@ -1,7 +1,3 @@
 mkdir -p gpurun_out
-for rep in 1 2; do
-python tools/time_stages.py C3 20 2>&1 | tail -1 | sed "s|^|base |" >> gpurun_out/sweep54.txt
-TAT_RING2=15 TAT_LIB=variants/k5m3.so python tools/time_stages.py C3 20 2>&1 | tail -1 | sed "s|^|k5m3 r15 |" >> gpurun_out/sweep54.txt
-TAT_LIB=variants/k5m3.so python tools/time_stages.py C4 20 2>&1 | tail -1 | sed "s|^|k5m3 C4 |" >> gpurun_out/sweep54.txt
-python tools/time_stages.py C4 20 2>&1 | tail -1 | sed "s|^|base C4 |" >> gpurun_out/sweep54.txt
-done
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/sweep55_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/sweep55_pytest.log
+for r in -1 0 15; do TAT_RING2=$r python tools/time_stages.py C5 20 2>&1 | tail -1 | sed "s|^|ring2=$r |" >> gpurun_out/sweep55.txt; done
