@@ -858,6 +858,13 @@ cudaError_t launch_k2t_sumf(const DevPlan& P, cudaStream_t s) {
 // for p in [0, N/2].  One CTA (128 threads) per two row pairs (rows y0..y0+3); the [p][4 y]
 // output tiles are transposed into S1 by TMA tensor stores (32-byte rows per p).
 constexpr int kK1BoxP = 128;   // p extent of one S1 tile (= C.s1boxP on this path)
+#ifndef TAT_K1_PAD
+#define TAT_K1_PAD 1           // K1 column buffers: padded rows (1) or XOR swizzle (0)
+#endif
+#ifndef TAT_K1_SLOTS
+#define TAT_K1_SLOTS 2         // K1 output tiles in flight
+#endif
+constexpr int kK1Slots = TAT_K1_SLOTS;
 constexpr int kK1TSlots = 8;   // K1T: S~1 tiles in flight (TMA loads issued ahead)
 #ifndef TAT_K1T_EMPTY
 #define TAT_K1T_EMPTY 0        // K1T: per-slot consumed barriers instead of a CTA barrier per tile
@@ -867,16 +874,16 @@ constexpr int kK1TSlots = 8;   // K1T: S~1 tiles in flight (TMA loads issued ahe
 template <int n, bool VAR>
 __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPlan P, const __grid_constant__ CUtensorMap tm,
                                                   const float* __restrict__ f) {
-  using G = ColGeo<n>;
+  using G = ColGeo<n, 8, TAT_K1_PAD>;
   extern __shared__ __align__(128) float2 sm[];
   const Consts& C = P.C;
   const int t = threadIdx.x, j = t % G::J, sg = t / G::J;
   const int b = C.b0 + blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
   float2* W0 = sm;
   float2* W1 = sm + G::WS;
-  // 2 tiles [kK1BoxP][4]; at the start the 4 input rows (2n float2)
+  // kK1Slots tiles [kK1BoxP][4]; at the start the 4 input rows (2n float2)
   float2* stg = sm + 2 * G::WS;
-  constexpr int STG = (2 * kK1BoxP * 4 > 2 * n) ? 2 * kK1BoxP * 4 : 2 * n;
+  constexpr int STG = (kK1Slots * kK1BoxP * 4 > 2 * n) ? kK1Slots * kK1BoxP * 4 : 2 * n;
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + STG);
   const float* rows = reinterpret_cast<const float*>(stg);
   float2 A[G::NRES][G::R];
@@ -917,9 +924,9 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPl
   // (measured: per-thread 16-byte stores of the row segments instead of TMA tile stores: K1
   // 52 -> 74 us at C3)
   for (int c = 0; c < nch; ++c) {
-    float4* tile = reinterpret_cast<float4*>(stg + (c & 1) * kK1BoxP * 4);
-    if (c >= 2) {   // the store issued from this slot two chunks ago has read its tile
-      if (t == 0) ac::bulk_wait_read<1>();
+    float4* tile = reinterpret_cast<float4*>(stg + (c % kK1Slots) * kK1BoxP * 4);
+    if (c >= kK1Slots) {   // the store issued from this slot kK1Slots chunks ago has read its tile
+      if (t == 0) ac::bulk_wait_read<kK1Slots - 1>();
       __syncthreads();
     }
     const int p = c * kK1BoxP + t;
@@ -1261,7 +1268,8 @@ size_t smem_k2c_adjf(const Consts& C) {
 }
 
 size_t smem_k1c(const Consts& C) {
-  return (size_t)2 * (col_R(C.n) * 8) * (C.n / col_R(C.n) + 1) * 8 + (size_t)std::max(2 * kK1BoxP * 4, 2 * C.n) * 8 + 64;
+  return (size_t)2 * (col_R(C.n) * 8) * (C.n / col_R(C.n) + TAT_K1_PAD) * 8 +
+         (size_t)std::max(kK1Slots * kK1BoxP * 4, 2 * C.n) * 8 + 64;
 }
 size_t smem_k1c_adj(const Consts& C) {
   return (size_t)2 * 8 * C.n * 8 + (size_t)kK1TSlots * kK1BoxP * 32 + 128;
