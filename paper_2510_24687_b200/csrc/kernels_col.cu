@@ -1060,6 +1060,13 @@ template <int n, bool ADJ>
 #define TAT_K4_TWS 0   // output twiddles staged in smem per CTA (1) or read from L1 per output
                        // (0; measured at C3: K4 68.3 -> 66.2 us, K4T 77.9 -> 74.8 us)
 #endif
+#ifndef TAT_K4_U
+#define TAT_K4_U 4     // K4/K4T outputs per thread per pass (twiddle loads issued together)
+#endif
+#ifndef TAT_K4_W2SQ
+#define TAT_K4_W2SQ 1  // W^{2u} as the square of W^u instead of a table load (measured at C3:
+                       // K4 61.7 -> 59.7 us, K4T 72.0 -> 69.7)
+#endif
 #ifndef TAT_K4_ALDG
 #define TAT_K4_ALDG 0  // stage-A pre-twiddles from L1 at each use (1) or in registers (0)
 #endif
@@ -1165,7 +1172,7 @@ __global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : TAT_K4_MI
       const float2 c2 = ce::cadd(cmul(sm[2 * G::WS + vp], w2), cmulc(sm[2 * G::WS + vm], w2));
       return ce::cadd(a, ce::cadd(c1, c2));
     };
-    constexpr int U4 = 4;
+    constexpr int U4 = TAT_K4_U;
     const int nout = ADJ ? NL : n_t;
     const float2 hJ = (!ADJ && NL == 3 * n + 1) ? in[3 * n] : make_float2(0.f, 0.f);
     const float om = (float)C.omega;
@@ -1184,7 +1191,8 @@ __global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : TAT_K4_MI
         } else {
           const int uu = o < nout ? u : 0, u2 = 2 * uu >= M2 ? 2 * uu - M2 : 2 * uu;
           w1[q] = __ldg(&P.tw_dct[uu]);
-          w2[q] = __ldg(&P.tw_dct[u2]);
+          if (TAT_K4_W2SQ) w2[q] = cmul(w1[q], w1[q]);   // W^{2u} = (W^u)^2 (one rounding more)
+          else w2[q] = __ldg(&P.tw_dct[u2]);
         }
         ml[q] = (ADJ && o < nout) ? __ldg(&P.mult[(size_t)k * NL + o]) : 0.f;
       }
