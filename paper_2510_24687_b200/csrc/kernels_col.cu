@@ -1061,11 +1061,16 @@ template <int n, bool ADJ>
                        // (0; measured at C3: K4 68.3 -> 66.2 us, K4T 77.9 -> 74.8 us)
 #endif
 #ifndef TAT_K4_U
-#define TAT_K4_U 4     // K4/K4T outputs per thread per pass (twiddle loads issued together)
+#define TAT_K4_U 0     // K4/K4T outputs per thread per pass (twiddle loads issued together);
+                       // 0: 4 for K4, 8 for K4T (measured with W1REC: K4T 69.7 -> 68.0 us)
 #endif
 #ifndef TAT_K4_W2SQ
 #define TAT_K4_W2SQ 1  // W^{2u} as the square of W^u instead of a table load (measured at C3:
                        // K4 61.7 -> 59.7 us, K4T 72.0 -> 69.7)
+#endif
+#ifndef TAT_K4_W1REC
+#define TAT_K4_W1REC -1 // W^u of a thread's later outputs by multiplication with W^{blockDim}
+                        // (-1: K4T only; for K4 it measured 59.7 -> 62.0 us)
 #endif
 #ifndef TAT_K4_ALDG
 #define TAT_K4_ALDG 0  // stage-A pre-twiddles from L1 at each use (1) or in registers (0)
@@ -1172,11 +1177,13 @@ __global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : TAT_K4_MI
       const float2 c2 = ce::cadd(cmul(sm[2 * G::WS + vp], w2), cmulc(sm[2 * G::WS + vm], w2));
       return ce::cadd(a, ce::cadd(c1, c2));
     };
-    constexpr int U4 = TAT_K4_U;
+    constexpr int U4 = TAT_K4_U > 0 ? TAT_K4_U : (ADJ ? 8 : 4);
+    constexpr bool W1REC = TAT_K4_W1REC < 0 ? ADJ : (TAT_K4_W1REC != 0);
     const int nout = ADJ ? NL : n_t;
     const float2 hJ = (!ADJ && NL == 3 * n + 1) ? in[3 * n] : make_float2(0.f, 0.f);
     const float om = (float)C.omega;
     float2* out = ADJ ? P.S3 + (size_t)(rbase + row) * NL : P.S4 + (size_t)(rbase + row) * n_t;
+    const float2 wstep = W1REC ? __ldg(&P.tw_dct[blockDim.x]) : make_float2(1.f, 0.f);
     for (int o0 = t; o0 < nout; o0 += U4 * (int)blockDim.x) {
       float2 w1[U4], w2[U4];
       float ml[U4];
@@ -1190,7 +1197,8 @@ __global__ void __launch_bounds__(3 * ColGeo<n, 4>::T, n >= 1024 ? 1 : TAT_K4_MI
           w2[q] = make_float2(tw.z, tw.w);
         } else {
           const int uu = o < nout ? u : 0, u2 = 2 * uu >= M2 ? 2 * uu - M2 : 2 * uu;
-          w1[q] = __ldg(&P.tw_dct[uu]);
+          if (W1REC && q > 0) w1[q] = cmul(w1[q - 1], wstep);   // W^{u + q T}
+          else w1[q] = __ldg(&P.tw_dct[uu]);
           if (TAT_K4_W2SQ) w2[q] = cmul(w1[q], w1[q]);   // W^{2u} = (W^u)^2 (one rounding more)
           else w2[q] = __ldg(&P.tw_dct[u2]);
         }
