@@ -866,6 +866,7 @@ constexpr int kK1BoxP = 128;   // p extent of one S1 tile (= C.s1boxP on this pa
 #endif
 constexpr int kK1Slots = TAT_K1_SLOTS;
 constexpr int kK1TSlots = 8;   // K1T: S~1 tiles in flight (TMA loads issued ahead)
+constexpr int kK1TEpiBars = 2 * kK1TSlots + 2;   // K1T mbarriers (tiles, consumed, epilogue), 16-B multiple
 #ifndef TAT_K1T_EMPTY
 #define TAT_K1T_EMPTY 0        // K1T: per-slot consumed barriers instead of a CTA barrier per tile
                                // (measured: K1T 69.7 -> 70.3 us at C3, 93 -> 100 at C5)
@@ -971,11 +972,24 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
   pdl_trigger();
   const int nch = (C.ncols + kK1BoxP - 1) / kK1BoxP;
   uint64_t* ebar = bar + kK1TSlots;   // per-slot "consumed" barriers (arrival count T)
+  uint64_t* pbar = bar + 2 * kK1TSlots;   // the staged epilogue inputs
+  // fused update epilogue (tat_adjoint_step): the CTA's 4 rows of f (and of the roi mask) are
+  // brought in by bulk copies at the start instead of being loaded at the store
+  // (measured at C3: K1T with the update 111 -> 65 us; the NNLS loop 44.6 -> 41.1 ms)
+  float* epf = reinterpret_cast<float*>(bar + kK1TEpiBars);
+  float* epr = epf + 4 * n;
+  const bool stage_epi = P.epi_update != 0;
   if (t == 0) {
     for (int q = 0; q < kK1TSlots; ++q) ac::mbar_init(&bar[q], 1);
     if (TAT_K1T_EMPTY)
       for (int q = 0; q < kK1TSlots; ++q) ac::mbar_init(&ebar[q], G::T);
+    ac::mbar_init(pbar, 1);
     ac::fence_mbar_init();
+    if (stage_epi) {
+      ac::mbar_expect_tx(pbar, (P.epi_roi ? 32 : 16) * n);
+      ac::bulk_g2s(epf, fout + ((size_t)b * n + y0) * n, 16 * n, pbar);
+      if (P.epi_roi) ac::bulk_g2s(epr, P.epi_roi + (size_t)y0 * n, 16 * n, pbar);
+    }
     for (int c = 0; c < kK1TSlots && c < nch; ++c) {
       ac::mbar_expect_tx(&bar[c], kK1BoxP * 32);
       ac::tma_load_3d(stg + c * kK1BoxP * 4, &tm, y0, c * kK1BoxP, b, &bar[c]);
@@ -1025,6 +1039,8 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
   stage_b<G, 1>(W0, t);
   stage_b<G, 1>(W1, t);
   __syncthreads();
+  const bool active = !P.epi_active || __ldg(&P.epi_active[b]);
+  if (stage_epi) ac::mbar_wait(pbar, 0);
 #pragma unroll 1
   for (int pr = 0; pr < 2; ++pr) {
     float2* W = pr ? W1 : W0;
@@ -1035,8 +1051,14 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
     const int oxy = (y0 + 2 * pr) * n;
     for (int xx = t; xx < n; xx += G::T) {
       const float2 z = residue_sum<G>(W, xx);
-      epi_adj_store<VAR>(P, fout, o + xx, oxy + xx, z.x);
-      epi_adj_store<VAR>(P, fout, o + n + xx, oxy + n + xx, z.y);
+      if (stage_epi) {
+        const int r0 = 2 * pr * n + xx, r1 = r0 + n;
+        epi_adj_store_pre<VAR>(P, fout, o + xx, oxy + xx, z.x, epf[r0], P.epi_roi ? epr[r0] : 1.f, active);
+        epi_adj_store_pre<VAR>(P, fout, o + n + xx, oxy + n + xx, z.y, epf[r1], P.epi_roi ? epr[r1] : 1.f, active);
+      } else {
+        epi_adj_store<VAR>(P, fout, o + xx, oxy + xx, z.x);
+        epi_adj_store<VAR>(P, fout, o + n + xx, oxy + n + xx, z.y);
+      }
     }
   }
 }
@@ -1287,8 +1309,8 @@ size_t smem_k1c(const Consts& C) {
   return (size_t)2 * (col_R(C.n) * 8) * (C.n / col_R(C.n) + TAT_K1_PAD) * 8 +
          (size_t)std::max(kK1Slots * kK1BoxP * 4, 2 * C.n) * 8 + 64;
 }
-size_t smem_k1c_adj(const Consts& C) {
-  return (size_t)2 * 8 * C.n * 8 + (size_t)kK1TSlots * kK1BoxP * 32 + 128;
+size_t smem_k1c_adj(const Consts& C, bool epi) {
+  return (size_t)2 * 8 * C.n * 8 + (size_t)kK1TSlots * kK1BoxP * 32 + 8 * kK1TEpiBars + (epi ? (size_t)32 * C.n : 0);
 }
 
 template <int n>
@@ -1364,8 +1386,8 @@ static cudaError_t launch_k1c_n(const DevPlan& P, const CUtensorMap& tm, const f
     if (P.deapod) return launch_pdl(C.pdl, k1c_fwd<n, true>, grid, blk, smem_k1c(C), s, P, tm, f);
     return launch_pdl(C.pdl, k1c_fwd<n, false>, grid, blk, smem_k1c(C), s, P, tm, f);
   }
-  if (P.deapod || P.lowk_add) return launch_pdl(C.pdl, k1c_adj<n, true>, grid, blk, smem_k1c_adj(C), s, P, tm, fo);
-  return launch_pdl(C.pdl, k1c_adj<n, false>, grid, blk, smem_k1c_adj(C), s, P, tm, fo);
+  if (P.deapod || P.lowk_add) return launch_pdl(C.pdl, k1c_adj<n, true>, grid, blk, smem_k1c_adj(C, P.epi_update != 0), s, P, tm, fo);
+  return launch_pdl(C.pdl, k1c_adj<n, false>, grid, blk, smem_k1c_adj(C, P.epi_update != 0), s, P, tm, fo);
 }
 
 cudaError_t launch_k1c_fwd(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s) {

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(512) k3t_ring(DevPlan P) {
 
 // ------------------------------------------------------------------ K5
 // transform g carries time samples t0 + 2g (real part) and t0 + 2g + 1 (imaginary part)
-template <int nf, bool VAR>
+template <int nf, bool VAR, bool SUB>
 __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ gout) {
   extern __shared__ float2 sm[];
   constexpr int G = ring_G<nf>();
@@ -192,6 +192,16 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
   float2* A = sm;
   float2* B = sm + G * rs;
   const float2* S4 = P.S4 + (size_t)b * C.Kp * n_t;
+  const int tt_n = min(2 * G, n_t - t0);
+  // fused residual (A x - g_obs): this thread's first detector's g_obs samples, loaded before
+  // the dependency wait (g_obs is an input of the whole chain)
+  const bool pre = SUB && (int)threadIdx.x < n_det;   // SUB: launched for plans with epi_sub
+  float es[2 * G];
+  if (pre) {
+    const float* sb = P.epi_sub + ((size_t)b * n_t + t0) * n_det + threadIdx.x;
+#pragma unroll
+    for (int tt = 0; tt < 2 * G; ++tt) es[tt] = tt < tt_n ? __ldg(&sb[(size_t)tt * n_det]) : 0.f;
+  }
   pdl_wait();
   pdl_trigger();
   float2 w0[NIN], w1[NIN];
@@ -219,11 +229,22 @@ __global__ void __launch_bounds__(512) k5_ring(DevPlan P, float* __restrict__ go
     }
   }
   const float2* X = TAT_RING_FFT(nf, 1);
-  const int tt_n = min(2 * G, n_t - t0);
   // detector-major loop (no integer division): thread d restricts all 2G samples of detector d
   for (int d = threadIdx.x; d < n_det; d += blockDim.x) {
     const int pos = phys(__ldg(&P.ring[d]));
     const size_t i0 = ((size_t)b * n_t + t0) * n_det + d;
+    if (pre && d == (int)threadIdx.x) {
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        if (2 * gg < tt_n) {
+          const float2 z = X[gg * rs + pos];
+          const size_t i = i0 + (size_t)(2 * gg) * n_det;
+          gout[i] = epi_fwd_pre<VAR>(P, i, z.x, es[2 * gg]);
+          if (2 * gg + 1 < tt_n) gout[i + n_det] = epi_fwd_pre<VAR>(P, i + n_det, z.y, es[2 * gg + 1]);
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {   // transform gg: samples 2 gg (real part), 2 gg + 1 (imag)
       if (2 * gg < tt_n) {
@@ -313,8 +334,10 @@ cudaError_t configure_ring_kernels(const Consts& C) {
   TAT_RING_SWITCH({
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k3_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k3t_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k5_ring<NF, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k5t_ring<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   });
   if (e == cudaSuccess) e = configure_ring2_kernels(C);
@@ -350,10 +373,13 @@ cudaError_t launch_k5(const DevPlan& P, float* g, cudaStream_t s) {
   const size_t sm = smem_ring_fast(C);
   TAT_RING_SWITCH({
     constexpr int G = ring_G<NF>();
+    const dim3 grid((C.n_t + 2 * G - 1) / (2 * G), C.batch), blk(G * NF / 8);
     if (P.lowk_add)
-      e = launch_pdl(C.pdl, k5_ring<NF, true>, dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), dim3(G * NF / 8), sm, s, P, g);
+      e = P.epi_sub ? launch_pdl(C.pdl, k5_ring<NF, true, true>, grid, blk, sm, s, P, g)
+                    : launch_pdl(C.pdl, k5_ring<NF, true, false>, grid, blk, sm, s, P, g);
     else
-      e = launch_pdl(C.pdl, k5_ring<NF, false>, dim3((C.n_t + 2 * G - 1) / (2 * G), C.batch), dim3(G * NF / 8), sm, s, P, g);
+      e = P.epi_sub ? launch_pdl(C.pdl, k5_ring<NF, false, true>, grid, blk, sm, s, P, g)
+                    : launch_pdl(C.pdl, k5_ring<NF, false, false>, grid, blk, sm, s, P, g);
   });
   return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -233,6 +233,12 @@ cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, 
 
 // forward epilogue: value at flat output index i of g
 // VAR = false: the kernel was instantiated for plans without the G25 / G26 variants
+// as epi_fwd with epi_sub[i] already loaded (sub; 0 when there is no subtraction)
+template <bool VAR = true>
+__device__ __forceinline__ float epi_fwd_pre(const DevPlan& P, size_t i, float v, float sub) {
+  if (VAR && P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n_t * P.C.n_det)];
+  return v * P.epi_scale - sub;
+}
 template <bool VAR = true>
 __device__ __forceinline__ float epi_fwd(const DevPlan& P, size_t i, float v) {
   if (VAR && P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n_t * P.C.n_det)];
@@ -240,6 +246,18 @@ __device__ __forceinline__ float epi_fwd(const DevPlan& P, size_t i, float v) {
   return P.epi_sub ? v - __ldg(&P.epi_sub[i]) : v;
 }
 // adjoint epilogue: store value v of A* g at flat index i of f (pixel ixy = i mod n^2)
+// as epi_adj_store with the update's inputs already at hand: fold = f[i], roi = epi_roi[ixy]
+// (staged in shared memory by the caller); `active` = epi_active of the image
+template <bool VAR = true>
+__device__ __forceinline__ void epi_adj_store_pre(const DevPlan& P, float* f, size_t i, int ixy, float v,
+                                                  float fold, float roi, bool active) {
+  if (VAR && P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n * P.C.n)];
+  if (VAR && P.deapod) v *= P.deapod[ixy % P.C.n] * P.deapod[ixy / P.C.n];
+  if (!active) return;
+  float o = fold - P.epi_tau * v;
+  if (P.epi_update == 2) o = fmaxf(o, 0.f);
+  f[i] = o * roi;
+}
 template <bool VAR = true>
 __device__ __forceinline__ void epi_adj_store(const DevPlan& P, float* f, size_t i, int ixy, float v) {
   if (VAR && P.lowk_add) v += P.lowk_add[i / ((size_t)P.C.n * P.C.n)];
