@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(kSumfT) k2t_sumf(DevPlan P) {
 #ifndef TAT_STRIP_SLOTS
 #define TAT_STRIP_SLOTS 2   // measured at C3: 2 -> K2Ta 54.7 us, 3 -> 57.8, 4 -> 65.7
 #endif
-constexpr int kStripT = 256, kStripKR = 10;
+constexpr int kStripT = 256, kStripKR = (kStripTargets + kStripT - 1) / kStripT;   // 10
 constexpr int kStripSlots = TAT_STRIP_SLOTS;   // node-window buffers (windows in flight + 1)
 __global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
   constexpr int T = kStripT, KR = kStripKR, NW = T / 32;

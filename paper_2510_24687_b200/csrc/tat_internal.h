@@ -107,8 +107,14 @@ struct HostTables {
   int k2s_nheavy = 0;               // heavy strips, placed first (one image per CTA)
   int k2s_ovcap = 0;                // smem budget for a light strip's overflow lists (bytes)
 };
-constexpr int kStripNodes = 4096;   // k2t_strip: node-window budget of a strip
-constexpr int kStripTargets = 2560; // ... and its target budget
+#ifndef TAT_STRIP_NODES
+#define TAT_STRIP_NODES 4096
+#endif
+#ifndef TAT_STRIP_TARGETS
+#define TAT_STRIP_TARGETS 2560
+#endif
+constexpr int kStripNodes = TAT_STRIP_NODES;     // k2t_strip: node-window budget of a strip
+constexpr int kStripTargets = TAT_STRIP_TARGETS; // ... and its target budget (<= 256 KR)
 // ... and for its overflow lists (descriptors + entries, staged in smem); measured at C3 / C5:
 // 8 KB -> K2Ta 93 / 142 us, 16 KB -> 65.5 / 93, 24 KB -> 68.6 / 81 (fewer heavy strips vs
 // occupancy)
