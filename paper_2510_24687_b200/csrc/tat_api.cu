@@ -241,8 +241,13 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
       P.C.pdl = pdl ? atoi(pdl) : 1;
       const char* sf = getenv("TAT_STRIP_FWD");   // tuning switches: columns per CTA of K2 / K2Tb
       const char* sa = getenv("TAT_STRIP_ADJ");
-      if (sf) P.C.col_strip = std::max(2, atoi(sf));
-      if (sa) P.C.col_strip_adj = std::max(1, atoi(sa));    }
+      // small problems (few columns x images): narrower strips so that the column kernels still
+      // have ~4 CTAs per SM (measured at C2, n = 256, batch 1: strips 16 -> 2 take the step from
+      // 98 to 59 us); large ones keep 16 (the halo column of K2 costs 1/strip)
+      const int auto_strip = std::max(2, std::min(16, (int)((long)C.ncols * C.batch / (4 * 148))));
+      P.C.col_strip = sf ? std::max(2, atoi(sf)) : auto_strip;
+      P.C.col_strip_adj = sa ? std::max(1, atoi(sa)) : auto_strip;
+    }
     if ((size_t)P.C.k2t_win * 8 > 227 * 1024) {
       e = cudaErrorInvalidConfiguration;
       break;
