@@ -20,7 +20,7 @@ namespace tat {
 
 using namespace fe;
 
-constexpr int kStrip = 16;   // K2/K2T: columns per CTA (K2: sliding window, one halo column)
+// K2 / K2T columns per CTA: C.col_strip / C.col_strip_adj (K2: sliding window, one halo column)
 
 // Per-residue-group barrier: a group is the n/8 threads of one residue transform.
 template <int n>
@@ -81,7 +81,7 @@ __device__ __forceinline__ int fidx(int q, int L1, int lg, int rs) {   // F[q] i
 }
 
 // ================================================================== K2 forward
-// Strip of kStrip columns with a sliding window of two column spectra.  The next column is
+// Strip of C.col_strip columns with a sliding window of two column spectra.  The next column is
 // fetched with a 1-D TMA bulk copy into a double buffer while the current one is transformed;
 // the first node record of each gather is prefetched into registers before the transform.
 template <int n>
@@ -91,8 +91,8 @@ __global__ void __launch_bounds__(1024) k2_fwd(DevPlan P) {
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs, N1 = C.N - 1;
   const int b = C.b0 + blockIdx.y;
-  const int P0 = blockIdx.x * kStrip;
-  const int Pend = min(P0 + kStrip, C.ncols);
+  const int P0 = blockIdx.x * C.col_strip;
+  const int Pend = min(P0 + C.col_strip, C.ncols);
   const int plast = min(Pend, C.ncols - 1);
   const int g = threadIdx.x / (n / 8), j = threadIdx.x & (n / 8 - 1);
   const int so = g * rs;
@@ -327,8 +327,8 @@ __global__ void __launch_bounds__(1024) k2t_adj(DevPlan P) {
   const Consts& C = P.C;
   const int L = C.Lres, L1 = L - 1, lg = C.log2L, ln = L * rs;
   const int b = C.b0 + blockIdx.y;
-  const int P0 = blockIdx.x * kStrip;
-  const int Pend = min(P0 + kStrip, C.ncols);
+  const int P0 = blockIdx.x * C.col_strip_adj;
+  const int Pend = min(P0 + C.col_strip_adj, C.ncols);
   const int g = threadIdx.x / (n / 8), j = threadIdx.x & (n / 8 - 1);
   const int so = g * rs;
   float2 post[8];
@@ -529,14 +529,14 @@ cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, c
 cudaError_t launch_k2(const DevPlan& P, cudaStream_t s) {
   const Consts& C = P.C;
   if (col_ok(C)) return launch_k2c_fwd(P, s);
-  const dim3 grid((C.ncols + kStrip - 1) / kStrip, C.batch);
+  const dim3 grid((C.ncols + C.col_strip - 1) / C.col_strip, C.batch);
   TAT_DISPATCH_N(k2_fwd<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P));
   return cudaGetLastError();
 }
 cudaError_t launch_k2tb(const DevPlan& P, cudaStream_t s) {   // K2Tb only (targets in Rc)
   const Consts& C = P.C;
   if (col_ok(C)) return launch_k2c_adj(P, s);
-  const dim3 grid((C.ncols + kStrip - 1) / kStrip, C.batch);
+  const dim3 grid((C.ncols + C.col_strip_adj - 1) / C.col_strip_adj, C.batch);
   TAT_DISPATCH_N(k2t_adj<NN><<<grid, fft_threads(C), smem_k2t(C), s>>>(P));
   return cudaGetLastError();
 }
@@ -552,7 +552,7 @@ cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s, cudaEvent_t mid) {
   if (e != cudaSuccess) return e;
   if (mid) cudaEventRecord(mid, s);
   if (col_ok(C)) return launch_k2c_adj(P, s);
-  const dim3 grid((C.ncols + kStrip - 1) / kStrip, C.batch);
+  const dim3 grid((C.ncols + C.col_strip_adj - 1) / C.col_strip_adj, C.batch);
   TAT_DISPATCH_N(k2t_adj<NN><<<grid, fft_threads(C), smem_k2t(C), s>>>(P));
   return cudaGetLastError();
 }
