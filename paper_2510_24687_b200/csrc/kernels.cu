@@ -301,7 +301,7 @@ cudaError_t launch_forward(const DevPlan& P, const CUtensorMap& tm, const float*
   e = launch_k1(P, tm, f, s);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
-  e = launch_k2(P, s);
+  e = launch_k2(P, tm, s);
   if (e != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[2], s);
   if (ring_fast_ok(C)) e = launch_k3(P, s);

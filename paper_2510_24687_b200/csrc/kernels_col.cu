@@ -179,6 +179,12 @@ __device__ __forceinline__ float2 residue_sum(const float2* W, int y) {
   return s;
 }
 
+// S1 of the two-stage engine is blocked [B][n/4][ncols][4 y]: the 4 rows y of one quad at one p
+// are 32 contiguous bytes, so K1's output (and K1T's input) for a quad of rows is one contiguous
+// range, while a column p (K2's input, K2Tb's output) is n/4 pieces of 32 bytes
+__device__ __forceinline__ size_t s1b(const Consts& C, int b, int y, int p) {
+  return (((size_t)b * (C.n / 4) + (y >> 2)) * C.ncols + p) * 4 + (y & 3);
+}
 // ================================================================== forward
 #ifndef TAT_K2_3BUF
 #define TAT_K2_3BUF 0   // three column buffers at every n (default: only where occupancy is 1 anyway)
@@ -188,7 +194,8 @@ __device__ __forceinline__ float2 residue_sum(const float2* W, int y) {
 // n = 512 it costs the third resident CTA (C3 K2 229 -> 252 us), so two buffers there.
 __host__ __device__ constexpr int k2_bufs(int n) { return (TAT_K2_3BUF || n >= 1024) ? 3 : 2; }
 template <int n>
-__global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : (TAT_K2_3BUF ? 2 : 3)) k2c_fwd(DevPlan P) {
+__global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : (TAT_K2_3BUF ? 2 : 3))
+    k2c_fwd(DevPlan P, const __grid_constant__ CUtensorMap tm) {
   constexpr int kK2Bufs = k2_bufs(n);
   using G = ColGeo<n>;
   constexpr int R = G::R, J = G::J, NRES = G::NRES;
@@ -207,16 +214,16 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : (TAT_K2_3BUF ? 2
   float2 A[NRES][R];
   PowR<G::R, kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
-  const float2* S1 = P.S1 + (size_t)b * C.ncols * n;
   float2* S2 = P.S2 + (size_t)b * C.half * C.NL;
   pdl_wait();
   pdl_trigger();
+  // column p of the blocked S1 (s1b): one TMA box of n/4 pieces of 32 bytes, in y order
   if (t == 0) {
     ac::mbar_init(&bar[0], 1);
     ac::mbar_init(&bar[1], 1);
     ac::fence_mbar_init();
     ac::mbar_expect_tx(&bar[0], n * 8);
-    ac::bulk_g2s(xbuf, S1 + (size_t)P0 * n, n * 8, &bar[0]);
+    ac::tma_load_4d(xbuf, &tm, 0, P0, 0, b, &bar[0]);
   }
   __syncthreads();
   float2* Fprev = Fb;
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : (TAT_K2_3BUF ? 2
     if (t == 0 && p < plast) {
       ac::fence_proxy_async();
       ac::mbar_expect_tx(&bar[slot ^ 1], n * 8);
-      ac::bulk_g2s(xbuf + (slot ^ 1) * n, S1 + (size_t)(p + 1) * n, n * 8, &bar[slot ^ 1]);
+      ac::tma_load_4d(xbuf + (slot ^ 1) * n, &tm, 0, p + 1, 0, b, &bar[slot ^ 1]);
     }
     ac::mbar_wait(&bar[slot], (it >> 1) & 1);
     {   // stage A
@@ -311,7 +318,6 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPl
   PowR<G::R, kFactPow> pw;
   col_twiddles<G>(P.tw_col, P.tw_n, n / 2, j, sg, A, pw);
   const float2* Rc = P.Rc + (size_t)b * C.ntpad;
-  float2* out = P.S1 + (size_t)b * C.ncols * n;
   auto issue = [&](int p, int slot) {   // thread 0: bulk copy of column p's targets
     const int s0 = __ldg(&P.k2t_colptr[p]) & ~1;
     const int s1 = (__ldg(&P.k2t_colptr[p + 1]) + 1) & ~1;
@@ -376,7 +382,10 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPl
     float2 acc[R];
     stage_a_adj<G>(Wb, A, pw, j, sg, acc);
     residue_reduce<G>(Wb, acc, j, sg);
-    for (int y = t; y < n; y += G::T) out[(size_t)p * n + y] = residue_sum<G>(Wb, y);
+    // the column into the blocked S1 (s1b): a warp's 32 consecutive y are 8 pieces of 32 bytes
+    // (measured: staged in shared memory and stored as one TMA box instead, K2Tb 218 -> 219 us at
+    // C3, 219 -> 232 at C4)
+    for (int y = t; y < n; y += G::T) P.S1[s1b(C, b, y, p)] = residue_sum<G>(Wb, y);
     __syncthreads();   // Wb free; rbuf[slot] consumed
     m = m_next;
     base = base_next;
@@ -549,8 +558,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adjf(DevP
     float2 acc[R];
     stage_a_adj<G>(Wb, A, pw, j, sg, acc);
     residue_reduce<G>(Wb, acc, j, sg);
-    float2* out = P.S1 + ((size_t)b * C.ncols + p) * n;
-    for (int y = t; y < n; y += T) out[y] = residue_sum<G>(Wb, y);
+    for (int y = t; y < n; y += T) P.S1[s1b(C, b, y, p)] = residue_sum<G>(Wb, y);
     __syncthreads();   // Wb free; win[slot] consumed
   }
 }
@@ -855,16 +863,12 @@ cudaError_t launch_k2t_sumf(const DevPlan& P, cudaStream_t s) {
 // ================================================================== K1 forward (row pairs)
 // z = f_y + i f_{y+1}; Z[p] = sum_x z[x] W_N^{p (x - n/2)} (Alg. 1 steps 1-2, the zero-extended
 // row DFT); S1[b][p][y] = (Z[p] + conj Z[-p]) / 2, S1[b][p][y+1] = (Z[p] - conj Z[-p]) / (2i)
-// for p in [0, N/2].  One CTA (128 threads) per two row pairs (rows y0..y0+3); the [p][4 y]
-// output tiles are transposed into S1 by TMA tensor stores (32-byte rows per p).
-constexpr int kK1BoxP = 128;   // p extent of one S1 tile (= C.s1boxP on this path)
+// for p in [0, N/2].  One CTA (128 threads) per two row pairs (rows y0..y0+3), whose outputs
+// are one contiguous range of the blocked S1 (s1b: 32 bytes per p), stored by the threads.
+constexpr int kK1BoxP = 128;   // p extent of one K1T input chunk
 #ifndef TAT_K1_PAD
 #define TAT_K1_PAD 1           // K1 column buffers: padded rows (1) or XOR swizzle (0)
 #endif
-#ifndef TAT_K1_SLOTS
-#define TAT_K1_SLOTS 2         // K1 output tiles in flight
-#endif
-constexpr int kK1Slots = TAT_K1_SLOTS;
 constexpr int kK1TSlots = 8;   // K1T: S~1 tiles in flight (TMA loads issued ahead)
 constexpr int kK1TEpiBars = 2 * kK1TSlots + 2;   // K1T mbarriers (tiles, consumed, epilogue), 16-B multiple
 #ifndef TAT_K1T_EMPTY
@@ -882,9 +886,9 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPl
   const int b = C.b0 + blockIdx.y, y0 = 4 * blockIdx.x, N = C.N;
   float2* W0 = sm;
   float2* W1 = sm + G::WS;
-  // kK1Slots tiles [kK1BoxP][4]; at the start the 4 input rows (2n float2)
+  // the 4 input rows (2n float2)
   float2* stg = sm + 2 * G::WS;
-  constexpr int STG = (kK1Slots * kK1BoxP * 4 > 2 * n) ? kK1Slots * kK1BoxP * 4 : 2 * n;
+  constexpr int STG = 2 * n;
   uint64_t* bar = reinterpret_cast<uint64_t*>(stg + STG);
   const float* rows = reinterpret_cast<const float*>(stg);
   float2 A[G::NRES][G::R];
@@ -921,38 +925,25 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPl
   stage_b<G, -1>(W0, t);
   stage_b<G, -1>(W1, t);
   __syncthreads();
-  const int nch = (C.ncols + kK1BoxP - 1) / kK1BoxP;
-  // (measured: per-thread 16-byte stores of the row segments instead of TMA tile stores: K1
-  // 52 -> 74 us at C3)
-  for (int c = 0; c < nch; ++c) {
-    float4* tile = reinterpret_cast<float4*>(stg + (c % kK1Slots) * kK1BoxP * 4);
-    if (c >= kK1Slots) {   // the store issued from this slot kK1Slots chunks ago has read its tile
-      if (t == 0) ac::bulk_wait_read<kK1Slots - 1>();
-      __syncthreads();
-    }
-    const int p = c * kK1BoxP + t;
-    if (t < kK1BoxP && p < C.ncols) {
-      const int ia = G::fq(p), im = G::fq((N - p) & (N - 1));
-      const float2 za = W0[ia], zm = W0[im], zb = W1[ia], zn = W1[im];
-      tile[2 * t] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y), 0.5f * (za.y + zm.y),
-                                -0.5f * (za.x - zm.x));
-      tile[2 * t + 1] = make_float4(0.5f * (zb.x + zn.x), 0.5f * (zb.y - zn.y), 0.5f * (zb.y + zn.y),
-                                    -0.5f * (zb.x - zn.x));
-    }
-    ac::fence_proxy_async();
-    __syncthreads();
-    if (t == 0) {
-      ac::tma_store_3d(&tm, tile, y0, c * kK1BoxP, b);
-      ac::bulk_commit();
-    }
+  // S1 blocked (s1b): the quad of rows y0..y0+3 is one contiguous run of ncols x 32 bytes, stored
+  // by consecutive threads (consecutive p) with 16-byte stores.  (Measured at C3: K1 52 -> 43.5 us
+  // against the column-major S1 written by TMA tile stores through a 2-slot staging ring.)
+  float4* dst = reinterpret_cast<float4*>(P.S1 + s1b(C, b, y0, 0));
+  for (int p = t; p < C.ncols; p += G::T) {
+    const int ia = G::fq(p), im = G::fq((N - p) & (N - 1));
+    const float2 za = W0[ia], zm = W0[im], zb = W1[ia], zn = W1[im];
+    dst[2 * p] = make_float4(0.5f * (za.x + zm.x), 0.5f * (za.y - zm.y), 0.5f * (za.y + zm.y),
+                             -0.5f * (za.x - zm.x));
+    dst[2 * p + 1] = make_float4(0.5f * (zb.x + zn.x), 0.5f * (zb.y - zn.y), 0.5f * (zb.y + zn.y),
+                                 -0.5f * (zb.x - zn.x));
   }
-  if (t == 0) ac::bulk_wait_all();
 }
 
 // ================================================================== K1T (transpose of K1)
 // Z[p] = C_y[p] + i C_{y+1}[p] and Z[-p] = conj C_y[p] + i conj C_{y+1}[p] (Hermitian
 // completion; C[0], C[N/2] -> 2 Re), conjugate transform, f~_y = Re z~, f~_{y+1} = Im z~.
-// Two row pairs per CTA; the [p][4 y] tiles of S~1 arrive by TMA tensor loads.
+// Two row pairs per CTA; the [128 p][4 y] chunks of S~1 (contiguous in the blocked layout s1b)
+// arrive by 1-D bulk copies, kK1TSlots in flight.
 template <int n, bool VAR>
 __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPlan P, const __grid_constant__ CUtensorMap tm,
                                                   float* __restrict__ fout) {
@@ -979,6 +970,13 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
   float* epf = reinterpret_cast<float*>(bar + kK1TEpiBars);
   float* epr = epf + 4 * n;
   const bool stage_epi = P.epi_update != 0;
+  // S~1 blocked (s1b): chunk c (p in [128 c, 128 c + 128)) of the row quad is one contiguous run
+  const float2* s1q = P.S1 + s1b(C, b, y0, 0);
+  auto chunk = [&](int c, int slot) {   // thread 0
+    const uint32_t bytes = (uint32_t)min(kK1BoxP, C.ncols - c * kK1BoxP) * 32;
+    ac::mbar_expect_tx(&bar[slot], bytes);
+    ac::bulk_g2s(stg + slot * kK1BoxP * 4, s1q + (size_t)c * kK1BoxP * 4, bytes, &bar[slot]);
+  };
   if (t == 0) {
     for (int q = 0; q < kK1TSlots; ++q) ac::mbar_init(&bar[q], 1);
     if (TAT_K1T_EMPTY)
@@ -990,10 +988,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
       ac::bulk_g2s(epf, fout + ((size_t)b * n + y0) * n, 16 * n, pbar);
       if (P.epi_roi) ac::bulk_g2s(epr, P.epi_roi + (size_t)y0 * n, 16 * n, pbar);
     }
-    for (int c = 0; c < kK1TSlots && c < nch; ++c) {
-      ac::mbar_expect_tx(&bar[c], kK1BoxP * 32);
-      ac::tma_load_3d(stg + c * kK1BoxP * 4, &tm, y0, c * kK1BoxP, b, &bar[c]);
-    }
+    for (int c = 0; c < kK1TSlots && c < nch; ++c) chunk(c, c);
   }
   __syncthreads();
   for (int c = 0; c < nch; ++c) {
@@ -1022,8 +1017,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
     if (t == 0 && c + kK1TSlots < nch) {
       ac::mbar_wait(&ebar[slot], (c / kK1TSlots) & 1);
       ac::fence_proxy_async();
-      ac::mbar_expect_tx(&bar[slot], kK1BoxP * 32);
-      ac::tma_load_3d(stg + slot * kK1BoxP * 4, &tm, y0, (c + kK1TSlots) * kK1BoxP, b, &bar[slot]);
+      chunk(c + kK1TSlots, slot);
     }
   }
   __syncthreads();   // W0 / W1 complete
@@ -1031,8 +1025,7 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
     __syncthreads();   // tile consumed
     if (t == 0 && c + kK1TSlots < nch) {
       ac::fence_proxy_async();
-      ac::mbar_expect_tx(&bar[slot], kK1BoxP * 32);
-      ac::tma_load_3d(stg + slot * kK1BoxP * 4, &tm, y0, (c + kK1TSlots) * kK1BoxP, b, &bar[slot]);
+      chunk(c + kK1TSlots, slot);
     }
   }
 #endif
@@ -1306,8 +1299,7 @@ size_t smem_k2c_adjf(const Consts& C) {
 }
 
 size_t smem_k1c(const Consts& C) {
-  return (size_t)2 * (col_R(C.n) * 8) * (C.n / col_R(C.n) + TAT_K1_PAD) * 8 +
-         (size_t)std::max(kK1Slots * kK1BoxP * 4, 2 * C.n) * 8 + 64;
+  return (size_t)2 * (col_R(C.n) * 8) * (C.n / col_R(C.n) + TAT_K1_PAD) * 8 + (size_t)2 * C.n * 8 + 64;
 }
 size_t smem_k1c_adj(const Consts& C, bool epi) {
   return (size_t)2 * 8 * C.n * 8 + (size_t)kK1TSlots * kK1BoxP * 32 + 8 * kK1TEpiBars + (epi ? (size_t)32 * C.n : 0);
@@ -1339,14 +1331,14 @@ cudaError_t configure_col_kernels(const Consts& C) {
   return C.n == 1024 ? cfg_col<1024>() : (C.n == 512 ? cfg_col<512>() : cfg_col<256>());
 }
 
-cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s) {
+cudaError_t launch_k2c_fwd(const DevPlan& P, const CUtensorMap& tm, cudaStream_t s) {
   const Consts& C = P.C;
   cudaError_t e = cudaSuccess;
   const dim3 grid((C.ncols + C.col_strip - 1) / C.col_strip, C.batch);
   const dim3 blk(col_T(C.n, 8));
-  if (C.n == 1024) e = launch_pdl(C.pdl, k2c_fwd<1024>, grid, blk, smem_k2c_fwd(C), s, P);
-  else if (C.n == 512) e = launch_pdl(C.pdl, k2c_fwd<512>, grid, blk, smem_k2c_fwd(C), s, P);
-  else e = launch_pdl(C.pdl, k2c_fwd<256>, grid, blk, smem_k2c_fwd(C), s, P);
+  if (C.n == 1024) e = launch_pdl(C.pdl, k2c_fwd<1024>, grid, blk, smem_k2c_fwd(C), s, P, tm);
+  else if (C.n == 512) e = launch_pdl(C.pdl, k2c_fwd<512>, grid, blk, smem_k2c_fwd(C), s, P, tm);
+  else e = launch_pdl(C.pdl, k2c_fwd<256>, grid, blk, smem_k2c_fwd(C), s, P, tm);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

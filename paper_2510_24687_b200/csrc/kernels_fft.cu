@@ -509,6 +509,16 @@ cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out) {
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const Consts& C = P.C;
+  if (col_ok(C)) {   // the two-stage engine's blocked S1 [B][n/4][ncols][4 y]: boxes of one column
+    cuuint64_t d4[4] = {4, (cuuint64_t)C.ncols, (cuuint64_t)C.n / 4, (cuuint64_t)C.batch};
+    cuuint64_t s4[3] = {32, (cuuint64_t)C.ncols * 32, (cuuint64_t)C.ncols * 32 * (C.n / 4)};
+    cuuint32_t b4[4] = {4, 1, (cuuint32_t)C.n / 4, 1};
+    cuuint32_t e4[4] = {1, 1, 1, 1};
+    CUresult r4 = encode(out, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, P.S1, d4, s4, b4, e4,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r4 == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+  }
   cuuint64_t dims[3] = {(cuuint64_t)C.n, (cuuint64_t)C.ncols, (cuuint64_t)C.batch};
   cuuint64_t strides[2] = {(cuuint64_t)C.n * 8, (cuuint64_t)C.ncols * C.n * 8};
   cuuint32_t box[3] = {kS1BoxY, (cuuint32_t)C.s1boxP, 1};
@@ -526,9 +536,9 @@ cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, c
   TAT_DISPATCH_N(k1_fwd<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P, tm, f));
   return cudaGetLastError();
 }
-cudaError_t launch_k2(const DevPlan& P, cudaStream_t s) {
+cudaError_t launch_k2(const DevPlan& P, const CUtensorMap& tm, cudaStream_t s) {
   const Consts& C = P.C;
-  if (col_ok(C)) return launch_k2c_fwd(P, s);
+  if (col_ok(C)) return launch_k2c_fwd(P, tm, s);
   const dim3 grid((C.ncols + C.col_strip - 1) / C.col_strip, C.batch);
   TAT_DISPATCH_N(k2_fwd<NN><<<grid, fft_threads(C), smem_fft4(C), s>>>(P));
   return cudaGetLastError();

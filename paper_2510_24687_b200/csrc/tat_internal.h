@@ -299,7 +299,7 @@ size_t smem_fft4(const Consts& C);
 constexpr int kS1BoxY = 4;
 cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out);
 cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
-cudaError_t launch_k2(const DevPlan& P, cudaStream_t s);
+cudaError_t launch_k2(const DevPlan& P, const CUtensorMap& tm, cudaStream_t s);
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s, cudaEvent_t mid = nullptr);   // target sums + column IDFT
 cudaError_t launch_k2tb(const DevPlan& P, cudaStream_t s);  // column IDFT of the targets in Rc
 cudaError_t launch_k1t(const DevPlan& P, const CUtensorMap& tm, float* f, cudaStream_t s);
@@ -326,7 +326,7 @@ int col_R(int n);   // stage-A points per thread of the two-stage engine (Q0 = c
 size_t smem_k2c_fwd(const Consts& C);
 size_t smem_k2c_adj(const Consts& C);
 cudaError_t configure_col_kernels(const Consts& C);
-cudaError_t launch_k2c_fwd(const DevPlan& P, cudaStream_t s);
+cudaError_t launch_k2c_fwd(const DevPlan& P, const CUtensorMap& tm, cudaStream_t s);
 cudaError_t launch_k2c_adj(const DevPlan& P, cudaStream_t s);
 size_t smem_k2c_adjf(const Consts& C);
 cudaError_t launch_k2c_adjf(const DevPlan& P, cudaStream_t s);
