@@ -179,9 +179,10 @@ __device__ __forceinline__ float2 residue_sum(const float2* W, int y) {
   return s;
 }
 
-// S1 of the two-stage engine is blocked [B][n/4][ncols][4 y]: the 4 rows y of one quad at one p
-// are 32 contiguous bytes, so K1's output (and K1T's input) for a quad of rows is one contiguous
-// range, while a column p (K2's input, K2Tb's output) is n/4 pieces of 32 bytes
+// The forward's S1 in the two-stage engine is blocked [B][n/4][ncols][4 y]: the 4 rows y of one
+// quad at one p are 32 contiguous bytes, so K1's output for a quad of rows is one contiguous
+// range, while a column p (K2's input) is one TMA box of n/4 pieces of 32 bytes.  The adjoint's
+// S~1 (K2Tb -> K1T) stays column-major [B][ncols][n].
 __device__ __forceinline__ size_t s1b(const Consts& C, int b, int y, int p) {
   return (((size_t)b * (C.n / 4) + (y >> 2)) * C.ncols + p) * 4 + (y & 3);
 }
@@ -382,10 +383,11 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adj(DevPl
     float2 acc[R];
     stage_a_adj<G>(Wb, A, pw, j, sg, acc);
     residue_reduce<G>(Wb, acc, j, sg);
-    // the column into the blocked S1 (s1b): a warp's 32 consecutive y are 8 pieces of 32 bytes
-    // (measured: staged in shared memory and stored as one TMA box instead, K2Tb 218 -> 219 us at
-    // C3, 219 -> 232 at C4)
-    for (int y = t; y < n; y += G::T) P.S1[s1b(C, b, y, p)] = residue_sum<G>(Wb, y);
+    // the adjoint's S~1 is column-major (coalesced column stores; K1T reads [128 p][4 y] TMA tiles).
+    // (Measured with the forward's blocked layout here: K2Tb 211.5 -> 218 us at C3, 8 pieces of
+    // 32 bytes per warp store; staged and stored as one TMA box: 219.)
+    float2* out = P.S1 + ((size_t)b * C.ncols + p) * n;
+    for (int y = t; y < n; y += G::T) out[y] = residue_sum<G>(Wb, y);
     __syncthreads();   // Wb free; rbuf[slot] consumed
     m = m_next;
     base = base_next;
@@ -558,7 +560,8 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k2c_adjf(DevP
     float2 acc[R];
     stage_a_adj<G>(Wb, A, pw, j, sg, acc);
     residue_reduce<G>(Wb, acc, j, sg);
-    for (int y = t; y < n; y += T) P.S1[s1b(C, b, y, p)] = residue_sum<G>(Wb, y);
+    float2* out = P.S1 + ((size_t)b * C.ncols + p) * n;   // column-major (see k2c_adj)
+    for (int y = t; y < n; y += T) out[y] = residue_sum<G>(Wb, y);
     __syncthreads();   // Wb free; win[slot] consumed
   }
 }
@@ -942,8 +945,8 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_fwd(DevPl
 // ================================================================== K1T (transpose of K1)
 // Z[p] = C_y[p] + i C_{y+1}[p] and Z[-p] = conj C_y[p] + i conj C_{y+1}[p] (Hermitian
 // completion; C[0], C[N/2] -> 2 Re), conjugate transform, f~_y = Re z~, f~_{y+1} = Im z~.
-// Two row pairs per CTA; the [128 p][4 y] chunks of S~1 (contiguous in the blocked layout s1b)
-// arrive by 1-D bulk copies, kK1TSlots in flight.
+// Two row pairs per CTA; the [128 p][4 y] tiles of S~1 (column-major) arrive by TMA tensor loads,
+// kK1TSlots in flight.
 template <int n, bool VAR>
 __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPlan P, const __grid_constant__ CUtensorMap tm,
                                                   float* __restrict__ fout) {
@@ -970,12 +973,11 @@ __global__ void __launch_bounds__(ColGeo<n>::T, n >= 1024 ? 1 : 3) k1c_adj(DevPl
   float* epf = reinterpret_cast<float*>(bar + kK1TEpiBars);
   float* epr = epf + 4 * n;
   const bool stage_epi = P.epi_update != 0;
-  // S~1 blocked (s1b): chunk c (p in [128 c, 128 c + 128)) of the row quad is one contiguous run
-  const float2* s1q = P.S1 + s1b(C, b, y0, 0);
+  // S~1 is column-major [B][ncols][n] (written by K2Tb with coalesced column stores): chunk c is the
+  // [128 p][4 y] TMA tile at (y0, 128 c, b), rows beyond ncols zero-filled
   auto chunk = [&](int c, int slot) {   // thread 0
-    const uint32_t bytes = (uint32_t)min(kK1BoxP, C.ncols - c * kK1BoxP) * 32;
-    ac::mbar_expect_tx(&bar[slot], bytes);
-    ac::bulk_g2s(stg + slot * kK1BoxP * 4, s1q + (size_t)c * kK1BoxP * 4, bytes, &bar[slot]);
+    ac::mbar_expect_tx(&bar[slot], kK1BoxP * 32);
+    ac::tma_load_3d(stg + slot * kK1BoxP * 4, &tm, y0, c * kK1BoxP, b, &bar[slot]);
   };
   if (t == 0) {
     for (int q = 0; q < kK1TSlots; ++q) ac::mbar_init(&bar[q], 1);

@@ -499,7 +499,7 @@ cudaError_t configure_fft_kernels(const Consts& C) {
   return cudaSuccess;
 }
 
-cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out) {
+cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out, bool blocked) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -509,7 +509,7 @@ cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out) {
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const Consts& C = P.C;
-  if (col_ok(C)) {   // the two-stage engine's blocked S1 [B][n/4][ncols][4 y]: boxes of one column
+  if (blocked) {   // the two-stage engine's forward S1 [B][n/4][ncols][4 y]: boxes of one column
     cuuint64_t d4[4] = {4, (cuuint64_t)C.ncols, (cuuint64_t)C.n / 4, (cuuint64_t)C.batch};
     cuuint64_t s4[3] = {32, (cuuint64_t)C.ncols * 32, (cuuint64_t)C.ncols * 32 * (C.n / 4)};
     cuuint32_t b4[4] = {4, 1, (cuuint32_t)C.n / 4, 1};

@@ -19,7 +19,8 @@ using namespace tat;
 // iteration and inverse buffers, profiling slots) is not part of the operator and is `mutable`.
 struct tat_plan {
   DevPlan P;
-  CUtensorMap tm_s1;
+  CUtensorMap tm_s1;    // forward S1 (blocked for the two-stage engine, else column-major)
+  CUtensorMap tm_s1a;   // adjoint S~1 (column-major)
   std::vector<int> ring;
   mutable std::vector<void*> allocs;
   mutable size_t workspace_bytes = 0, table_bytes = 0;
@@ -340,7 +341,8 @@ tat_status tat_plan_create(tat_plan** plan, int n, int n_det, int n_t, double R,
       }
     }
     e = configure_kernels(P);
-    if (e == cudaSuccess) e = make_s1_tensor_map(P, &p->tm_s1);
+    if (e == cudaSuccess) e = make_s1_tensor_map(P, &p->tm_s1, col_ok(P.C));
+    if (e == cudaSuccess) e = make_s1_tensor_map(P, &p->tm_s1a, false);
   } while (false);
   p->table_bytes = tb;
   if (e != cudaSuccess) {
@@ -392,7 +394,7 @@ tat_status tat_adjoint(const tat_plan* plan, const float* g, float* f, cudaStrea
   if (!plan || !f || !g) return fail(TAT_ERR_INVALID_ARGUMENT, "NULL plan or buffer");
   if (!al16(f) || !al16(g)) return fail(TAT_ERR_INVALID_ARGUMENT, "f and g must be 16-byte aligned");
   cudaEvent_t* ev = prof_slot(plan, false);
-  cudaError_t e = launch_adjoint(plan->P, plan->tm_s1, g, f, stream, ev);
+  cudaError_t e = launch_adjoint(plan->P, plan->tm_s1a, g, f, stream, ev);
   if (e != cudaSuccess) return cuda_fail(e, "tat_adjoint launch");
   return TAT_OK;
 }
@@ -529,7 +531,7 @@ tat_status tat_transpose(const tat_plan* plan, const float* g, float* f, cudaStr
   if (!al16(f) || !al16(g)) return fail(TAT_ERR_INVALID_ARGUMENT, "f and g must be 16-byte aligned");
   DevPlan Q = plan->P;
   Q.C.omega = 1.0;   // omega enters only through the K4T multiplier: A^T = A* / omega
-  cudaError_t e = launch_adjoint(Q, plan->tm_s1, g, f, stream, nullptr);
+  cudaError_t e = launch_adjoint(Q, plan->tm_s1a, g, f, stream, nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "tat_transpose launch");
   return TAT_OK;
 }
@@ -681,7 +683,7 @@ tat_status tat_inverse(const tat_plan* plan, const float* g, float* f, double r0
     p->inv_r0 = r0;
     p->inv_annulus = cnt;
   }
-  e = launch_inverse(p->Pinv, p->tm_s1, g, f, stream);
+  e = launch_inverse(p->Pinv, p->tm_s1a, g, f, stream);
   if (e == cudaSuccess) e = launch_k2i_finish(p->Pinv, f, p->inv_region, p->inv_csum, p->inv_annulus, stream);
   if (e != cudaSuccess) return cuda_fail(e, "tat_inverse launch");
   return TAT_OK;
@@ -710,7 +712,7 @@ tat_status tat_adjoint_step(const tat_plan* plan, const float* r, float* f, floa
   Q.epi_update = nonneg ? 2 : 1;
   Q.epi_tau = lambda;
   Q.epi_roi = roi;
-  cudaError_t e = launch_adjoint(Q, plan->tm_s1, r, f, stream, nullptr);
+  cudaError_t e = launch_adjoint(Q, plan->tm_s1a, r, f, stream, nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "tat_adjoint_step launch");
   return TAT_OK;
 }
@@ -772,7 +774,7 @@ tat_status tat_nnls_converge(const tat_plan* plan, const float* g_obs, float* f,
     const bool chk = unset || k % check_every == 0;
     if (chk) e = cudaMemcpyAsync(p->nn_prev, f, (size_t)B * per * sizeof(float), cudaMemcpyDeviceToDevice, stream);
     if (e == cudaSuccess) e = launch_forward(R, p->tm_s1, f, r_work, stream, nullptr);
-    if (e == cudaSuccess) e = launch_adjoint(U, p->tm_s1, r_work, f, stream, nullptr);
+    if (e == cudaSuccess) e = launch_adjoint(U, p->tm_s1a, r_work, f, stream, nullptr);
     if (e != cudaSuccess || !chk) continue;
     e = launch_diff_norms(f, p->nn_prev, B, per, p->nn_part, stream);
     if (e == cudaSuccess) e = cudaMemcpyAsync(part.data(), p->nn_part, part.size() * sizeof(double),
@@ -854,7 +856,7 @@ tat_status tat_power_norm(const tat_plan* plan, int iters, unsigned long long se
     if (!(vv > 0.0)) return fail(TAT_ERR_CUDA, "power iteration collapsed to zero");
     e = launch_scale(v, nimg, (float)(1.0 / std::sqrt(vv)), stream);
     if (e == cudaSuccess) e = launch_forward(p->P, p->tm_s1, v, w, stream, nullptr);
-    if (e == cudaSuccess) e = launch_adjoint(p->P, p->tm_s1, w, u, stream, nullptr);
+    if (e == cudaSuccess) e = launch_adjoint(p->P, p->tm_s1a, w, u, stream, nullptr);
     if (e == cudaSuccess) e = dot_host(p, v, u, nimg, stream, &lam);   // Rayleigh quotient
     std::swap(v, u);
   }

@@ -297,7 +297,7 @@ cudaError_t configure_fft_kernels(const Consts& C);
 size_t smem_fft4(const Consts& C);
 // S1 viewed as a 3-D tensor {n (y), ncols (p), batch} of 8-byte elements; TMA box {4, 256, 1}
 constexpr int kS1BoxY = 4;
-cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out);
+cudaError_t make_s1_tensor_map(const DevPlan& P, CUtensorMap* out, bool blocked);   // forward (blocked) / column-major
 cudaError_t launch_k1(const DevPlan& P, const CUtensorMap& tm, const float* f, cudaStream_t s);
 cudaError_t launch_k2(const DevPlan& P, const CUtensorMap& tm, cudaStream_t s);
 cudaError_t launch_k2t(const DevPlan& P, cudaStream_t s, cudaEvent_t mid = nullptr);   // target sums + column IDFT
