@@ -22,8 +22,12 @@ def _plan(geo, batch):
     return Plan(geo.n, geo.n_det, geo.n_t, geo.R, geo.c, geo.T, batch, geo.angles_array())
 
 
-@pytest.mark.parametrize("name", ["C1", "C2"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5"])
 def test_fused_residual_and_update_epilogues(torch_cuda, name):
+    """The fused epilogues (residual in K5, update + projection + ROI in K1T, their inputs staged
+    early: K5's g_obs before the dependency wait, K1T's x / ROI rows by bulk copies) against the
+    unfused operators, on every engine (C1: first generation; C2 / C3 / C5: two-stage, with the
+    Stockham K5 at n_phi = 512 and the two-stage one elsewhere)."""
     torch = torch_cuda
     geo = synth.geometry(name)
     plan = _plan(geo, 2)
