@@ -382,3 +382,21 @@ def test_ring_engines_agree(torch_cuda, monkeypatch, name):
         torch.cuda.synchronize()
         assert (a - a0).abs().max().item() <= 2e-6 * a0.abs().max().item(), key
         assert (u - u0).abs().max().item() <= 2e-6 * u0.abs().max().item(), key
+
+
+def test_full_ring_at_the_largest_n(torch_cuda):
+    """The largest supported grid with a full detector ring: n = 1024, 1024 detectors (n_phi =
+    1024, every ring position occupied: the two-stage K5T without its zero fill), n_t = 2048,
+    batch 2 (the second image checks the batch stride): A and A* of image 0 against the oracle,
+    the 1e-5 adjoint identity on both images."""
+    import dataclasses
+    geo = dataclasses.replace(synth.geometry("C5"), n_det=1024, batch=2, angles=synth.ring_angles(1024))
+    C = O.derive_geom(geo)
+    plan = _plan(geo)
+    f = np.stack([synth.phantom("C5", b) for b in range(2)])
+    g_gpu = _run(torch_cuda, plan, f=f)
+    _check(g_gpu[0], O.forward(f[0].astype(np.float64), C), "n=1024 full ring A")
+    u_gpu = _run(torch_cuda, plan, g=g_gpu)
+    _check(u_gpu[0], O.adjoint(g_gpu[0].astype(np.float64), C), "n=1024 full ring A*")
+    gr = np.stack([synth.random_data(geo.n_t, geo.n_det, 510 + b) for b in range(2)])
+    _adjoint_identity(torch_cuda, plan, geo, C, f, gr)
