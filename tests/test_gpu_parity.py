@@ -400,3 +400,25 @@ def test_full_ring_at_the_largest_n(torch_cuda):
     _check(u_gpu[0], O.adjoint(g_gpu[0].astype(np.float64), C), "n=1024 full ring A*")
     gr = np.stack([synth.random_data(geo.n_t, geo.n_det, 510 + b) for b in range(2)])
     _adjoint_identity(torch_cuda, plan, geo, C, f, gr)
+
+
+@pytest.mark.parametrize("n,n_det,n_t,batch", [(128, 256, 216, 3), (256, 512, 432, 2), (256, 1024, 486, 1)])
+def test_ring2_ragged_time_tiles(torch_cuda, n, n_det, n_t, batch):
+    """The two-stage ring kernels (n_phi = n_det = 256 / 512 / 1024) with n_t (= 2^a 3^b, as 2M = 6 n_t
+    must be) not a multiple of
+    their 2G time samples per CTA (ragged last K5 / K5T tile) and an odd batch: A and A* of every
+    image against the oracle."""
+    geo = synth.Geometry(n, n_det, n_t, T=2.0, batch=batch, angles=synth.ring_angles(n_det))
+    from paper_2510_24687_b200 import derive
+    info, _, st = derive(n, n_det, n_t, 1.0, 1.0, 2.0, batch, geo.angles_array())
+    if st != 0:
+        pytest.skip(f"geometry unsupported by the kernels (status {st})")
+    C = O.derive_geom(geo)
+    plan = _plan(geo)
+    f = np.stack([synth.phantom("C2", b, n=n) for b in range(batch)])
+    gg = _run(torch_cuda, plan, f=f)
+    gr = np.stack([synth.random_data(n_t, n_det, 40 + b) for b in range(batch)])
+    uu = _run(torch_cuda, plan, g=gr)
+    for b in range(batch):
+        _check(gg[b], O.forward(f[b].astype(np.float64), C), f"A image {b}")
+        _check(uu[b], O.adjoint(gr[b].astype(np.float64), C), f"A* image {b}")
