@@ -404,10 +404,9 @@ def test_full_ring_at_the_largest_n(torch_cuda):
 
 @pytest.mark.parametrize("n,n_det,n_t,batch", [(128, 256, 216, 3), (256, 512, 432, 2), (256, 1024, 486, 1)])
 def test_ring2_ragged_time_tiles(torch_cuda, n, n_det, n_t, batch):
-    """The two-stage ring kernels (n_phi = n_det = 256 / 512 / 1024) with n_t (= 2^a 3^b, as 2M = 6 n_t
-    must be) not a multiple of
-    their 2G time samples per CTA (ragged last K5 / K5T tile) and an odd batch: A and A* of every
-    image against the oracle."""
+    """The two-stage ring kernels (n_phi = n_det = 256 / 512 / 1024) with n_t not a multiple of
+    their 2G time samples per CTA (ragged last K5 / K5T tile; n_t = 2^a 3^b as 2M = 6 n_t must be)
+    and an odd batch: A and A* of every image against the oracle."""
     geo = synth.Geometry(n, n_det, n_t, T=2.0, batch=batch, angles=synth.ring_angles(n_det))
     from paper_2510_24687_b200 import derive
     info, _, st = derive(n, n_det, n_t, 1.0, 1.0, 2.0, batch, geo.angles_array())
