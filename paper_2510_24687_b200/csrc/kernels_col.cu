@@ -872,7 +872,10 @@ constexpr int kK1BoxP = 128;   // p extent of one K1T input chunk
 #ifndef TAT_K1_PAD
 #define TAT_K1_PAD 1           // K1 column buffers: padded rows (1) or XOR swizzle (0)
 #endif
-constexpr int kK1TSlots = 8;   // K1T: S~1 tiles in flight (TMA loads issued ahead)
+#ifndef TAT_K1T_SLOTS
+#define TAT_K1T_SLOTS 8
+#endif
+constexpr int kK1TSlots = TAT_K1T_SLOTS;   // K1T: S~1 tiles in flight (TMA loads issued ahead)
 constexpr int kK1TEpiBars = 2 * kK1TSlots + 2;   // K1T mbarriers (tiles, consumed, epilogue), 16-B multiple
 #ifndef TAT_K1T_EMPTY
 #define TAT_K1T_EMPTY 0        // K1T: per-slot consumed barriers instead of a CTA barrier per tile
