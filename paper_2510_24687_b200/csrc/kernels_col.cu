@@ -709,7 +709,10 @@ __global__ void __launch_bounds__(kSumfT) k2t_sumf(DevPlan P) {
 #endif
 constexpr int kStripT = 256, kStripKR = (kStripTargets + kStripT - 1) / kStripT;   // 10
 constexpr int kStripSlots = TAT_STRIP_SLOTS;   // node-window buffers (windows in flight + 1)
-__global__ void __launch_bounds__(kStripT, 3) k2t_strip(DevPlan P) {
+#ifndef TAT_STRIP_MINB
+#define TAT_STRIP_MINB 3   // (4 CTAs per SM: 64 registers with spills, K2Ta 53.7 -> 67 us at C3)
+#endif
+__global__ void __launch_bounds__(kStripT, TAT_STRIP_MINB) k2t_strip(DevPlan P) {
   constexpr int T = kStripT, KR = kStripKR, NW = T / 32;
   extern __shared__ __align__(128) float2 win[];
   const Consts& C = P.C;
